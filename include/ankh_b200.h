@@ -1,0 +1,143 @@
+/* ankh_b200 -- B200-native (sm_100a) drop-in for the reference's energy call.
+ *
+ * C-ABI of libankh_b200.so.  Plain pointers and sizes only.  Each entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj/core):
+ *
+ *   ankh_fmm_energy_v1   <- ankh::fmm_energy(const ParticleSystem&,
+ *                                            const EwaldConfig&, int threads)
+ *                           include/ankh/fmm.hpp:98-99, src/fmm.cpp:383-436
+ *   ankh_plan_*_v1       <- the same call split into a cached, geometry-only
+ *                           plan (build_m2l_cache fmm.cpp:141-179,
+ *                           build_periodic_operator fmm.cpp:333-377) and a
+ *                           per-system evaluation (fmm.cpp:397-434).  The
+ *                           reference rebuilds the plan on every call.
+ *   ankh_leaf_csr_v1     <- ankh::build_tree, include/ankh/octree.hpp:41,
+ *                           src/octree.cpp:27-45 (bucket contents, bit-exact)
+ *
+ * Data layout is byte-identical to the reference's storage:
+ *   positions : n x 3 doubles  == std::vector<Vec3>            (types.hpp:13-38)
+ *   sources   : n x 10 doubles == std::vector<MultipoleSource> (types.hpp:76-84)
+ *               q, mu_x, mu_y, mu_z, Theta_xx, xy, xz, yy, yz, zz
+ *
+ * Return codes (the C++ wrapper include/ankh_b200.hpp re-throws them as the
+ * reference's exception types; `err` receives the reference's message text):
+ *   0 ANKH_OK
+ *   1 ANKH_INVALID_ARGUMENT  std::invalid_argument (types.cpp:65-79,
+ *                            fmm.cpp:385-388, octree.cpp:28, chebyshev.cpp:86)
+ *   2 ANKH_DOMAIN_ERROR      std::domain_error "pair_interaction: coincident
+ *                            points" (kernel.cpp:161)
+ *   3 ANKH_RUNTIME_ERROR     std::runtime_error (unsupported size / plan misuse)
+ *   4 ANKH_CUDA_ERROR        CUDA / NCCL failure (no reference counterpart)
+ */
+#ifndef ANKH_B200_H
+#define ANKH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ANKH_OK = 0,
+  ANKH_INVALID_ARGUMENT = 1,
+  ANKH_DOMAIN_ERROR = 2,
+  ANKH_RUNTIME_ERROR = 3,
+  ANKH_CUDA_ERROR = 4
+};
+
+/* EwaldConfig (types.hpp:96-104) plus execution fields. */
+typedef struct ankh_config_v1 {
+  double xi;         /* Ewald splitting parameter (default 0.01) */
+  int p;             /* image half-width: 0 open, >= 2 periodic (default 15) */
+  int order_cheb;    /* Chebyshev order L (default 8) */
+  int order_equi;    /* validated, unused by the FMM (types.cpp:73) */
+  int depth;         /* octree depth E; 0 = default_depth(N) */
+  double svd_tol;    /* M2L singular-value cutoff (default 1e-7) */
+  int recip_cutoff;  /* validated, unused (types.cpp:78) */
+  /* ---- extensions (no EwaldConfig counterpart) ---- */
+  int threads;       /* host threads for plan precompute; <= 0 = all cores */
+  int device;        /* CUDA device ordinal; -1 = current */
+  int rank;          /* spatial shard index (multi-GPU), 0 for one GPU */
+  int world;         /* number of shards; 1 for one GPU */
+  int phase_timing;  /* 1 = record per-phase CUDA-event times in the report */
+} ankh_config_v1;
+
+/* EnergyReport (types.hpp:123-135).  With world > 1 the energies are this
+ * shard's partial sums (e_self and e_periodic_far only on rank 0); the caller
+ * all-reduces them. */
+typedef struct ankh_report_v1 {
+  double e_total, e_self, e_near, e_far, e_periodic_far, e_reciprocal;
+  /* wall_times keys of fmm.cpp:409-434, seconds */
+  double t_precompute, t_interpolation, t_far_field, t_near_field, t_periodic_far, t_self,
+      t_total;
+  int depth;         /* tree depth used */
+  int order_cheb;
+  uint64_t near_pairs;      /* unordered P2P pairs evaluated (this shard) */
+  uint64_t far_instances;   /* canonical M2L instances evaluated (this shard) */
+  double far_flops;         /* sum over instances of 4kK + 2k (this shard) */
+  uint32_t gpu_launches;    /* kernels launched by the last evaluation */
+} ankh_report_v1;
+
+typedef struct ankh_plan_v1 ankh_plan_v1;
+
+/* Fill `cfg` with the EwaldConfig defaults (types.hpp:96-104). */
+void ankh_config_default_v1(ankh_config_v1* cfg);
+
+/* Drop-in for ankh::fmm_energy.  Host buffers; host<->device copies inside.
+ * A process-wide plan cache keyed by (n, box_radius, config) makes repeated
+ * calls skip the geometry-only precompute. */
+int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
+                       double box_radius, const ankh_config_v1* cfg, ankh_report_v1* out,
+                       char* err, size_t errlen);
+
+/* Plan for n particles in the box [-box_radius, box_radius]^3 under cfg. */
+int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg,
+                        ankh_plan_v1** plan, char* err, size_t errlen);
+void ankh_plan_destroy_v1(ankh_plan_v1* plan);
+
+/* Evaluate with HOST input buffers (copied in on the plan's stream). */
+int ankh_plan_energy_v1(ankh_plan_v1* plan, const double* positions, const double* sources,
+                        ankh_report_v1* out, char* err, size_t errlen);
+
+/* Evaluate with DEVICE input buffers (same layouts), on `stream`
+ * (cudaStream_t; NULL = the plan's own stream).  Synchronises before return. */
+int ankh_plan_energy_device_v1(ankh_plan_v1* plan, const double* d_positions,
+                               const double* d_sources, void* stream, ankh_report_v1* out,
+                               char* err, size_t errlen);
+
+/* Enqueue an evaluation without synchronising; results are fetched with
+ * ankh_plan_result_v1.  Used for device-timed loops and CUDA-graph capture. */
+int ankh_plan_enqueue_v1(ankh_plan_v1* plan, const double* d_positions, const double* d_sources,
+                         void* stream, char* err, size_t errlen);
+int ankh_plan_result_v1(ankh_plan_v1* plan, ankh_report_v1* out, char* err, size_t errlen);
+
+/* Plan introspection. */
+int ankh_plan_info_v1(const ankh_plan_v1* plan, int* depth, int* order, size_t* n_cells_leaf,
+                      size_t* m2l_instances, size_t* m2l_operators, double* m2l_rank_mean,
+                      size_t* device_bytes);
+
+/* Per-level expansions (levels 0..depth, lex cell order, K = L^3 per cell)
+ * from the last evaluation, copied to host `out` (count doubles). */
+int ankh_plan_expansions_v1(ankh_plan_v1* plan, double* out, size_t count, char* err,
+                            size_t errlen);
+
+/* Leaf CSR of build_tree: offsets[8^depth + 1] and indices[n] (lex leaves,
+ * ascending particle index inside a leaf), computed on the GPU. */
+int ankh_leaf_csr_v1(size_t n, const double* positions, double box_radius, int depth,
+                     uint32_t* leaf_offsets, uint32_t* indices, char* err, size_t errlen);
+
+/* M2L factors the plan uses for (level, offset): k x K row-major each. */
+int ankh_plan_m2l_factors_v1(ankh_plan_v1* plan, int level, const int* offset, double* lmat,
+                             double* rmat, int max_rank, int* rank, char* err, size_t errlen);
+
+/* Library version string. */
+const char* ankh_version_v1(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ANKH_B200_H */

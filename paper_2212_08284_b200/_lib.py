@@ -1,0 +1,72 @@
+"""Loader for the in-tree sm_100a library (libankh_b200.so).  Fails loudly when
+the library is missing: the product has no CPU fallback."""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libankh_b200.so")
+
+_lib: Optional[ctypes.CDLL] = None
+
+EXPORTS = [
+    "ankh_config_default_v1",
+    "ankh_fmm_energy_v1",
+    "ankh_plan_create_v1",
+    "ankh_plan_destroy_v1",
+    "ankh_plan_energy_v1",
+    "ankh_plan_energy_device_v1",
+    "ankh_plan_enqueue_v1",
+    "ankh_plan_result_v1",
+    "ankh_plan_info_v1",
+    "ankh_plan_expansions_v1",
+    "ankh_leaf_csr_v1",
+    "ankh_plan_m2l_factors_v1",
+    "ankh_version_v1",
+]
+
+
+def build(verbose: bool = False) -> str:
+    """Compile csrc/ into libankh_b200.so (nvcc -gencode arch=compute_100a,code=sm_100a)."""
+    import subprocess
+
+    cmd = ["make", "-j8", "-C", os.path.join(HERE, "csrc")]
+    if not verbose:
+        cmd.insert(1, "-s")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        c_void_p, c_size_t, c_int, c_double = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_double
+        D = ctypes.POINTER(ctypes.c_double)
+        U32 = ctypes.POINTER(ctypes.c_uint32)
+        I = ctypes.POINTER(ctypes.c_int)
+        cp = ctypes.c_char_p
+        L.ankh_config_default_v1.argtypes = [c_void_p]
+        L.ankh_config_default_v1.restype = None
+        L.ankh_fmm_energy_v1.argtypes = [c_size_t, D, D, c_double, c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_plan_create_v1.argtypes = [c_size_t, c_double, c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_plan_destroy_v1.argtypes = [c_void_p]
+        L.ankh_plan_destroy_v1.restype = None
+        L.ankh_plan_energy_v1.argtypes = [c_void_p, D, D, c_void_p, cp, c_size_t]
+        L.ankh_plan_energy_device_v1.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_plan_enqueue_v1.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_plan_result_v1.argtypes = [c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_plan_info_v1.argtypes = [c_void_p] + [c_void_p] * 7
+        L.ankh_plan_expansions_v1.argtypes = [c_void_p, D, c_size_t, cp, c_size_t]
+        L.ankh_leaf_csr_v1.argtypes = [c_size_t, D, c_double, c_int, U32, U32, cp, c_size_t]
+        L.ankh_plan_m2l_factors_v1.argtypes = [c_void_p, c_int, I, D, D, c_int, I, cp, c_size_t]
+        L.ankh_version_v1.argtypes = []
+        L.ankh_version_v1.restype = ctypes.c_char_p
+        _lib = L
+    return _lib

@@ -1,0 +1,359 @@
+"""Python mirror of the reference's energy API over the C-ABI of libankh_b200.so.
+
+Names, fields and error behaviour follow the reference (paths relative to
+/root/reference/proj/core):
+
+* ``EwaldConfig``      <- ``ankh::EwaldConfig``   (include/ankh/types.hpp:96-104)
+* ``ParticleSystem``   <- ``ankh::ParticleSystem`` (types.hpp:88-94)
+* ``EnergyReport``     <- ``ankh::EnergyReport``   (types.hpp:123-135)
+* ``fmm_energy``       <- ``ankh::fmm_energy``     (include/ankh/fmm.hpp:98-99)
+* ``default_depth``    <- ``ankh::default_depth``  (src/types.cpp:9-14)
+* ``build_tree_csr``   <- ``ankh::build_tree``     (src/octree.cpp:27-45), as CSR
+
+Exceptions map the reference's C++ types: ``InvalidArgument`` (a ValueError)
+for std::invalid_argument, ``DomainError`` (an ArithmeticError) for
+std::domain_error, ``AnkhRuntimeError`` for std::runtime_error and
+``CudaError`` for device failures.  There is no CPU fallback: without the
+built library or a GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from ._lib import lib
+
+__all__ = [
+    "EwaldConfig",
+    "ParticleSystem",
+    "EnergyReport",
+    "InvalidArgument",
+    "DomainError",
+    "AnkhRuntimeError",
+    "CudaError",
+    "fmm_energy",
+    "default_depth",
+    "build_tree_csr",
+    "Plan",
+]
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument."""
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error."""
+
+
+class AnkhRuntimeError(RuntimeError):
+    """std::runtime_error."""
+
+
+class CudaError(RuntimeError):
+    """CUDA / NCCL failure (no reference counterpart)."""
+
+
+_ERRORS = {1: InvalidArgument, 2: DomainError, 3: AnkhRuntimeError, 4: CudaError}
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [
+        ("xi", ctypes.c_double),
+        ("p", ctypes.c_int),
+        ("order_cheb", ctypes.c_int),
+        ("order_equi", ctypes.c_int),
+        ("depth", ctypes.c_int),
+        ("svd_tol", ctypes.c_double),
+        ("recip_cutoff", ctypes.c_int),
+        ("threads", ctypes.c_int),
+        ("device", ctypes.c_int),
+        ("rank", ctypes.c_int),
+        ("world", ctypes.c_int),
+        ("phase_timing", ctypes.c_int),
+    ]
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [
+        ("e_total", ctypes.c_double),
+        ("e_self", ctypes.c_double),
+        ("e_near", ctypes.c_double),
+        ("e_far", ctypes.c_double),
+        ("e_periodic_far", ctypes.c_double),
+        ("e_reciprocal", ctypes.c_double),
+        ("t_precompute", ctypes.c_double),
+        ("t_interpolation", ctypes.c_double),
+        ("t_far_field", ctypes.c_double),
+        ("t_near_field", ctypes.c_double),
+        ("t_periodic_far", ctypes.c_double),
+        ("t_self", ctypes.c_double),
+        ("t_total", ctypes.c_double),
+        ("depth", ctypes.c_int),
+        ("order_cheb", ctypes.c_int),
+        ("near_pairs", ctypes.c_uint64),
+        ("far_instances", ctypes.c_uint64),
+        ("far_flops", ctypes.c_double),
+        ("gpu_launches", ctypes.c_uint32),
+    ]
+
+
+@dataclasses.dataclass
+class EwaldConfig:
+    """ankh::EwaldConfig (types.hpp:96-104) with the same defaults."""
+
+    xi: float = 0.01
+    p: int = 15
+    order_cheb: int = 8
+    order_equi: int = 8
+    depth: int = 0
+    svd_tol: float = 1e-7
+    recip_cutoff: int = 12
+
+    def _c(self, threads: int = 0, device: int = -1, rank: int = 0, world: int = 1,
+           phase_timing: bool = True) -> _Config:
+        return _Config(float(self.xi), int(self.p), int(self.order_cheb), int(self.order_equi),
+                       int(self.depth), float(self.svd_tol), int(self.recip_cutoff), int(threads),
+                       int(device), int(rank), int(world), 1 if phase_timing else 0)
+
+
+@dataclasses.dataclass
+class ParticleSystem:
+    """ankh::ParticleSystem: positions N x 3, sources N x 10 (q, mu, Theta xx xy xz yy yz zz)."""
+
+    positions: np.ndarray
+    sources: np.ndarray
+    box_radius: float = 1.0
+
+    def size(self) -> int:
+        return int(np.asarray(self.positions).shape[0])
+
+
+@dataclasses.dataclass
+class EnergyReport:
+    """ankh::EnergyReport (types.hpp:123-135) plus work counters."""
+
+    e_total: float = 0.0
+    e_self: float = 0.0
+    e_near: float = 0.0
+    e_far: float = 0.0
+    e_periodic_far: float = 0.0
+    e_reciprocal: float = 0.0
+    wall_times: Dict[str, float] = dataclasses.field(default_factory=dict)
+    depth: int = 0
+    order_cheb: int = 0
+    near_pairs: int = 0
+    far_instances: int = 0
+    far_flops: float = 0.0
+    gpu_launches: int = 0
+
+    def component_sum(self) -> float:
+        return self.e_self + self.e_near + self.e_far + self.e_periodic_far + self.e_reciprocal
+
+    @staticmethod
+    def _from_c(r: _Report, wall: Optional[float] = None) -> "EnergyReport":
+        times = {
+            "precompute": r.t_precompute,
+            "interpolation": r.t_interpolation,
+            "far_field": r.t_far_field,
+            "near_field": r.t_near_field,
+            "periodic_far": r.t_periodic_far,
+            "self": r.t_self,
+            "total": r.t_total if wall is None else wall,
+        }
+        return EnergyReport(r.e_total, r.e_self, r.e_near, r.e_far, r.e_periodic_far,
+                            r.e_reciprocal, times, r.depth, r.order_cheb, int(r.near_pairs),
+                            int(r.far_instances), float(r.far_flops), int(r.gpu_launches))
+
+
+def _check(code: int, err: ctypes.Array) -> None:
+    if code != 0:
+        raise _ERRORS.get(code, AnkhRuntimeError)(err.value.decode(errors="replace"))
+
+
+def _as_host(a, cols: int) -> np.ndarray:
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if arr.size == 0:
+        return arr.reshape(0, cols)
+    return arr.reshape(-1, cols)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def default_depth(n: int) -> int:
+    """types.cpp:9-14."""
+    if n <= 64:
+        return 1
+    levels = math.log(n / 64.0) / math.log(8.0)
+    return max(1, int(math.ceil(levels - 1e-12)))
+
+
+def fmm_energy(system: ParticleSystem, config: Optional[EwaldConfig] = None,
+               threads: int = 1) -> EnergyReport:
+    """Drop-in for ankh::fmm_energy; host arrays in, energy out (one GPU).
+
+    ``threads`` only sizes the host precompute pool (<= 0: all cores); the
+    geometry-only plan is cached inside the library across calls.
+    """
+    import time
+
+    config = config or EwaldConfig()
+    pos = _as_host(system.positions, 3)
+    src = _as_host(system.sources, 10)
+    if pos.shape[0] != src.shape[0]:
+        raise InvalidArgument("fmm_energy: invalid system: positions and sources must have equal length")
+    rep = _Report()
+    err = ctypes.create_string_buffer(512)
+    t0 = time.perf_counter()
+    code = lib().ankh_fmm_energy_v1(pos.shape[0], _ptr(pos), _ptr(src), float(system.box_radius),
+                                    ctypes.byref(config._c(threads=threads)), ctypes.byref(rep),
+                                    err, 512)
+    wall = time.perf_counter() - t0
+    _check(code, err)
+    return EnergyReport._from_c(rep, wall)
+
+
+def build_tree_csr(positions, box_radius: float, depth: int) -> Tuple[np.ndarray, np.ndarray]:
+    """Leaf buckets of build_tree as CSR (offsets[8^depth+1], indices[N]), on the GPU."""
+    pos = _as_host(positions, 3)
+    n = pos.shape[0]
+    if depth < 1 or depth > 8:
+        raise InvalidArgument("build_tree: depth must be in [1, 8]")
+    offs = np.zeros(8 ** depth + 1, dtype=np.uint32)
+    idx = np.zeros(max(n, 1), dtype=np.uint32)
+    err = ctypes.create_string_buffer(512)
+    code = lib().ankh_leaf_csr_v1(n, _ptr(pos), float(box_radius), int(depth),
+                                  offs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                  idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), err, 512)
+    _check(code, err)
+    return offs, idx[:n]
+
+
+class Plan:
+    """Cached geometry-only precompute (M2L factors, periodic spectrum, buffers)
+    for n particles in [-box_radius, box_radius]^3, evaluated many times.
+
+    ``rank``/``world`` select a spatial shard (Morton leaf range + M2L tiles);
+    the per-shard energies are partial sums for the caller to all-reduce.
+    """
+
+    def __init__(self, n: int, box_radius: float, config: Optional[EwaldConfig] = None,
+                 threads: int = 0, device: int = -1, rank: int = 0, world: int = 1,
+                 phase_timing: bool = True):
+        self.config = config or EwaldConfig()
+        self.n = int(n)
+        self.box_radius = float(box_radius)
+        self._h = ctypes.c_void_p()
+        err = ctypes.create_string_buffer(512)
+        cfg = self.config._c(threads=threads, device=device, rank=rank, world=world,
+                             phase_timing=phase_timing)
+        _check(lib().ankh_plan_create_v1(self.n, self.box_radius, ctypes.byref(cfg),
+                                         ctypes.byref(self._h), err, 512), err)
+
+    def close(self) -> None:
+        if self._h:
+            lib().ankh_plan_destroy_v1(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def energy(self, positions, sources) -> EnergyReport:
+        """Host arrays (copied to HBM on the plan's stream)."""
+        pos = _as_host(positions, 3)
+        src = _as_host(sources, 10)
+        self._check_n(pos, src)
+        rep = _Report()
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_energy_v1(self._h, _ptr(pos), _ptr(src), ctypes.byref(rep), err, 512), err)
+        return EnergyReport._from_c(rep)
+
+    def energy_device(self, positions, sources, stream: int = 0) -> EnergyReport:
+        """Device tensors (torch CUDA float64, contiguous N x 3 / N x 10)."""
+        self._check_dev(positions, sources)
+        rep = _Report()
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_energy_device_v1(
+            self._h, ctypes.c_void_p(positions.data_ptr()), ctypes.c_void_p(sources.data_ptr()),
+            ctypes.c_void_p(stream), ctypes.byref(rep), err, 512), err)
+        return EnergyReport._from_c(rep)
+
+    def enqueue(self, positions, sources, stream: int = 0) -> None:
+        """Queue an evaluation of device tensors without synchronising."""
+        self._check_dev(positions, sources)
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_enqueue_v1(self._h, ctypes.c_void_p(positions.data_ptr()),
+                                          ctypes.c_void_p(sources.data_ptr()),
+                                          ctypes.c_void_p(stream), err, 512), err)
+
+    def result(self) -> EnergyReport:
+        rep = _Report()
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_result_v1(self._h, ctypes.byref(rep), err, 512), err)
+        return EnergyReport._from_c(rep)
+
+    def info(self) -> Dict[str, float]:
+        d, o = ctypes.c_int(), ctypes.c_int()
+        nl, ni, no, nb = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        rm = ctypes.c_double()
+        lib().ankh_plan_info_v1(self._h, ctypes.byref(d), ctypes.byref(o), ctypes.byref(nl),
+                                ctypes.byref(ni), ctypes.byref(no), ctypes.byref(rm), ctypes.byref(nb))
+        return {"depth": d.value, "order": o.value, "leaves": nl.value, "m2l_instances": ni.value,
+                "m2l_operators": no.value, "m2l_rank_mean": rm.value, "device_bytes": nb.value}
+
+    def expansions(self):
+        """Per-level expansions of the last evaluation: list of (8^l, K) arrays."""
+        inf = self.info()
+        depth, L = inf["depth"], inf["order"]
+        K = L ** 3
+        total = sum(8 ** l for l in range(depth + 1)) * K
+        out = np.zeros(total)
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_expansions_v1(self._h, _ptr(out), total, err, 512), err)
+        res, o = [], 0
+        for l in range(depth + 1):
+            cnt = 8 ** l * K
+            res.append(out[o:o + cnt].reshape(8 ** l, K))
+            o += cnt
+        return res
+
+    def m2l_factors(self, level: int, offset) -> Tuple[np.ndarray, np.ndarray]:
+        L = self.info()["order"]
+        K = L ** 3
+        lm = np.zeros(K * K)
+        rm = np.zeros(K * K)
+        rank = ctypes.c_int(0)
+        off = np.asarray(offset, dtype=np.int32)
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_m2l_factors_v1(self._h, int(level),
+                                              off.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                              _ptr(lm), _ptr(rm), K, ctypes.byref(rank), err, 512), err)
+        k = rank.value
+        return lm[: k * K].reshape(k, K), rm[: k * K].reshape(k, K)
+
+    def _check_n(self, pos: np.ndarray, src: np.ndarray) -> None:
+        if pos.shape[0] != self.n or src.shape[0] != self.n:
+            raise InvalidArgument("fmm_energy: invalid system: positions and sources must have equal length")
+
+    def _check_dev(self, positions, sources) -> None:
+        import torch
+
+        for t, c in ((positions, 3), (sources, 10)):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64
+                    and t.is_contiguous() and t.numel() == self.n * c):
+                raise InvalidArgument("device inputs must be contiguous CUDA float64 tensors of shape (n, 3) / (n, 10)")

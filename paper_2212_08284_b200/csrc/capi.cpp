@@ -1,0 +1,211 @@
+// C-ABI of libankh_b200.so (declared in include/ankh_b200.h).
+#include <cstring>
+#include <vector>
+#include <list>
+#include <memory>
+#include <mutex>
+
+#include "plan.hpp"
+
+using ankh_b200::AnkhError;
+using ankh_b200::Plan;
+
+struct ankh_plan_v1 {
+  std::unique_ptr<Plan> plan;
+  std::mutex mu;
+};
+
+namespace {
+
+int set_err(char* err, std::size_t errlen, const char* msg, int code) {
+  if (err && errlen) {
+    std::strncpy(err, msg, errlen - 1);
+    err[errlen - 1] = '\0';
+  }
+  return code;
+}
+
+template <class F>
+int guarded(char* err, std::size_t errlen, F&& f) {
+  try {
+    f();
+    if (err && errlen) err[0] = '\0';
+    return ANKH_OK;
+  } catch (const AnkhError& e) {
+    return set_err(err, errlen, e.what(), e.code);
+  } catch (const std::bad_alloc&) {
+    return set_err(err, errlen, "host allocation failed", ANKH_RUNTIME_ERROR);
+  } catch (const std::exception& e) {
+    return set_err(err, errlen, e.what(), ANKH_RUNTIME_ERROR);
+  }
+}
+
+// Process-wide cache of plans for the one-shot drop-in call: the geometry-only
+// precompute (M2L factors, periodic spectrum, buffers) is reused whenever the
+// particle count, box radius and configuration repeat.
+struct CacheEntry {
+  std::size_t n;
+  double rb;
+  ankh_config_v1 cfg;
+  std::unique_ptr<Plan> plan;
+};
+std::mutex g_cache_mu;
+std::list<CacheEntry> g_cache;
+constexpr std::size_t kCacheMax = 2;
+
+bool same_cfg(const ankh_config_v1& a, const ankh_config_v1& b) {
+  return a.xi == b.xi && a.p == b.p && a.order_cheb == b.order_cheb &&
+         a.order_equi == b.order_equi && a.depth == b.depth && a.svd_tol == b.svd_tol &&
+         a.recip_cutoff == b.recip_cutoff && a.device == b.device && a.rank == b.rank &&
+         a.world == b.world && a.phase_timing == b.phase_timing;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ankh_config_default_v1(ankh_config_v1* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->xi = 0.01;
+  c->p = 15;
+  c->order_cheb = 8;
+  c->order_equi = 8;
+  c->depth = 0;
+  c->svd_tol = 1e-7;
+  c->recip_cutoff = 12;
+  c->threads = 0;
+  c->device = -1;
+  c->rank = 0;
+  c->world = 1;
+  c->phase_timing = 1;
+}
+
+const char* ankh_version_v1(void) { return "ankh_b200 0.1.0 (sm_100a)"; }
+
+int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources, double box_radius,
+                       const ankh_config_v1* cfg, ankh_report_v1* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!cfg || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null config or report");
+    if (n > 0 && (!positions || !sources)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+    ankh_b200::validate_config(*cfg);
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    Plan* plan = nullptr;
+    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+      if (it->n == n && it->rb == box_radius && same_cfg(it->cfg, *cfg)) {
+        g_cache.splice(g_cache.begin(), g_cache, it);
+        plan = g_cache.front().plan.get();
+        break;
+      }
+    }
+    if (!plan) {
+      while (g_cache.size() >= kCacheMax) g_cache.pop_back();
+      auto p = std::make_unique<Plan>(n, box_radius, *cfg);
+      g_cache.push_front({n, box_radius, *cfg, std::move(p)});
+      plan = g_cache.front().plan.get();
+    }
+    plan->enqueue_host(positions, sources, nullptr);
+    plan->result(out);
+  });
+}
+
+int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg, ankh_plan_v1** plan,
+                        char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!cfg || !plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null config or plan pointer");
+    auto h = std::make_unique<ankh_plan_v1>();
+    h->plan = std::make_unique<Plan>(n, box_radius, *cfg);
+    *plan = h.release();
+  });
+}
+
+void ankh_plan_destroy_v1(ankh_plan_v1* plan) { delete plan; }
+
+int ankh_plan_energy_v1(ankh_plan_v1* plan, const double* positions, const double* sources,
+                        ankh_report_v1* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->plan->enqueue_host(positions, sources, nullptr);
+    plan->plan->result(out);
+  });
+}
+
+int ankh_plan_energy_device_v1(ankh_plan_v1* plan, const double* d_positions,
+                               const double* d_sources, void* stream, ankh_report_v1* out,
+                               char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->plan->enqueue(d_positions, d_sources, static_cast<cudaStream_t>(stream));
+    plan->plan->result(out);
+  });
+}
+
+int ankh_plan_enqueue_v1(ankh_plan_v1* plan, const double* d_positions, const double* d_sources,
+                         void* stream, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->plan->enqueue(d_positions, d_sources, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ankh_plan_result_v1(ankh_plan_v1* plan, ankh_report_v1* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->plan->result(out);
+  });
+}
+
+int ankh_plan_info_v1(const ankh_plan_v1* plan, int* depth, int* order, size_t* n_cells_leaf,
+                      size_t* m2l_instances, size_t* m2l_operators, double* m2l_rank_mean,
+                      size_t* device_bytes) {
+  if (!plan) return ANKH_INVALID_ARGUMENT;
+  const Plan& p = *plan->plan;
+  if (depth) *depth = p.depth;
+  if (order) *order = p.L;
+  if (n_cells_leaf) *n_cells_leaf = static_cast<size_t>(p.n_leaves);
+  if (m2l_instances) *m2l_instances = p.m2l_instances;
+  if (m2l_operators) *m2l_operators = p.m2l_operators;
+  if (m2l_rank_mean) *m2l_rank_mean = p.m2l_rank_mean;
+  if (device_bytes) *device_bytes = p.device_bytes;
+  return ANKH_OK;
+}
+
+int ankh_plan_expansions_v1(ankh_plan_v1* plan, double* out, size_t count, char* err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or buffer");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->plan->expansions(out, count);
+  });
+}
+
+int ankh_leaf_csr_v1(size_t n, const double* positions, double box_radius, int depth,
+                     uint32_t* leaf_offsets, uint32_t* indices, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (depth < 1 || depth > 8) throw AnkhError(ANKH_INVALID_ARGUMENT, "build_tree: depth must be in [1, 8]");
+    ankh_config_v1 cfg;
+    ankh_config_default_v1(&cfg);
+    cfg.depth = depth;
+    cfg.order_cheb = 2;
+    cfg.order_equi = 2;
+    cfg.p = 0;
+    cfg.phase_timing = 0;
+    Plan plan(n, box_radius, cfg, /*csr_only=*/true);
+    std::vector<double> zeros(n * 10, 0.0);
+    plan.enqueue_host(positions, zeros.data(), nullptr);
+    plan.leaf_csr(leaf_offsets, indices);  // build_tree does not validate (octree.cpp:27-45)
+  });
+}
+
+int ankh_plan_m2l_factors_v1(ankh_plan_v1* plan, int level, const int* offset, double* lmat,
+                             double* rmat, int max_rank, int* rank, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !offset || !rank) throw AnkhError(ANKH_INVALID_ARGUMENT, "null argument");
+    plan->plan->m2l_factors(level, offset, lmat, rmat, max_rank, rank);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+// Validation, leaf binning, stable sort and gather (sm_100a).
+//
+// Reference: validate_system (types.cpp:16-63), build_tree (octree.cpp:27-45),
+// self_energy (kernel.cpp:206-213).  Binning is bit-exact with the reference:
+// shifted = (x + r_B) * inv_side with inv_side = n / (2 r_B) computed on the
+// host exactly as octree.cpp:35, IEEE round-to-nearest add and multiply (no
+// FMA contraction), floor, clamp to [0, n-1].  The stable LSD radix sort keeps
+// ascending particle index inside each leaf, which is the reference's bucket
+// order.  All of it is HBM-bound (~24+80+8 B read, ~136 B written per atom).
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+
+namespace ankh_b200 {
+
+namespace {
+
+__device__ __forceinline__ int bin_axis(double x, double rb, double inv_side, int n) {
+  const double shifted = __dmul_rn(__dadd_rn(x, rb), inv_side);
+  double f = floor(shifted);
+  f = fmin(fmax(f, 0.0), static_cast<double>(n - 1));
+  return static_cast<int>(f);
+}
+
+__global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
+                                             const double* __restrict__ src, std::size_t n,
+                                             double rb, double inv_side, int nax, double c_mu,
+                                             double c_th, unsigned* __restrict__ keys,
+                                             unsigned* __restrict__ idx,
+                                             unsigned* __restrict__ counts,
+                                             double* __restrict__ self_partial, DevResult* res) {
+  __shared__ double red[8];
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  double acc = 0.0;
+  bool mp = false;
+  if (i < n) {
+    const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+    double s[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) s[k] = src[10 * i + k];
+    bool finite = isfinite(x) && isfinite(y) && isfinite(z);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) finite = finite && isfinite(s[k]);
+    unsigned key = 0;
+    if (!finite) {
+      atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
+    } else {
+      if (fabs(x) > rb || fabs(y) > rb || fabs(z) > rb)
+        atomicMin(&res->min_outside, static_cast<unsigned long long>(i));
+      const int ix = bin_axis(x, rb, inv_side, nax);
+      const int iy = bin_axis(y, rb, inv_side, nax);
+      const int iz = bin_axis(z, rb, inv_side, nax);
+      key = static_cast<unsigned>((ix * nax + iy) * nax + iz);
+      // self_energy summand (kernel.cpp:208-209)
+      const double mu2 = s[1] * s[1] + s[2] * s[2] + s[3] * s[3];
+      const double th2 = s[4] * s[4] + s[7] * s[7] + s[9] * s[9] +
+                         2.0 * (s[5] * s[5] + s[6] * s[6] + s[8] * s[8]);
+      acc = s[0] * s[0] + c_mu * mu2 + c_th * th2;
+      // moment_order (kernel.cpp:40-44) > 0 for this particle?
+      mp = (s[1] != 0.0 || s[2] != 0.0 || s[3] != 0.0 || th2 != 0.0);
+    }
+    keys[i] = key;
+    idx[i] = static_cast<unsigned>(i);
+    if (counts) atomicAdd(&counts[key], 1u);
+  }
+  if (__any_sync(0xffffffffu, mp) && (threadIdx.x & 31) == 0) atomicOr(&res->any_multipole, 1);
+  // deterministic block reduction
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    self_partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gather(const double* __restrict__ pos,
+                                                const double* __restrict__ src,
+                                                const unsigned* __restrict__ idx_sorted,
+                                                std::size_t n, double* __restrict__ part) {
+  const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (j >= n) return;
+  const std::size_t i = idx_sorted[j];
+  double r[kRec];
+  r[0] = pos[3 * i];
+  r[1] = pos[3 * i + 1];
+  r[2] = pos[3 * i + 2];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) r[3 + k] = src[10 * i + k];
+  r[13] = (r[7] + r[10]) + r[12];  // SymMat3::trace (types.hpp:57)
+  r[14] = 0.0;
+  r[15] = 0.0;
+  double2* out = reinterpret_cast<double2*>(part + j * kRec);
+#pragma unroll
+  for (int k = 0; k < kRec / 2; ++k) out[k] = make_double2(r[2 * k], r[2 * k + 1]);
+}
+
+__global__ void k_init_result(DevResult* res) {
+  res->e_self = res->e_near = res->e_far = res->e_periodic = 0.0;
+  res->near_pairs = 0;
+  res->min_nonfinite = ~0ull;
+  res->min_outside = ~0ull;
+  res->duplicate = 0;
+  res->coincident = 0;
+  res->any_multipole = 0;
+}
+
+// Exact-duplicate scan over (key, index)-sorted particles: duplicates share a
+// leaf, so only runs of equal keys are compared (validate_system's rule,
+// types.cpp:45-61).  Used on the error path where no P2P pass runs.
+__global__ void k_dup_check(const unsigned* __restrict__ keys, const unsigned* __restrict__ idx,
+                            const double* __restrict__ pos, std::size_t n, DevResult* res) {
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (i >= n) return;
+  const std::size_t a = idx[i];
+  for (std::size_t j = i + 1; j < n && keys[j] == keys[i]; ++j) {
+    const std::size_t b = idx[j];
+    if (pos[3 * a] == pos[3 * b] && pos[3 * a + 1] == pos[3 * b + 1] &&
+        pos[3 * a + 2] == pos[3 * b + 2]) {
+      atomicOr(&res->duplicate, 1);
+      return;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_init_result(DevResult* res, cudaStream_t st) { k_init_result<<<1, 1, 0, st>>>(res); }
+
+void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
+                      std::size_t n, DevResult* res, cudaStream_t st) {
+  if (n < 2) return;
+  k_dup_check<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys_sorted, idx_sorted, pos,
+                                                                     n, res);
+}
+
+void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
+                double inv_side, int n_axis, double xi, unsigned* keys, unsigned* idx,
+                unsigned* counts, double* self_partial, DevResult* res, cudaStream_t st) {
+  if (n == 0) return;
+  const double c_mu = 2.0 * xi * xi / 3.0;
+  const double c_th = 8.0 * xi * xi * xi * xi / 5.0;
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  k_bin<<<blocks, 256, 0, st>>>(pos, src, n, box_radius, inv_side, n_axis, c_mu, c_th, keys, idx,
+                                counts, self_partial, res);
+}
+
+void launch_gather(const double* pos, const double* src, const unsigned* idx_sorted, std::size_t n,
+                   double* part, cudaStream_t st) {
+  if (n == 0) return;
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  k_gather<<<blocks, 256, 0, st>>>(pos, src, idx_sorted, n, part);
+}
+
+std::size_t sort_temp_bytes(std::size_t n, int n_leaves) {
+  std::size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const unsigned*>(nullptr),
+                                  static_cast<unsigned*>(nullptr),
+                                  static_cast<const unsigned*>(nullptr),
+                                  static_cast<unsigned*>(nullptr), static_cast<int>(n), 0, 32);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const unsigned*>(nullptr),
+                                static_cast<unsigned*>(nullptr), n_leaves + 1);
+  return (a > b ? a : b) + 256;
+}
+
+void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
+                 const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
+                 const unsigned* counts, unsigned* offsets, int n_leaves, cudaStream_t st) {
+  if (n > 0) {
+    std::size_t bytes = temp_bytes;
+    cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out, idx_in, idx_out,
+                                    static_cast<int>(n), 0, end_bit > 0 ? end_bit : 1, st);
+  }
+  if (counts) {
+    std::size_t bytes = temp_bytes;
+    cub::DeviceScan::ExclusiveSum(temp, bytes, counts, offsets, n_leaves + 1, st);
+  }
+}
+
+}  // namespace ankh_b200

@@ -1,0 +1,166 @@
+// M2L far-field energy on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).
+//
+// Restates far_field_energy (fmm.cpp:238-276): for every canonical instance
+// (t, s) of one (level, offset) operator with factors L, R (k x K, from
+// compress_m2l fmm.cpp:98-133)
+//     e += (L M_t) . (R M_s)
+// As a grouped GEMM: a CTA takes 64 instances of one operator, streams the
+// factor rows (padded to kp = 8*KP8) and the 2 x 64 gathered expansions
+// through shared memory in 32-column chunks, and each warp accumulates
+// U = L [M_t...] and V = R [M_s...] for its 8 instances in DMMA fragments
+// (rank rows = M dim, instances = N dim, nodes = K dim).  The energy of the
+// tile is sum(U o V), reduced in a fixed order into one partial per tile.
+// FP64-pipe bound: 4kK + 2k flops per instance.
+#include "kernels.cuh"
+
+namespace ankh_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;          // 8 warps x 8 instances
+constexpr int kStride = kM2LChunk + 4; // smem row stride (doubles): conflict-free fragments
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int KP8>
+__global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp,
+                                                  const long long* __restrict__ level_off,
+                                                  const double* __restrict__ factors,
+                                                  const M2LOp* __restrict__ ops,
+                                                  const M2LTile* __restrict__ tiles,
+                                                  const int* __restrict__ tile_ids,
+                                                  const uint2* __restrict__ inst, int K, int Kp,
+                                                  double* __restrict__ far_partial) {
+  constexpr int kp = 8 * KP8;
+  extern __shared__ double sm[];
+  double* sL = sm;                       // kp x kStride
+  double* sR = sL + kp * kStride;        // kp x kStride
+  double* sT = sR + kp * kStride;        // 64 x kStride (targets)
+  double* sS = sT + kM2LTile * kStride;  // 64 x kStride (sources)
+  __shared__ double red[kThreads / 32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile_index = tile_ids[blockIdx.x];
+  const M2LTile tile = tiles[tile_index];
+  const M2LOp op = ops[tile.op];
+  const double* Lg = factors + op.factor_off;
+  const double* Rg = Lg + static_cast<long long>(op.kp) * Kp;
+  const double* E = exp + level_off[tile.level];
+
+  double u[KP8][2], v[KP8][2];
+#pragma unroll
+  for (int m = 0; m < KP8; ++m) u[m][0] = u[m][1] = v[m][0] = v[m][1] = 0.0;
+
+  const int row = lane >> 2, col = lane & 3;
+  for (int k0 = 0; k0 < Kp; k0 += kM2LChunk) {
+    // stage factor columns [k0, k0+32) of L and R (rows beyond op.kp are zero)
+    for (int w = tid; w < kp * kM2LChunk; w += kThreads) {
+      const int r = w / kM2LChunk, c = w - kM2LChunk * (w / kM2LChunk);
+      double lv = 0.0, rv = 0.0;
+      if (r < op.kp) {
+        lv = __ldg(Lg + static_cast<long long>(r) * Kp + k0 + c);
+        rv = __ldg(Rg + static_cast<long long>(r) * Kp + k0 + c);
+      }
+      sL[r * kStride + c] = lv;
+      sR[r * kStride + c] = rv;
+    }
+    // stage expansion columns of the 64 target and source cells
+    for (int w = tid; w < kM2LTile * kM2LChunk; w += kThreads) {
+      const int q = w / kM2LChunk, c = w - kM2LChunk * (w / kM2LChunk);
+      const int k = k0 + c;
+      double tv = 0.0, sv = 0.0;
+      if (q < tile.count && k < K) {
+        const uint2 ts = inst[tile.begin + q];
+        tv = __ldg(E + static_cast<long long>(ts.x) * K + k);
+        sv = __ldg(E + static_cast<long long>(ts.y) * K + k);
+      }
+      sT[q * kStride + c] = tv;
+      sS[q * kStride + c] = sv;
+    }
+    __syncthreads();
+    const double* bT = sT + (warp * 8 + row) * kStride + col;
+    const double* bS = sS + (warp * 8 + row) * kStride + col;
+#pragma unroll
+    for (int ks = 0; ks < kM2LChunk / 4; ++ks) {
+      const double bt = bT[4 * ks];
+      const double bs = bS[4 * ks];
+#pragma unroll
+      for (int m = 0; m < KP8; ++m) {
+        const double al = sL[(8 * m + row) * kStride + 4 * ks + col];
+        const double ar = sR[(8 * m + row) * kStride + 4 * ks + col];
+        dmma(u[m], al, bt);
+        dmma(v[m], ar, bs);
+      }
+    }
+    __syncthreads();
+  }
+  double e = 0.0;
+#pragma unroll
+  for (int m = 0; m < KP8; ++m) e += u[m][0] * v[m][0] + u[m][1] * v[m][1];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
+  if (lane == 0) red[warp] = e;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+    far_partial[tile_index] = t;
+  }
+}
+
+template <int KP8>
+void launch_class(const double* exp, const long long* level_off, const double* factors,
+                  const M2LOp* ops, const M2LTile* tiles, int n_tiles, const int* tile_ids,
+                  const uint2* inst, int K, int Kp, double* far_partial, cudaStream_t st) {
+  const std::size_t smem = sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_m2l<KP8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  k_m2l<KP8><<<n_tiles, kThreads, smem, st>>>(exp, level_off, factors, ops, tiles, tile_ids, inst,
+                                              K, Kp, far_partial);
+}
+
+}  // namespace
+
+void launch_m2l(const double* exp, const long long* level_off, const double* factors,
+                const M2LOp* ops, const M2LTile* tiles, int n_tiles_class, int kp8,
+                const int* tile_ids, const uint2* inst, int K, int Kp, double* far_partial,
+                cudaStream_t st) {
+  if (n_tiles_class <= 0) return;
+#define ANKH_M2L_CASE(N)                                                                    \
+  case N:                                                                                   \
+    launch_class<N>(exp, level_off, factors, ops, tiles, n_tiles_class, tile_ids, inst, K, \
+                    Kp, far_partial, st);                                                   \
+    break;
+  switch (kp8) {
+    ANKH_M2L_CASE(1)
+    ANKH_M2L_CASE(2)
+    ANKH_M2L_CASE(3)
+    ANKH_M2L_CASE(4)
+    ANKH_M2L_CASE(5)
+    ANKH_M2L_CASE(6)
+    ANKH_M2L_CASE(7)
+    ANKH_M2L_CASE(8)
+    ANKH_M2L_CASE(9)
+    ANKH_M2L_CASE(10)
+    ANKH_M2L_CASE(11)
+    ANKH_M2L_CASE(12)
+    ANKH_M2L_CASE(13)
+    ANKH_M2L_CASE(14)
+    ANKH_M2L_CASE(15)
+    ANKH_M2L_CASE(16)
+    default:
+      break;
+  }
+#undef ANKH_M2L_CASE
+}
+
+}  // namespace ankh_b200

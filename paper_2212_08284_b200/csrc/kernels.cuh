@@ -1,0 +1,84 @@
+// Device-side declarations shared by the sm_100a kernels and the host plan.
+//
+// HBM layout (all float64 unless noted):
+//   part    : N x 16   particle records sorted by lex leaf id, ascending input
+//                      index inside a leaf (== build_tree bucket order,
+//                      octree.cpp:27-45): x y z q mux muy muz Txx Txy Txz Tyy
+//                      Tyz Tzz tr(Theta) 0 0   (128 B, 16-B aligned)
+//   leaf_off: 8^E + 1  uint32 leaf CSR offsets into `part`
+//   exp     : sum_l 8^l x K   expansions, level-major, lex cell order
+//   factors : per M2L operator, L (kp x Kp) then R (kp x Kp), zero padded
+//   inst    : uint2 (t, s) canonical M2L instances grouped by operator
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ankh_b200 {
+
+constexpr int kRec = 16;          // doubles per particle record
+constexpr int kM2LTile = 64;      // instances per M2L CTA
+constexpr int kM2LChunk = 32;     // node columns per staged chunk
+constexpr int kMaxKp8 = 16;       // ranks up to 128
+constexpr int kP2PThreads = 256;
+
+struct DevResult {
+  double e_self, e_near, e_far, e_periodic;
+  unsigned long long near_pairs;
+  unsigned long long min_nonfinite;  // lowest index with a non-finite value
+  unsigned long long min_outside;    // lowest finite index outside the box
+  int duplicate;                     // exact duplicate positions found
+  int coincident;                    // r == 0 under an image shift
+  int any_multipole;                 // some particle has mu or Theta != 0
+};
+
+struct M2LTile {
+  int op;       // operator index
+  int level;    // tree level (selects the expansion slice)
+  int begin;    // first instance
+  int count;    // instances in this tile (<= kM2LTile)
+};
+
+struct M2LOp {
+  long long factor_off;  // offset (doubles) of L; R follows at + kp*Kp
+  int kp;                // padded rank (multiple of 8)
+  int rank;
+};
+
+// ---- launchers (defined in the .cu files) ----
+void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
+                double inv_side, int n_axis, double xi, unsigned* keys, unsigned* idx,
+                unsigned* counts, double* self_partial, DevResult* res, cudaStream_t st);
+void launch_gather(const double* pos, const double* src, const unsigned* idx_sorted, std::size_t n,
+                   double* part, cudaStream_t st);
+std::size_t sort_temp_bytes(std::size_t n, int n_leaves);
+void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
+                 const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
+                 const unsigned* counts, unsigned* offsets, int n_leaves, cudaStream_t st);
+void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
+                double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
+                cudaStream_t st);
+void launch_m2m(const double* child, double* parent, int parent_level, int order,
+                const double* m2m, cudaStream_t st);
+void launch_m2l(const double* exp, const long long* level_off, const double* factors,
+                const M2LOp* ops, const M2LTile* tiles, int n_tiles_class, int kp8,
+                const int* tile_ids, const uint2* inst, int K, int Kp, double* far_partial,
+                cudaStream_t st);
+void launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
+                double period, double xi, int nterms, int leaf_begin, int leaf_end,
+                double* near_partial, unsigned long long* pair_count, DevResult* res,
+                cudaStream_t st);
+int p2p_terms_for(double s_max);
+void launch_periodic_gen(double* gen, int order, double box_radius, double xi, int p,
+                         cudaStream_t st);
+void launch_periodic_eval(const double* root, const double* to_equi, const double* spec_re,
+                          int order, double* out, cudaStream_t st);
+void launch_finalize(const double* near_partial, int n_near, const unsigned long long* pair_count,
+                     const double* far_partial, int n_far, const double* self_partial,
+                     int n_self, double self_scale, const double* periodic, int use_periodic,
+                     int include_self, DevResult* res, cudaStream_t st);
+void launch_init_result(DevResult* res, cudaStream_t st);
+void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
+                      std::size_t n, DevResult* res, cudaStream_t st);
+
+}  // namespace ankh_b200

@@ -1,0 +1,557 @@
+// Host side of the B200 engine: geometry-only precompute and the launch
+// sequence of one energy evaluation (fmm.cpp:383-436 re-planned for HBM).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <set>
+
+#include "host_numerics.hpp"
+
+namespace ankh_b200 {
+
+int default_depth(std::size_t n) {
+  constexpr double target_per_leaf = 64.0;
+  if (n <= target_per_leaf) return 1;
+  const double levels = std::log(static_cast<double>(n) / target_per_leaf) / std::log(8.0);
+  return std::max(1, static_cast<int>(std::ceil(levels - 1e-12)));
+}
+
+void validate_config(const ankh_config_v1& c) {
+  auto bad = [](const char* m) { throw AnkhError(ANKH_INVALID_ARGUMENT, m); };
+  if (!(c.xi > 0.0) || !std::isfinite(c.xi)) bad("xi must be positive");
+  if (c.p < 0 || c.p == 1) bad("image half-width p must be 0 (open) or >= 2 (periodic)");
+  if (c.order_cheb < 2) bad("order_cheb must be >= 2");
+  if (c.order_equi < 2) bad("order_equi must be >= 2");
+  if (c.depth < 0) bad("depth must be >= 1 (or 0 for automatic)");
+  if (!(c.svd_tol > 0.0) || !(c.svd_tol < 1.0)) bad("svd_tol must lie in (0, 1)");
+  if (c.recip_cutoff < 1) bad("recip_cutoff must be >= 1");
+}
+
+namespace {
+constexpr double kInvSqrtPi = 0.5641895835477562869;
+constexpr int kMaxOrderGpu = 10;
+
+int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace
+
+Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool csr_only)
+    : n(n_), rb(box_radius), cfg(cfg_), csr_only_(csr_only) {
+  const auto t0 = std::chrono::steady_clock::now();
+  validate_config(cfg);
+  if (!(rb > 0.0) || !std::isfinite(rb))
+    throw AnkhError(ANKH_INVALID_ARGUMENT, "fmm_energy: invalid system: box_radius must be positive and finite");
+  if (n >= (1ull << 31)) throw AnkhError(ANKH_RUNTIME_ERROR, "fmm_energy: more than 2^31-1 particles");
+  if (cfg.world < 1) cfg.world = 1;
+  if (cfg.rank < 0 || cfg.rank >= cfg.world) throw AnkhError(ANKH_INVALID_ARGUMENT, "rank out of range");
+  if (cfg.device >= 0) {
+    device_ = cfg.device;
+    ANKH_CUDA(cudaSetDevice(device_));
+  } else {
+    ANKH_CUDA(cudaGetDevice(&device_));
+  }
+  periodic = cfg.p >= 2;
+  depth = cfg.depth > 0 ? cfg.depth : default_depth(n);
+  L = cfg.order_cheb;
+  // Errors the reference raises only after validate_system (octree.cpp:28,
+  // chebyshev.cpp:86) are deferred so a system violation still wins.
+  if (depth < 1 || depth > 8) {
+    pending_code_ = ANKH_INVALID_ARGUMENT;
+    pending_msg_ = "build_tree: depth must be in [1, 8]";
+  } else if (L > 64) {
+    pending_code_ = ANKH_INVALID_ARGUMENT;
+    pending_msg_ = "DiffOperator: order out of range";
+  } else if (L > kMaxOrderGpu) {
+    pending_code_ = ANKH_RUNTIME_ERROR;
+    pending_msg_ = "order_cheb > 10 is not supported by the B200 engine";
+  }
+  ANKH_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  for (auto& e : ev_) ANKH_CUDA(cudaEventCreate(&e));
+  if (pending_code_ != 0) {
+    depth = 1;  // validation-only plan
+    L = 2;
+  }
+  K = L * L * L;
+  Kp = ceil_div(K, kM2LChunk) * kM2LChunk;
+  nax = 1 << depth;
+  n_leaves = 1 << (3 * depth);
+  build_geometry();
+  allocate();
+  if (pending_code_ == 0 && n > 0 && !csr_only_) {
+    build_m2l();
+    if (periodic) build_periodic();
+  }
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+  precompute_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+Plan::~Plan() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (void* p : allocs_) cudaFree(p);
+  if (h_res_) cudaFreeHost(h_res_);
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void* Plan::dalloc(std::size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  ANKH_CUDA(cudaMalloc(&p, bytes));
+  allocs_.push_back(p);
+  device_bytes += bytes;
+  return p;
+}
+
+void Plan::build_geometry() {
+  // leaf ownership: contiguous Morton ranges
+  const long long nl = n_leaves;
+  leaf_begin_ = static_cast<int>(nl * cfg.rank / cfg.world);
+  leaf_end_ = static_cast<int>(nl * (cfg.rank + 1) / cfg.world);
+  include_self_ = cfg.rank == 0;
+  // P2P polynomial length from the largest possible near distance
+  // (2 leaf sides per axis): s_max = xi^2 (2 sqrt(3) * 2 r_B / n)^2
+  const double side = 2.0 * rb / nax;
+  const double dmax = 2.0 * std::sqrt(3.0) * side * 1.0001;
+  nterms_ = p2p_terms_for(cfg.xi * cfg.xi * dmax * dmax);
+}
+
+void Plan::allocate() {
+  const std::size_t nn = std::max<std::size_t>(n, 1);
+  d_pos_ = static_cast<double*>(dalloc(nn * 3 * sizeof(double)));
+  d_src_ = static_cast<double*>(dalloc(nn * 10 * sizeof(double)));
+  d_keys_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
+  d_keys2_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
+  d_idx_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
+  d_idx2_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
+  d_counts_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
+  d_off_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
+  temp_bytes_ = sort_temp_bytes(nn, n_leaves);
+  d_temp_ = dalloc(temp_bytes_);
+  d_part_ = static_cast<double*>(dalloc(nn * kRec * sizeof(double)));
+  level_off_.assign(depth + 2, 0);
+  for (int l = 0; l <= depth; ++l) level_off_[l + 1] = level_off_[l] + (1ll << (3 * l)) * K;
+  d_exp_ = static_cast<double*>(dalloc(level_off_[depth + 1] * sizeof(double)));
+  d_level_off_ = static_cast<long long*>(dalloc(level_off_.size() * sizeof(long long)));
+  ANKH_CUDA(cudaMemcpyAsync(d_level_off_, level_off_.data(), level_off_.size() * sizeof(long long),
+                            cudaMemcpyHostToDevice, stream_));
+  n_self_blocks_ = static_cast<int>((nn + 255) / 256);
+  d_self_part_ = static_cast<double*>(dalloc(n_self_blocks_ * sizeof(double)));
+  d_near_part_ = static_cast<double*>(dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(double)));
+  d_pair_count_ = static_cast<unsigned long long*>(
+      dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(unsigned long long)));
+  d_per_ = static_cast<double*>(dalloc(sizeof(double)));
+  d_res_ = static_cast<DevResult*>(dalloc(sizeof(DevResult)));
+  ANKH_CUDA(cudaMallocHost(&h_res_, sizeof(DevResult)));
+  // small operators (chebyshev.cpp:85-108, fmm.cpp:213-219, 421-424)
+  const auto hd = diff_operator(L);
+  std::vector<double> hd_all;
+  for (const auto& m : hd) hd_all.insert(hd_all.end(), m.begin(), m.end());
+  const std::vector<double> nodes = cheb_nodes(L);
+  std::vector<double> lo(L), hi(L);
+  for (int i = 0; i < L; ++i) {
+    lo[i] = 0.5 * (nodes[i] - 1.0);
+    hi[i] = 0.5 * (nodes[i] + 1.0);
+  }
+  std::vector<double> m2m = transfer_cheb(L, lo);
+  const std::vector<double> m2m_hi = transfer_cheb(L, hi);
+  m2m.insert(m2m.end(), m2m_hi.begin(), m2m_hi.end());
+  const std::vector<double> to_equi = transfer_equi(L, nodes);
+  d_hd_ = static_cast<double*>(dalloc(hd_all.size() * sizeof(double)));
+  d_m2m_ = static_cast<double*>(dalloc(m2m.size() * sizeof(double)));
+  d_to_equi_ = static_cast<double*>(dalloc(to_equi.size() * sizeof(double)));
+  ANKH_CUDA(cudaMemcpyAsync(d_hd_, hd_all.data(), hd_all.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaMemcpyAsync(d_m2m_, m2m.data(), m2m.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaMemcpyAsync(d_to_equi_, to_equi.data(), to_equi.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// build_m2l_cache (fmm.cpp:141-179) + the canonical instance lists of
+// far_field_energy (fmm.cpp:244-253), grouped by (level, offset).
+void Plan::build_m2l() {
+  struct OffsetWork {
+    int level;
+    std::array<int, 3> o;
+    std::vector<uint2> inst;
+    Factors f;
+  };
+  std::vector<OffsetWork> work;
+  for (int level = 1; level <= depth; ++level)
+    for (int ox = -3; ox <= 3; ++ox)
+      for (int oy = -3; oy <= 3; ++oy)
+        for (int oz = -3; oz <= 3; ++oz)
+          if (std::max({std::abs(ox), std::abs(oy), std::abs(oz)}) >= 2)
+            work.push_back({level, {ox, oy, oz}, {}, {}});
+  const int threads = cfg.threads;
+  // instance enumeration: Lambda(t) offsets are s - t in [-2-c, 3-c] per axis,
+  // c = t & 1 (octree.cpp:79-87); canonical iff t < s or (t == s and image
+  // lex-positive) (fmm.cpp:246-250)
+  parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
+    OffsetWork& w = work[wi];
+    const int nl = 1 << w.level;
+    int lo[3], hi[3], step[3];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = 0;
+      hi[a] = nl;
+      step[a] = 1;
+      if (w.o[a] == 3) step[a] = 2;                 // only even t_a
+      if (w.o[a] == -3) { lo[a] = 1; step[a] = 2; }  // only odd t_a
+    }
+    for (int tx = lo[0]; tx < hi[0]; tx += step[0])
+      for (int ty = lo[1]; ty < hi[1]; ty += step[1])
+        for (int tz = lo[2]; tz < hi[2]; tz += step[2]) {
+          const int ext[3] = {tx + w.o[0], ty + w.o[1], tz + w.o[2]};
+          int in[3], img[3];
+          bool ok = true;
+          for (int a = 0; a < 3; ++a) {
+            if (!periodic && (ext[a] < 0 || ext[a] >= nl)) ok = false;
+            img[a] = ext[a] >= 0 ? ext[a] / nl : -((-ext[a] + nl - 1) / nl);
+            in[a] = ext[a] - nl * img[a];
+          }
+          if (!ok) continue;
+          const unsigned t = static_cast<unsigned>((tx * nl + ty) * nl + tz);
+          const unsigned s = static_cast<unsigned>((in[0] * nl + in[1]) * nl + in[2]);
+          bool lexpos = img[0] != 0 ? img[0] > 0 : (img[1] != 0 ? img[1] > 0 : img[2] > 0);
+          if (t < s || (t == s && lexpos)) w.inst.push_back(make_uint2(t, s));
+        }
+  });
+  work.erase(std::remove_if(work.begin(), work.end(),
+                            [](const OffsetWork& w) { return w.inst.empty(); }),
+             work.end());
+  // factors: exact SVD path uses the signed-permutation symmetry of the block
+  // (one SVD per class, SURVEY.md Decision 3); K > 150 replicates the
+  // reference's seeded randomized path per offset.
+  if (K <= 150) {
+    std::map<std::pair<int, std::array<int, 3>>, Factors> reps;
+    for (const auto& w : work) reps[{w.level, symmetry_of(w.o).rep}] = Factors{};
+    std::vector<std::pair<int, std::array<int, 3>>> keys;
+    for (const auto& kv : reps) keys.push_back(kv.first);
+    std::vector<Factors> fac(keys.size());
+    parallel_for(static_cast<int>(keys.size()), threads, [&](int i) {
+      const int level = keys[i].first;
+      const double rad = rb / (1 << level);
+      fac[i] = compress_m2l(m2l_dense(L, rad, keys[i].second, cfg.xi), K, cfg.svd_tol, 0);
+    });
+    for (std::size_t i = 0; i < keys.size(); ++i) reps[keys[i]] = std::move(fac[i]);
+    parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
+      OffsetWork& w = work[wi];
+      const Symmetry sym = symmetry_of(w.o);
+      const Factors& r = reps.at({w.level, sym.rep});
+      const std::vector<int> perm = node_permutation(sym, L);
+      w.f.rank = r.rank;
+      w.f.k_full = K;
+      w.f.lmat.assign(r.lmat.size(), 0.0);
+      w.f.rmat.assign(r.rmat.size(), 0.0);
+      for (int row = 0; row < r.rank; ++row)
+        for (int k = 0; k < K; ++k) {
+          w.f.lmat[static_cast<std::size_t>(row) * K + perm[k]] = r.lmat[static_cast<std::size_t>(row) * K + k];
+          w.f.rmat[static_cast<std::size_t>(row) * K + perm[k]] = r.rmat[static_cast<std::size_t>(row) * K + k];
+        }
+    });
+  } else {
+    parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
+      OffsetWork& w = work[wi];
+      const double rad = rb / (1 << w.level);
+      const std::int64_t key = offset_key(w.o);
+      w.f = compress_m2l(m2l_dense(L, rad, w.o, cfg.xi), K, cfg.svd_tol, m2l_seed(w.level, key));
+    });
+  }
+  // device operators: row blocks of <= 128 ranks, L then R, zero padded
+  std::vector<M2LTile> tiles;
+  std::vector<uint2> inst;
+  h_ops_.clear();
+  h_factors_.clear();
+  double rank_sum = 0.0;
+  far_flops = 0.0;
+  m2l_instances = 0;
+  for (const auto& w : work) {
+    const int rank = w.f.rank;
+    OpInfo info{w.level, offset_key(w.o), rank, static_cast<int>(h_ops_.size()), 0};
+    const int inst_begin = static_cast<int>(inst.size());
+    inst.insert(inst.end(), w.inst.begin(), w.inst.end());
+    for (int r0 = 0; r0 < rank; r0 += 8 * kMaxKp8) {
+      const int rows = std::min(8 * kMaxKp8, rank - r0);
+      const int kp = ceil_div(rows, 8) * 8;
+      M2LOp op;
+      op.factor_off = static_cast<long long>(h_factors_.size());
+      op.kp = kp;
+      op.rank = rows;
+      std::vector<double> blockL(static_cast<std::size_t>(kp) * Kp, 0.0), blockR(blockL.size(), 0.0);
+      for (int r = 0; r < rows; ++r)
+        for (int k = 0; k < K; ++k) {
+          blockL[static_cast<std::size_t>(r) * Kp + k] = w.f.lmat[static_cast<std::size_t>(r0 + r) * K + k];
+          blockR[static_cast<std::size_t>(r) * Kp + k] = w.f.rmat[static_cast<std::size_t>(r0 + r) * K + k];
+        }
+      h_factors_.insert(h_factors_.end(), blockL.begin(), blockL.end());
+      h_factors_.insert(h_factors_.end(), blockR.begin(), blockR.end());
+      const int op_index = static_cast<int>(h_ops_.size());
+      h_ops_.push_back(op);
+      ++info.n_blocks;
+      for (int b = 0; b < static_cast<int>(w.inst.size()); b += kM2LTile)
+        tiles.push_back({op_index, w.level, inst_begin + b,
+                         std::min(kM2LTile, static_cast<int>(w.inst.size()) - b)});
+    }
+    op_info_[{w.level, info.key}] = info;
+    rank_sum += rank;
+    m2l_instances += w.inst.size();
+    far_flops += static_cast<double>(w.inst.size()) * (4.0 * rank * K + 2.0 * rank);
+  }
+  m2l_operators = work.size();
+  m2l_rank_mean = work.empty() ? 0.0 : rank_sum / work.size();
+  n_tiles_ = static_cast<int>(tiles.size());
+  // ownership of tiles: cost-weighted contiguous split across shards
+  std::vector<double> cost(tiles.size());
+  double total_cost = 0.0;
+  for (std::size_t i = 0; i < tiles.size(); ++i) {
+    cost[i] = static_cast<double>(h_ops_[tiles[i].op].kp) * tiles[i].count;
+    total_cost += cost[i];
+  }
+  std::vector<int> owned;
+  double run = 0.0;
+  for (std::size_t i = 0; i < tiles.size(); ++i) {
+    const double mid = run + 0.5 * cost[i];
+    run += cost[i];
+    const int owner = total_cost > 0 ? std::min(cfg.world - 1, static_cast<int>(mid / total_cost * cfg.world)) : 0;
+    if (owner == cfg.rank) owned.push_back(static_cast<int>(i));
+  }
+  // group owned tiles by kp class
+  class_range_.assign(kMaxKp8 + 1, {0, 0});
+  std::vector<int> ids;
+  for (int c = 1; c <= kMaxKp8; ++c) {
+    const int begin = static_cast<int>(ids.size());
+    for (int t : owned)
+      if (h_ops_[tiles[t].op].kp / 8 == c) ids.push_back(t);
+    class_range_[c] = {begin, static_cast<int>(ids.size()) - begin};
+  }
+  d_factors_ = static_cast<double*>(dalloc(h_factors_.size() * sizeof(double)));
+  d_ops_ = static_cast<M2LOp*>(dalloc(h_ops_.size() * sizeof(M2LOp)));
+  d_tiles_ = static_cast<M2LTile*>(dalloc(tiles.size() * sizeof(M2LTile)));
+  d_inst_ = static_cast<uint2*>(dalloc(inst.size() * sizeof(uint2)));
+  d_tile_ids_ = static_cast<int*>(dalloc(std::max<std::size_t>(ids.size(), 1) * sizeof(int)));
+  d_far_part_ = static_cast<double*>(dalloc(std::max<std::size_t>(tiles.size(), 1) * sizeof(double)));
+  ANKH_CUDA(cudaMemcpyAsync(d_factors_, h_factors_.data(), h_factors_.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaMemcpyAsync(d_ops_, h_ops_.data(), h_ops_.size() * sizeof(M2LOp),
+                            cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaMemcpyAsync(d_tiles_, tiles.data(), tiles.size() * sizeof(M2LTile),
+                            cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaMemcpyAsync(d_inst_, inst.data(), inst.size() * sizeof(uint2),
+                            cudaMemcpyHostToDevice, stream_));
+  if (!ids.empty())
+    ANKH_CUDA(cudaMemcpyAsync(d_tile_ids_, ids.data(), ids.size() * sizeof(int),
+                              cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaMemsetAsync(d_far_part_, 0, std::max<std::size_t>(tiles.size(), 1) * sizeof(double), stream_));
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// build_periodic_operator (fmm.cpp:333-377): generator on the GPU, its r2c
+// spectrum (FFTW layout, spectral.cpp:47-62) on the host, real part uploaded.
+void Plan::build_periodic() {
+  const int eb = 2 * L - 1;
+  const std::size_t m = static_cast<std::size_t>(eb) * eb * eb;
+  double* d_gen = static_cast<double*>(dalloc(m * sizeof(double)));
+  launch_periodic_gen(d_gen, L, rb, cfg.xi, cfg.p, stream_);
+  ANKH_CUDA(cudaGetLastError());
+  std::vector<double> gen(m);
+  ANKH_CUDA(cudaMemcpyAsync(gen.data(), d_gen, m * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+  const std::vector<double> spec = r2c_3d(gen, eb, eb, eb);
+  std::vector<double> re(spec.size() / 2);
+  for (std::size_t i = 0; i < re.size(); ++i) re[i] = spec[2 * i];
+  d_spec_re_ = static_cast<double*>(dalloc(re.size() * sizeof(double)));
+  ANKH_CUDA(cudaMemcpyAsync(d_spec_re_, re.data(), re.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Plan::validate_only(const double* d_pos, const double* d_src, cudaStream_t st) {
+  // per-particle flags and duplicates (types.cpp:16-63) without a tree
+  launch_init_result(d_res_, st);
+  const int nax8 = 256;  // depth-8 bins keep the duplicate scan local
+  const double inv_side = nax8 / (2.0 * rb);
+  launch_bin(d_pos, d_src, n, rb, inv_side, nax8, cfg.xi, d_keys_, d_idx_, nullptr, d_self_part_,
+             d_res_, st);
+  launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 24, nullptr, nullptr,
+              0, st);
+  launch_dup_check(d_keys2_, d_idx2_, d_pos, n, d_res_, st);
+  ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+  launches_ = 3;
+}
+
+void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st) {
+  const bool timing = cfg.phase_timing != 0;
+  std::uint32_t launches = 0;
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_[0], st));
+  ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
+  launch_init_result(d_res_, st);
+  ++launches;
+  // binning + sort + gather (build_tree, octree.cpp:27-45)
+  const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
+  launch_bin(d_pos, d_src, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_, d_self_part_,
+             d_res_, st);
+  ++launches;
+  launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 3 * depth, d_counts_,
+              d_off_, n_leaves, st);
+  launch_gather(d_pos, d_src, d_idx2_, n, d_part_, st);
+  ++launches;
+  if (csr_only_) {
+    launches_ = launches;
+    return;
+  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_[1], st));
+  // interpolation: P2M + M2M (fmm.cpp:181-236)
+  launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, st);
+  ++launches;
+  for (int l = depth - 1; l >= 0; --l) {
+    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, st);
+    ++launches;
+  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_[2], st));
+  // far field: M2L (fmm.cpp:238-276)
+  for (int c = 1; c <= kMaxKp8; ++c) {
+    const auto r = class_range_[c];
+    if (r.second == 0) continue;
+    launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c,
+               d_tile_ids_ + r.first, d_inst_, K, Kp, d_far_part_, st);
+    ++launches;
+  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
+  // near field: P2P (fmm.cpp:278-327)
+  launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, leaf_begin_,
+             leaf_end_, d_near_part_, d_pair_count_, d_res_, st);
+  ++launches;
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));
+  // periodic far images (fmm.cpp:421-427), counted once (rank 0)
+  const bool do_periodic = periodic && include_self_;
+  if (do_periodic) {
+    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, st);
+    ++launches;
+  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_[5], st));
+  launch_finalize(d_near_part_, leaf_end_ - leaf_begin_, d_pair_count_, d_far_part_, n_tiles_,
+                  d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
+                  include_self_ ? 1 : 0, d_res_, st);
+  ++launches;
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_[6], st));
+  ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+  ANKH_CUDA(cudaGetLastError());
+  launches_ = launches;
+}
+
+void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
+  if (!st) st = stream_;
+  last_stream_ = st;
+  evaluated_ = true;
+  if (n == 0) return;
+  if (pending_code_ != 0)
+    validate_only(d_pos, d_src, st);
+  else
+    launch_all(d_pos, d_src, st);
+}
+
+void Plan::enqueue_host(const double* h_pos, const double* h_src, cudaStream_t st) {
+  if (!st) st = stream_;
+  if (n > 0) {
+    ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  enqueue(d_pos_, d_src_, st);
+}
+
+void Plan::result(ankh_report_v1* out) {
+  if (!evaluated_) throw AnkhError(ANKH_RUNTIME_ERROR, "plan has not been evaluated");
+  std::memset(out, 0, sizeof(*out));
+  out->depth = depth;
+  out->order_cheb = L;
+  if (n == 0) {
+    if (pending_code_ != 0) throw AnkhError(pending_code_, pending_msg_);
+    return;
+  }
+  ANKH_CUDA(cudaStreamSynchronize(last_stream_));
+  const DevResult& r = *h_res_;
+  // validate_system precedence: first per-particle violation, then duplicates
+  if (r.min_nonfinite != ~0ull || r.min_outside != ~0ull) {
+    const bool nf = r.min_nonfinite <= r.min_outside;
+    throw AnkhError(ANKH_INVALID_ARGUMENT,
+                    std::string("fmm_energy: invalid system: ") +
+                        (nf ? "non-finite coordinate or moment" : "outside box"));
+  }
+  if (r.duplicate)
+    throw AnkhError(ANKH_INVALID_ARGUMENT, "fmm_energy: invalid system: duplicate position");
+  if (pending_code_ != 0) throw AnkhError(pending_code_, pending_msg_);
+  if (r.coincident) throw AnkhError(ANKH_DOMAIN_ERROR, "pair_interaction: coincident points");
+  out->e_self = r.e_self;
+  out->e_near = r.e_near;
+  out->e_far = r.e_far;
+  out->e_periodic_far = r.e_periodic;
+  out->e_reciprocal = 0.0;
+  // EnergyReport::component_sum order (types.hpp:132-134)
+  out->e_total = out->e_self + out->e_near + out->e_far + out->e_periodic_far + out->e_reciprocal;
+  out->near_pairs = r.near_pairs;
+  out->far_instances = 0;
+  out->gpu_launches = launches_;
+  if (cfg.world <= 1) {
+    out->far_instances = m2l_instances;
+    out->far_flops = far_flops;
+  }
+  if (cfg.phase_timing) {
+    float ms[6];
+    for (int i = 0; i < 6; ++i) ANKH_CUDA(cudaEventElapsedTime(&ms[i], ev_[i], ev_[i + 1]));
+    out->t_precompute = ms[0] * 1e-3;
+    out->t_interpolation = ms[1] * 1e-3;
+    out->t_far_field = ms[2] * 1e-3;
+    out->t_near_field = ms[3] * 1e-3;
+    out->t_periodic_far = ms[4] * 1e-3;
+    out->t_self = ms[5] * 1e-3;  // finalize (self energy is fused into binning)
+  }
+  if (!precompute_reported) {
+    out->t_precompute += precompute_seconds;
+    precompute_reported = true;
+  }
+}
+
+void Plan::expansions(double* out, std::size_t count) {
+  ANKH_CUDA(cudaStreamSynchronize(last_stream_ ? last_stream_ : stream_));
+  const std::size_t total = static_cast<std::size_t>(level_off_[depth + 1]);
+  ANKH_CUDA(cudaMemcpy(out, d_exp_, std::min(count, total) * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+void Plan::m2l_factors(int level, const int* offset, double* lmat, double* rmat, int max_rank,
+                       int* rank) {
+  const std::int64_t key = offset_key({offset[0], offset[1], offset[2]});
+  auto it = op_info_.find({level, key});
+  if (it == op_info_.end()) {
+    *rank = 0;
+    return;
+  }
+  const OpInfo& info = it->second;
+  *rank = info.rank;
+  if (info.rank > max_rank) return;
+  int row = 0;
+  for (int b = 0; b < info.n_blocks; ++b) {
+    const M2LOp& op = h_ops_[info.first_op + b];
+    const double* Lb = h_factors_.data() + op.factor_off;
+    const double* Rb = Lb + static_cast<std::size_t>(op.kp) * Kp;
+    for (int r = 0; r < op.rank; ++r, ++row)
+      for (int k = 0; k < K; ++k) {
+        lmat[static_cast<std::size_t>(row) * K + k] = Lb[static_cast<std::size_t>(r) * Kp + k];
+        rmat[static_cast<std::size_t>(row) * K + k] = Rb[static_cast<std::size_t>(r) * Kp + k];
+      }
+  }
+}
+
+void Plan::leaf_csr(std::uint32_t* offsets, std::uint32_t* indices) {
+  ANKH_CUDA(cudaStreamSynchronize(last_stream_ ? last_stream_ : stream_));
+  ANKH_CUDA(cudaMemcpy(offsets, d_off_, (n_leaves + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (n) ANKH_CUDA(cudaMemcpy(indices, d_idx2_, n * sizeof(unsigned), cudaMemcpyDeviceToHost));
+}
+
+}  // namespace ankh_b200

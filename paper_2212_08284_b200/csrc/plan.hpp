@@ -1,0 +1,133 @@
+// The B200 evaluation plan: geometry-only precompute resident in HBM plus the
+// per-evaluation launch sequence.  One plan per (n, box radius, config).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ankh_b200.h"
+#include "kernels.cuh"
+
+namespace ankh_b200 {
+
+struct AnkhError : std::runtime_error {
+  int code;
+  AnkhError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define ANKH_CUDA(call)                                                                 \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::ankh_b200::AnkhError(ANKH_CUDA_ERROR, std::string(#call) + ": " +         \
+                                                        cudaGetErrorString(e_));        \
+  } while (0)
+
+/// types.cpp:9-14
+int default_depth(std::size_t n);
+/// types.cpp:65-79 (throws AnkhError(ANKH_INVALID_ARGUMENT, same message))
+void validate_config(const ankh_config_v1& c);
+
+struct OpInfo {
+  int level;
+  std::int64_t key;
+  int rank;
+  int first_op;    // device op index of the first row block
+  int n_blocks;
+};
+
+class Plan {
+ public:
+  Plan(std::size_t n, double box_radius, const ankh_config_v1& cfg, bool csr_only = false);
+  ~Plan();
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+
+  /// Enqueue one evaluation reading device inputs (n x 3, n x 10).
+  void enqueue(const double* d_pos, const double* d_src, cudaStream_t st);
+  /// Enqueue including the host->device copy of host inputs.
+  void enqueue_host(const double* h_pos, const double* h_src, cudaStream_t st);
+  /// Wait for the last evaluation and fill the report (throws on validation errors).
+  void result(ankh_report_v1* out);
+
+  void expansions(double* out, std::size_t count);
+  void m2l_factors(int level, const int* offset, double* lmat, double* rmat, int max_rank,
+                   int* rank);
+  void leaf_csr(std::uint32_t* offsets, std::uint32_t* indices);
+
+  cudaStream_t stream() const { return stream_; }
+
+  // ---- geometry (public for introspection) ----
+  std::size_t n = 0;
+  double rb = 1.0;
+  ankh_config_v1 cfg{};
+  int depth = 1, L = 2, K = 8, Kp = 32, nax = 2, n_leaves = 8;
+  bool periodic = false;
+  std::size_t m2l_instances = 0, m2l_operators = 0;
+  double m2l_rank_mean = 0.0, far_flops = 0.0;
+  std::size_t device_bytes = 0;
+  double precompute_seconds = 0.0;
+  bool precompute_reported = false;
+
+ private:
+  void build_geometry();
+  void build_m2l();
+  void build_periodic();
+  void allocate();
+  void* dalloc(std::size_t bytes);
+  void launch_all(const double* d_pos, const double* d_src, cudaStream_t st);
+  void validate_only(const double* d_pos, const double* d_src, cudaStream_t st);
+
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  cudaStream_t last_stream_ = nullptr;
+  std::vector<void*> allocs_;
+  bool csr_only_ = false;
+  int pending_code_ = 0;
+  std::string pending_msg_;
+
+  // partition
+  int leaf_begin_ = 0, leaf_end_ = 0;
+  bool include_self_ = true;
+
+  // inputs / sort
+  double *d_pos_ = nullptr, *d_src_ = nullptr;
+  unsigned *d_keys_ = nullptr, *d_keys2_ = nullptr, *d_idx_ = nullptr, *d_idx2_ = nullptr;
+  unsigned *d_counts_ = nullptr, *d_off_ = nullptr;
+  void* d_temp_ = nullptr;
+  std::size_t temp_bytes_ = 0;
+  double* d_part_ = nullptr;
+  // expansions
+  double* d_exp_ = nullptr;
+  std::vector<long long> level_off_;
+  long long* d_level_off_ = nullptr;
+  double *d_hd_ = nullptr, *d_m2m_ = nullptr, *d_to_equi_ = nullptr, *d_spec_re_ = nullptr;
+  // M2L
+  double* d_factors_ = nullptr;
+  M2LOp* d_ops_ = nullptr;
+  M2LTile* d_tiles_ = nullptr;
+  uint2* d_inst_ = nullptr;
+  int* d_tile_ids_ = nullptr;
+  std::vector<std::pair<int, int>> class_range_;  // per kp8: (begin, count) in d_tile_ids_
+  int n_tiles_ = 0;
+  std::map<std::pair<int, std::int64_t>, OpInfo> op_info_;
+  std::vector<double> h_factors_;  // kept for introspection
+  std::vector<M2LOp> h_ops_;
+  // partials
+  double *d_near_part_ = nullptr, *d_far_part_ = nullptr, *d_self_part_ = nullptr,
+         *d_per_ = nullptr;
+  unsigned long long* d_pair_count_ = nullptr;
+  int n_self_blocks_ = 0;
+  DevResult* d_res_ = nullptr;
+  DevResult* h_res_ = nullptr;
+  int nterms_ = 14;
+  std::uint32_t launches_ = 0;
+  // timing
+  cudaEvent_t ev_[8] = {};
+  bool evaluated_ = false;
+};
+
+}  // namespace ankh_b200
