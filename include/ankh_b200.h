@@ -114,6 +114,13 @@ int ankh_plan_enqueue_v1(ankh_plan_v1* plan, const double* d_positions, const do
                          void* stream, char* err, size_t errlen);
 int ankh_plan_result_v1(ankh_plan_v1* plan, ankh_report_v1* out, char* err, size_t errlen);
 
+/* Enqueue a device-to-device copy of this shard's {e_self, e_near, e_far,
+ * e_periodic_far} (4 doubles) from the last enqueued evaluation into d_out on
+ * `stream`, so a collective (e.g. an NCCL all-reduce across shards) can follow
+ * on the device without a host round trip. */
+int ankh_plan_energies_device_v1(ankh_plan_v1* plan, double* d_out, void* stream, char* err,
+                                 size_t errlen);
+
 /* Plan introspection. */
 int ankh_plan_info_v1(const ankh_plan_v1* plan, int* depth, int* order, size_t* n_cells_leaf,
                       size_t* m2l_instances, size_t* m2l_operators, double* m2l_rank_mean,
@@ -132,6 +139,10 @@ int ankh_leaf_csr_v1(size_t n, const double* positions, double box_radius, int d
 /* M2L factors the plan uses for (level, offset): k x K row-major each. */
 int ankh_plan_m2l_factors_v1(ankh_plan_v1* plan, int level, const int* offset, double* lmat,
                              double* rmat, int max_rank, int* rank, char* err, size_t errlen);
+
+/* Measured FP64 (DFMA) throughput of the current device in TFLOP/s: the
+ * roofline denominator for the FP64-bound kernels (no reference counterpart). */
+double ankh_probe_fp64_tflops_v1(int iters);
 
 /* Library version string. */
 const char* ankh_version_v1(void);

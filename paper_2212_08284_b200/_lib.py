@@ -25,6 +25,8 @@ EXPORTS = [
     "ankh_leaf_csr_v1",
     "ankh_plan_m2l_factors_v1",
     "ankh_version_v1",
+    "ankh_plan_energies_device_v1",
+    "ankh_probe_fp64_tflops_v1",
 ]
 
 
@@ -66,6 +68,9 @@ def lib() -> ctypes.CDLL:
         L.ankh_plan_expansions_v1.argtypes = [c_void_p, D, c_size_t, cp, c_size_t]
         L.ankh_leaf_csr_v1.argtypes = [c_size_t, D, c_double, c_int, U32, U32, cp, c_size_t]
         L.ankh_plan_m2l_factors_v1.argtypes = [c_void_p, c_int, I, D, D, c_int, I, cp, c_size_t]
+        L.ankh_plan_energies_device_v1.argtypes = [c_void_p, c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_probe_fp64_tflops_v1.argtypes = [c_int]
+        L.ankh_probe_fp64_tflops_v1.restype = c_double
         L.ankh_version_v1.argtypes = []
         L.ankh_version_v1.restype = ctypes.c_char_p
         _lib = L

@@ -301,6 +301,13 @@ class Plan:
                                           ctypes.c_void_p(sources.data_ptr()),
                                           ctypes.c_void_p(stream), err, 512), err)
 
+    def energies_to(self, out, stream: int = 0) -> None:
+        """Queue a device copy of {e_self, e_near, e_far, e_periodic_far} into
+        ``out`` (CUDA float64 tensor with >= 4 elements) for a device collective."""
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_energies_device_v1(self._h, ctypes.c_void_p(out.data_ptr()),
+                                                  ctypes.c_void_p(stream), err, 512), err)
+
     def result(self) -> EnergyReport:
         rep = _Report()
         err = ctypes.create_string_buffer(512)

@@ -208,4 +208,21 @@ int ankh_plan_m2l_factors_v1(ankh_plan_v1* plan, int level, const int* offset, d
   });
 }
 
+int ankh_plan_energies_device_v1(ankh_plan_v1* plan, double* d_out, void* stream, char* err,
+                                 size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !d_out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or buffer");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->plan->energies_to_device(d_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+double ankh_probe_fp64_tflops_v1(int iters) {
+  try {
+    return ankh_b200::probe_fp64_tflops(iters > 0 ? iters : 4096);
+  } catch (...) {
+    return 0.0;
+  }
+}
+
 }  // extern "C"

@@ -78,6 +78,7 @@ void launch_finalize(const double* near_partial, int n_near, const unsigned long
                      int n_self, double self_scale, const double* periodic, int use_periodic,
                      int include_self, DevResult* res, cudaStream_t st);
 void launch_init_result(DevResult* res, cudaStream_t st);
+double probe_fp64_tflops(int iters);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);
 

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <numeric>
 #include <set>
@@ -546,6 +547,17 @@ void Plan::m2l_factors(int level, const int* offset, double* lmat, double* rmat,
         rmat[static_cast<std::size_t>(row) * K + k] = Rb[static_cast<std::size_t>(r) * Kp + k];
       }
   }
+}
+
+void Plan::energies_to_device(double* d_out, cudaStream_t st) {
+  if (!st) st = stream_;
+  if (n == 0) {
+    ANKH_CUDA(cudaMemsetAsync(d_out, 0, 4 * sizeof(double), st));
+    return;
+  }
+  static_assert(offsetof(DevResult, e_self) == 0 && offsetof(DevResult, e_periodic) == 24,
+                "DevResult energy layout");
+  ANKH_CUDA(cudaMemcpyAsync(d_out, d_res_, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
 
 void Plan::leaf_csr(std::uint32_t* offsets, std::uint32_t* indices) {

@@ -57,6 +57,8 @@ class Plan {
   void m2l_factors(int level, const int* offset, double* lmat, double* rmat, int max_rank,
                    int* rank);
   void leaf_csr(std::uint32_t* offsets, std::uint32_t* indices);
+  /// Enqueue a device copy of {e_self, e_near, e_far, e_periodic} (4 doubles).
+  void energies_to_device(double* d_out, cudaStream_t st);
 
   cudaStream_t stream() const { return stream_; }
 

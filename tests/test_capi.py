@@ -1,0 +1,92 @@
+"""CPU tests of the drop-in boundary: libankh_b200.so loads, exports every
+symbol include/ankh_b200.h declares, and rejects invalid configurations with
+the reference's messages before touching a device."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2212_08284_b200 as ankh
+from paper_2212_08284_b200 import _lib, api
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "ankh_b200.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(ankh_[a-z0-9_]+_v1)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ankh.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {ankh.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_struct_layouts_match_header():
+    # ankh_config_v1 / ankh_report_v1 sizes as laid out by the C compiler
+    assert ctypes.sizeof(api._Config) == 56
+    assert ctypes.sizeof(api._Report) == 13 * 8 + 2 * 4 + 8 + 8 + 8 + 8
+
+
+def test_default_config_matches_ewaldconfig():
+    c = api._Config()
+    ankh.lib().ankh_config_default_v1(ctypes.byref(c))
+    d = ankh.EwaldConfig()
+    assert (c.xi, c.p, c.order_cheb, c.order_equi, c.depth, c.svd_tol, c.recip_cutoff) == \
+        (d.xi, d.p, d.order_cheb, d.order_equi, d.depth, d.svd_tol, d.recip_cutoff)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(xi=0.0), "xi must be positive"),
+    (dict(xi=float("nan")), "xi must be positive"),
+    (dict(p=1), "image half-width p must be 0 (open) or >= 2 (periodic)"),
+    (dict(p=-3), "image half-width p must be 0 (open) or >= 2 (periodic)"),
+    (dict(order_cheb=1), "order_cheb must be >= 2"),
+    (dict(order_equi=0), "order_equi must be >= 2"),
+    (dict(depth=-1), "depth must be >= 1 (or 0 for automatic)"),
+    (dict(svd_tol=0.0), "svd_tol must lie in (0, 1)"),
+    (dict(svd_tol=1.0), "svd_tol must lie in (0, 1)"),
+    (dict(recip_cutoff=0), "recip_cutoff must be >= 1"),
+])
+def test_config_errors_match_reference(kw, msg):
+    # validate_config runs first (fmm.cpp:384) -- no device needed
+    sys_ = ankh.ParticleSystem(np.zeros((1, 3)), np.array([[1.0] + [0.0] * 9]), 1.0)
+    with pytest.raises(ankh.InvalidArgument) as ei:
+        ankh.fmm_energy(sys_, ankh.EwaldConfig(**kw))
+    assert str(ei.value) == msg
+
+
+def test_size_mismatch_message():
+    with pytest.raises(ankh.InvalidArgument, match="positions and sources must have equal length"):
+        ankh.fmm_energy(ankh.ParticleSystem(np.zeros((2, 3)), np.zeros((1, 10)), 1.0))
+
+
+def test_default_depth_matches_reference_rule():
+    import ankh_oracle as O
+
+    for n in (0, 1, 64, 65, 511, 512, 513, 3000, 24000, 96000, 1029000, 8232000, 10 ** 8):
+        assert ankh.default_depth(n) == O.default_depth(n)
+
+
+def test_product_does_not_import_oracle():
+    """The product path must never route through the checker."""
+    pkg = os.path.join(ROOT, "paper_2212_08284_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cpp", ".cu", ".cuh", ".hpp", ".h")):
+                with open(os.path.join(dirpath, fn)) as f:
+                    text = f.read()
+                assert "ankh_oracle" not in text and "libankh_ref" not in text, fn
+                assert "import ref" not in text, fn

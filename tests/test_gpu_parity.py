@@ -1,0 +1,257 @@
+"""GPU parity tests: the sm_100a engine, called through the C-ABI
+(libankh_b200.so via paper_2212_08284_b200.api), against the reference.
+
+Checkers: golden vectors produced by the reference itself
+(tests/golden/make_golden.py -> oracle/_ref), the reference library directly
+when it is present, and the numpy restatement (oracle/ankh_oracle.py).
+
+Tolerances (north star): e_total within 1e-10 relative; leaf assignment and
+order bit-exact.  Components are checked at 1e-11 relative (e_near, e_far,
+e_self) -- e_periodic_far is cancellation-limited (the root expansion of a
+neutral box sums to ~0 against a nearly constant generator), so it is checked
+at 1e-8 relative to itself and 1e-12 relative to e_total.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2212_08284_b200 as ankh
+from paper_2212_08284_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def check_energies(got, want, scale_total=True, tol_total=1e-10):
+    w = {k: float(v) for k, v in want.items()}
+    comps = abs(w["e_near"]) + abs(w["e_far"]) + abs(w["e_self"]) + abs(w["e_periodic_far"])
+    denom = abs(w["e_total"]) if scale_total else comps
+    assert abs(got.e_total - w["e_total"]) <= tol_total * denom, (got.e_total, w["e_total"])
+    for k in ("e_near", "e_far", "e_self"):
+        assert abs(getattr(got, k) - w[k]) <= 1e-11 * max(abs(w[k]), 1e-300) + 1e-14 * comps, k
+    dp = abs(got.e_periodic_far - w["e_periodic_far"])
+    assert dp <= 1e-8 * abs(w["e_periodic_far"]) + 1e-12 * comps, (got.e_periodic_far, w["e_periodic_far"])
+
+
+def _load(name):
+    with open(os.path.join(HERE, "golden", name)) as f:
+        return json.load(f)
+
+
+def _system(case):
+    if case["kind"] == "random":
+        pos, src = inputs.random_system(case["n"], case["box_radius"], seed=case["seed"],
+                                        multipoles=case["multipoles"])
+    else:
+        pos, src, _, _ = inputs.make_config(case["config_index"])
+    assert hashlib.sha256(pos.tobytes() + src.tobytes()).hexdigest() == case["sha256"]
+    return pos, src
+
+
+GOLDEN = _load("golden.json")["systems"]
+GOLDEN_BIG = _load("golden_big.json")["systems"] if os.path.exists(
+    os.path.join(HERE, "golden", "golden_big.json")) else []
+
+
+@pytest.mark.parametrize("case", GOLDEN, ids=[c["name"] for c in GOLDEN])
+def test_golden_small(cuda, case):
+    pos, src = _system(case)
+    kw = dict(case["config"])
+    rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, case["box_radius"]), ankh.EwaldConfig(**kw))
+    # random test systems have strongly cancelling components; water boxes do not
+    check_energies(rep, case["energies"], scale_total=case["kind"] != "random")
+    offs, idx = ankh.build_tree_csr(pos, case["box_radius"], rep.depth)
+    assert hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest() == case["leaf_csr_sha256"]
+
+
+@pytest.mark.parametrize("case", [c for c in GOLDEN_BIG if c["kind"] == "config"],
+                         ids=[c["name"] for c in GOLDEN_BIG if c["kind"] == "config"])
+def test_golden_configs(cuda, case):
+    """BASELINE configs 0-2 (c2 at L = 3..6) against the reference's energies."""
+    pos, src = _system(case)
+    kw = dict(case["config"])
+    rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, case["box_radius"]), ankh.EwaldConfig(**kw))
+    check_energies(rep, case["energies"])
+    offs, idx = ankh.build_tree_csr(pos, case["box_radius"], rep.depth)
+    assert hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest() == case["leaf_csr_sha256"]
+
+
+@pytest.mark.parametrize("kw,n,rb,mp", [
+    (dict(order_cheb=4, order_equi=4, depth=2, p=15), 300, 5.0, True),
+    (dict(order_cheb=3, order_equi=3, depth=3, p=0), 900, 6.0, True),
+    (dict(order_cheb=5, order_equi=5, depth=1, p=2), 250, 4.0, False),
+    (dict(order_cheb=2, order_equi=2, depth=2, p=4), 200, 3.0, True),
+    (dict(order_cheb=7, order_equi=7, depth=1, p=2), 120, 3.0, True),
+    (dict(order_cheb=4, order_equi=4, depth=2, p=3, xi=0.5), 300, 4.0, True),  # z > 0.5 branch
+])
+def test_oracle_random(cuda, ref, kw, n, rb, mp):
+    pos, src = inputs.random_system(n, rb, seed=n + kw["order_cheb"], multipoles=mp)
+    want = ref.fmm_energy(pos, src, rb, threads=os.cpu_count(), **kw)
+    rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, rb), ankh.EwaldConfig(**kw))
+    check_energies(rep, want, scale_total=False)
+
+
+def test_mixed_moment_orders(cuda, ref):
+    """Some particles charge-only, some dipole-only, some full (moment_order 0/1/2)."""
+    pos, src = inputs.random_system(600, 5.0, seed=21, multipoles=True)
+    src[::3, 1:] = 0.0
+    src[1::3, 4:] = 0.0
+    kw = dict(order_cheb=4, order_equi=4, depth=2, p=15)
+    want = ref.fmm_energy(pos, src, 5.0, threads=os.cpu_count(), **kw)
+    rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 5.0), ankh.EwaldConfig(**kw))
+    check_energies(rep, want, scale_total=False)
+
+
+def test_large_leaves_chunking(cuda, ref):
+    """Leaves with more targets than threads and more sources than one staged chunk."""
+    pos, src = inputs.random_system(3000, 10.0, seed=8, multipoles=True)
+    kw = dict(order_cheb=3, order_equi=3, depth=1, p=2)
+    want = ref.fmm_energy(pos, src, 10.0, threads=os.cpu_count(), **kw)
+    rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 10.0), ankh.EwaldConfig(**kw))
+    check_energies(rep, want, scale_total=False)
+
+
+def test_leaf_csr_bit_exact(cuda, ref):
+    for seed, n, rb, depth in [(0, 5000, 4.0, 3), (1, 777, 1.0, 2), (2, 100, 2.5, 5)]:
+        pos, _ = inputs.random_system(n, rb, seed=seed)
+        pos[0] = [rb, rb, rb]
+        pos[1] = [-rb, -rb, -rb]
+        pos[2] = [0.0, rb, -rb]
+        offs, idx = ankh.build_tree_csr(pos, rb, depth)
+        o2, i2 = ref.leaf_csr(pos, rb, depth)
+        assert np.array_equal(offs, o2) and np.array_equal(idx, i2)
+
+
+def test_expansions_per_level(cuda, ref):
+    pos, src = inputs.random_system(2000, 6.0, seed=4, multipoles=True)
+    plan = ankh.Plan(2000, 6.0, ankh.EwaldConfig(order_cheb=5, order_equi=5, depth=3))
+    plan.energy(pos, src)
+    got = plan.expansions()
+    want = ref.expansions(pos, src, 6.0, 3, 5)
+    for l in range(4):
+        scale = np.abs(want[l]).max()
+        assert np.abs(got[l] - want[l]).max() <= 1e-13 * scale, l
+
+
+@pytest.mark.parametrize("L,level,offset", [(4, 2, (2, 0, 0)), (4, 3, (-3, 1, 2)), (5, 2, (0, -2, 3)),
+                                            (6, 2, (2, 1, 0)), (6, 3, (-3, -3, -3))])
+def test_m2l_factors(cuda, ref, L, level, offset):
+    """Plan factors reproduce the reference's truncated operator L^T R (the
+    SVD bits may differ; rank and subspace may not)."""
+    rb = 20.0
+    plan = ankh.Plan(600, rb, ankh.EwaldConfig(order_cheb=L, order_equi=L, depth=3))
+    lm, rm = plan.m2l_factors(level, offset)
+    rad = rb / (1 << level)
+    key = (offset[0] * 4096 + offset[1]) * 4096 + offset[2]
+    seed = (level * 0x100000001B3 + (key & ((1 << 64) - 1))) & ((1 << 64) - 1)
+    l2, r2 = ref.m2l_factors(L, rad, offset, seed=seed)
+    assert lm.shape == l2.shape
+    c = ref.m2l_dense(L, rad, offset)
+    assert np.abs(lm.T @ rm - l2.T @ r2).max() <= 1e-12 * np.abs(c).max()
+
+
+def test_deterministic_and_device_path(cuda):
+    torch = cuda
+    pos, src, rb, cfg = inputs.make_config(1)
+    plan = ankh.Plan(pos.shape[0], rb, ankh.EwaldConfig(order_cheb=4, order_equi=4))
+    a = plan.energy(pos, src)
+    b = plan.energy(pos, src)
+    assert a.e_total == b.e_total and a.e_near == b.e_near and a.e_far == b.e_far
+    dp, ds = torch.from_numpy(pos).cuda(), torch.from_numpy(src).cuda()
+    c = plan.energy_device(dp, ds)
+    assert c.e_total == a.e_total
+
+
+def test_quadratic_scaling_bitwise(cuda):
+    """E(2 s) = 4 E(s) exactly: every stage is bilinear in the moments and
+    scaling by 2 commutes with rounding (size-independent property)."""
+    pos, src, rb, _ = inputs.make_config(1)
+    plan = ankh.Plan(pos.shape[0], rb, ankh.EwaldConfig(order_cheb=4, order_equi=4))
+    a = plan.energy(pos, src)
+    b = plan.energy(pos, 2.0 * src)
+    for k in ("e_near", "e_far", "e_self", "e_periodic_far", "e_total"):
+        assert getattr(b, k) == 4.0 * getattr(a, k), k
+
+
+def test_polarization_identity(cuda):
+    """E(s1+s2) + E(s1-s2) = 2 E(s1) + 2 E(s2) (bilinearity) at config-1 size."""
+    pos, src, rb, _ = inputs.make_config(1)
+    rng = np.random.default_rng(5)
+    s2 = src * rng.uniform(0.5, 1.5, size=src.shape)
+    plan = ankh.Plan(pos.shape[0], rb, ankh.EwaldConfig(order_cheb=4, order_equi=4))
+    e = lambda s: plan.energy(pos, s).e_total
+    lhs = e(src + s2) + e(src - s2)
+    rhs = 2 * e(src) + 2 * e(s2)
+    assert abs(lhs - rhs) <= 1e-12 * (abs(lhs) + abs(rhs))
+
+
+def test_permutation_invariance(cuda):
+    pos, src, rb, _ = inputs.make_config(0)
+    perm = np.random.default_rng(1).permutation(pos.shape[0])
+    cfg = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    a = ankh.fmm_energy(ankh.ParticleSystem(pos, src, rb), cfg)
+    b = ankh.fmm_energy(ankh.ParticleSystem(pos[perm], src[perm], rb), cfg)
+    assert rel(b.e_total, a.e_total) < 1e-13
+
+
+def test_config4_style_rescaled_dipoles(cuda, ref):
+    """Repeated evaluations with dipoles rescaled (config 4 pattern) on one plan."""
+    pos, src = inputs.random_system(1500, 6.0, seed=44, multipoles=True)
+    kw = dict(order_cheb=5, order_equi=5, depth=2)
+    plan = ankh.Plan(1500, 6.0, ankh.EwaldConfig(**kw))
+    for f in inputs.rescale_factors(1004, 3):
+        s = src.copy()
+        s[:, 1:4] *= f
+        want = ref.fmm_energy(pos, s, 6.0, threads=os.cpu_count(), **kw)
+        check_energies(plan.energy(pos, s), want, scale_total=False)
+
+
+# ------------------------------------------------------------ error semantics
+def _expect(exc, msg, pos, src, rb=1.0, **kw):
+    with pytest.raises(exc, match=msg):
+        ankh.fmm_energy(ankh.ParticleSystem(np.asarray(pos, float), np.asarray(src, float), rb),
+                        ankh.EwaldConfig(**kw))
+
+
+def test_errors(cuda):
+    q = [[1.0] + [0.0] * 9, [-1.0] + [0.0] * 9, [0.5] + [0.0] * 9]
+    ok = [[0.1, 0.2, 0.3], [-0.4, 0.5, 0.1], [0.7, -0.7, 0.0]]
+    _expect(ankh.InvalidArgument, "^xi must be positive$", ok, q, xi=0.0)
+    _expect(ankh.InvalidArgument, "^order_cheb must be >= 2$", ok, q, order_cheb=1)
+    _expect(ankh.InvalidArgument, "^svd_tol must lie in", ok, q, svd_tol=1.0)
+    _expect(ankh.InvalidArgument, "invalid system: box_radius must be positive", ok, q, rb=0.0)
+    bad = [row[:] for row in ok]
+    bad[2] = [2.0, 0, 0]
+    nan = [row[:] for row in ok]
+    nan[1] = [float("nan"), 0, 0]
+    # first violation in index order wins (types.cpp:29-44)
+    _expect(ankh.InvalidArgument, "invalid system: outside box$", bad, q)
+    _expect(ankh.InvalidArgument, "invalid system: non-finite coordinate or moment$", nan, q)
+    both = [row[:] for row in nan]
+    both[0] = [5.0, 0, 0]
+    _expect(ankh.InvalidArgument, "invalid system: outside box$", both, q)
+    dup = [ok[0], ok[1], ok[0]]
+    _expect(ankh.InvalidArgument, "invalid system: duplicate position$", dup, q, p=0)
+    _expect(ankh.InvalidArgument, "^build_tree: depth must be in \\[1, 8\\]$", ok, q, depth=9)
+    # a system violation outranks the depth error (fmm.cpp:385-398)
+    _expect(ankh.InvalidArgument, "duplicate position$", dup, q, depth=9)
+    _expect(ankh.InvalidArgument, "^DiffOperator: order out of range$", ok, q, order_cheb=65)
+    # x = -r_B and x = +r_B coincide under a +-2 r_B image (kernel.cpp:161)
+    img = [[-1.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.5, 0.5]]
+    _expect(ankh.DomainError, "^pair_interaction: coincident points$", img, q, depth=2)
+
+
+def test_empty_and_single(cuda):
+    r = ankh.fmm_energy(ankh.ParticleSystem(np.zeros((0, 3)), np.zeros((0, 10)), 1.0))
+    assert r.e_total == 0.0
+    r = ankh.fmm_energy(ankh.ParticleSystem(np.zeros((1, 3)), np.array([[1.0] + [0.0] * 9]), 1.0),
+                        ankh.EwaldConfig(order_cheb=4, order_equi=4, p=0))
+    assert rel(r.e_self, -0.01 / np.sqrt(np.pi)) < 1e-15 and r.e_near == 0.0
