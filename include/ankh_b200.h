@@ -140,6 +140,21 @@ int ankh_leaf_csr_v1(size_t n, const double* positions, double box_radius, int d
 int ankh_plan_m2l_factors_v1(ankh_plan_v1* plan, int level, const int* offset, double* lmat,
                              double* rmat, int max_rank, int* rank, char* err, size_t errlen);
 
+/* ---- spatial sharding (host only; no device needed) ----
+ * Shards own contiguous Morton ranges of leaves; a level-l cell belongs to the
+ * shard owning its first descendant leaf.  P2P work is owned by the target
+ * leaf, M2L work by the target cell of the reference's canonical instance
+ * (fmm.cpp:246-250), so each unordered pair / instance is counted once. */
+int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* morton_begin,
+                             int64_t* morton_end);
+int ankh_shard_cell_owner_v1(int level, uint32_t lex_cell, int depth, int world);
+/* Canonical M2L instances (level, t, s, offset[3]) owned by `rank` (rank < 0:
+ * all), in the plan's grouping order.  `*count` receives the total; at most
+ * `capacity` entries are written (pass 0 to query the count). */
+int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, uint32_t* level,
+                                uint32_t* t, uint32_t* s, int32_t* offset, size_t capacity,
+                                size_t* count);
+
 /* Measured FP64 (DFMA) throughput of the current device in TFLOP/s: the
  * roofline denominator for the FP64-bound kernels (no reference counterpart). */
 double ankh_probe_fp64_tflops_v1(int iters);

@@ -27,6 +27,9 @@ EXPORTS = [
     "ankh_version_v1",
     "ankh_plan_energies_device_v1",
     "ankh_probe_fp64_tflops_v1",
+    "ankh_shard_leaf_range_v1",
+    "ankh_shard_cell_owner_v1",
+    "ankh_shard_m2l_instances_v1",
 ]
 
 
@@ -71,6 +74,11 @@ def lib() -> ctypes.CDLL:
         L.ankh_plan_energies_device_v1.argtypes = [c_void_p, c_void_p, c_void_p, cp, c_size_t]
         L.ankh_probe_fp64_tflops_v1.argtypes = [c_int]
         L.ankh_probe_fp64_tflops_v1.restype = c_double
+        I64 = ctypes.POINTER(ctypes.c_int64)
+        L.ankh_shard_leaf_range_v1.argtypes = [c_int, c_int, c_int, I64, I64]
+        L.ankh_shard_cell_owner_v1.argtypes = [c_int, ctypes.c_uint32, c_int, c_int]
+        L.ankh_shard_m2l_instances_v1.argtypes = [c_int, c_int, c_int, c_int, U32, U32, U32, I,
+                                                  c_size_t, ctypes.POINTER(c_size_t)]
         L.ankh_version_v1.argtypes = []
         L.ankh_version_v1.restype = ctypes.c_char_p
         _lib = L

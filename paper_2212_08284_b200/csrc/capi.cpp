@@ -6,6 +6,7 @@
 #include <mutex>
 
 #include "plan.hpp"
+#include "shard.hpp"
 
 using ankh_b200::AnkhError;
 using ankh_b200::Plan;
@@ -215,6 +216,42 @@ int ankh_plan_energies_device_v1(ankh_plan_v1* plan, double* d_out, void* stream
     std::lock_guard<std::mutex> lock(plan->mu);
     plan->plan->energies_to_device(d_out, static_cast<cudaStream_t>(stream));
   });
+}
+
+int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* begin, int64_t* end) {
+  if (depth < 1 || depth > 8 || world < 1 || rank < 0 || rank >= world || !begin || !end)
+    return ANKH_INVALID_ARGUMENT;
+  ankh_b200::shard_leaf_range(depth, rank, world, begin, end);
+  return ANKH_OK;
+}
+
+int ankh_shard_cell_owner_v1(int level, uint32_t cell, int depth, int world) {
+  if (level < 0 || level > depth || depth > 8 || world < 1) return -1;
+  return ankh_b200::shard_cell_owner(level, cell, depth, world);
+}
+
+int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, uint32_t* level,
+                                uint32_t* t, uint32_t* s, int32_t* offset, size_t capacity,
+                                size_t* count) {
+  if (depth < 1 || depth > 8 || world < 1 || rank >= world || !count) return ANKH_INVALID_ARGUMENT;
+  try {
+    const auto groups = ankh_b200::enumerate_m2l(depth, periodic != 0, rank, world, 0);
+    size_t c = 0;
+    for (const auto& g : groups) {
+      for (size_t k = 0; k < g.t.size(); ++k, ++c) {
+        if (c >= capacity) continue;
+        if (level) level[c] = static_cast<uint32_t>(g.level);
+        if (t) t[c] = g.t[k];
+        if (s) s[c] = g.s[k];
+        if (offset)
+          for (int a = 0; a < 3; ++a) offset[3 * c + a] = g.offset[a];
+      }
+    }
+    *count = c;
+    return ANKH_OK;
+  } catch (...) {
+    return ANKH_RUNTIME_ERROR;
+  }
 }
 
 double ankh_probe_fp64_tflops_v1(int iters) {

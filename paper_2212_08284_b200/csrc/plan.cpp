@@ -11,6 +11,7 @@
 #include <set>
 
 #include "host_numerics.hpp"
+#include "shard.hpp"
 
 namespace ankh_b200 {
 
@@ -111,9 +112,10 @@ void* Plan::dalloc(std::size_t bytes) {
 
 void Plan::build_geometry() {
   // leaf ownership: contiguous Morton ranges
-  const long long nl = n_leaves;
-  leaf_begin_ = static_cast<int>(nl * cfg.rank / cfg.world);
-  leaf_end_ = static_cast<int>(nl * (cfg.rank + 1) / cfg.world);
+  std::int64_t lb = 0, le = 0;
+  shard_leaf_range(depth, cfg.rank, cfg.world, &lb, &le);
+  leaf_begin_ = static_cast<int>(lb);
+  leaf_end_ = static_cast<int>(le);
   include_self_ = cfg.rank == 0;
   // P2P polynomial length from the largest possible near distance
   // (2 leaf sides per axis): s_max = xi^2 (2 sqrt(3) * 2 r_B / n)^2
@@ -184,49 +186,19 @@ void Plan::build_m2l() {
     std::vector<uint2> inst;
     Factors f;
   };
-  std::vector<OffsetWork> work;
-  for (int level = 1; level <= depth; ++level)
-    for (int ox = -3; ox <= 3; ++ox)
-      for (int oy = -3; oy <= 3; ++oy)
-        for (int oz = -3; oz <= 3; ++oz)
-          if (std::max({std::abs(ox), std::abs(oy), std::abs(oz)}) >= 2)
-            work.push_back({level, {ox, oy, oz}, {}, {}});
   const int threads = cfg.threads;
-  // instance enumeration: Lambda(t) offsets are s - t in [-2-c, 3-c] per axis,
-  // c = t & 1 (octree.cpp:79-87); canonical iff t < s or (t == s and image
-  // lex-positive) (fmm.cpp:246-250)
-  parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
-    OffsetWork& w = work[wi];
-    const int nl = 1 << w.level;
-    int lo[3], hi[3], step[3];
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = 0;
-      hi[a] = nl;
-      step[a] = 1;
-      if (w.o[a] == 3) step[a] = 2;                 // only even t_a
-      if (w.o[a] == -3) { lo[a] = 1; step[a] = 2; }  // only odd t_a
-    }
-    for (int tx = lo[0]; tx < hi[0]; tx += step[0])
-      for (int ty = lo[1]; ty < hi[1]; ty += step[1])
-        for (int tz = lo[2]; tz < hi[2]; tz += step[2]) {
-          const int ext[3] = {tx + w.o[0], ty + w.o[1], tz + w.o[2]};
-          int in[3], img[3];
-          bool ok = true;
-          for (int a = 0; a < 3; ++a) {
-            if (!periodic && (ext[a] < 0 || ext[a] >= nl)) ok = false;
-            img[a] = ext[a] >= 0 ? ext[a] / nl : -((-ext[a] + nl - 1) / nl);
-            in[a] = ext[a] - nl * img[a];
-          }
-          if (!ok) continue;
-          const unsigned t = static_cast<unsigned>((tx * nl + ty) * nl + tz);
-          const unsigned s = static_cast<unsigned>((in[0] * nl + in[1]) * nl + in[2]);
-          bool lexpos = img[0] != 0 ? img[0] > 0 : (img[1] != 0 ? img[1] > 0 : img[2] > 0);
-          if (t < s || (t == s && lexpos)) w.inst.push_back(make_uint2(t, s));
-        }
-  });
-  work.erase(std::remove_if(work.begin(), work.end(),
-                            [](const OffsetWork& w) { return w.inst.empty(); }),
-             work.end());
+  // canonical instances owned by this shard (shard.cpp, fmm.cpp:244-253)
+  std::vector<OffsetInstances> groups =
+      enumerate_m2l(depth, periodic, cfg.world > 1 ? cfg.rank : -1, cfg.world, threads);
+  std::vector<OffsetWork> work(groups.size());
+  for (std::size_t i = 0; i < groups.size(); ++i) {
+    work[i].level = groups[i].level;
+    work[i].o = groups[i].offset;
+    work[i].inst.resize(groups[i].t.size());
+    for (std::size_t k = 0; k < groups[i].t.size(); ++k)
+      work[i].inst[k] = make_uint2(groups[i].t[k], groups[i].s[k]);
+  }
+  groups.clear();
   // factors: exact SVD path uses the signed-permutation symmetry of the block
   // (one SVD per class, SURVEY.md Decision 3); K > 150 replicates the
   // reference's seeded randomized path per offset.
@@ -308,21 +280,8 @@ void Plan::build_m2l() {
   m2l_operators = work.size();
   m2l_rank_mean = work.empty() ? 0.0 : rank_sum / work.size();
   n_tiles_ = static_cast<int>(tiles.size());
-  // ownership of tiles: cost-weighted contiguous split across shards
-  std::vector<double> cost(tiles.size());
-  double total_cost = 0.0;
-  for (std::size_t i = 0; i < tiles.size(); ++i) {
-    cost[i] = static_cast<double>(h_ops_[tiles[i].op].kp) * tiles[i].count;
-    total_cost += cost[i];
-  }
-  std::vector<int> owned;
-  double run = 0.0;
-  for (std::size_t i = 0; i < tiles.size(); ++i) {
-    const double mid = run + 0.5 * cost[i];
-    run += cost[i];
-    const int owner = total_cost > 0 ? std::min(cfg.world - 1, static_cast<int>(mid / total_cost * cfg.world)) : 0;
-    if (owner == cfg.rank) owned.push_back(static_cast<int>(i));
-  }
+  std::vector<int> owned(tiles.size());
+  std::iota(owned.begin(), owned.end(), 0);
   // group owned tiles by kp class
   class_range_.assign(kMaxKp8 + 1, {0, 0});
   std::vector<int> ids;

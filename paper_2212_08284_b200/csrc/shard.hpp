@@ -1,0 +1,42 @@
+// Spatial sharding and M2L instance enumeration (host only, no CUDA).
+//
+// Shards own contiguous Morton ranges of leaves.  A level-l
+// cell belongs to the shard that owns its first descendant leaf, so for
+// world | 8 every shard owns whole level-1 subtrees.  P2P work is owned by
+// the target leaf, M2L work by the target cell t of the reference's canonical
+// instance (t, s, image) (fmm.cpp:246-250); every unordered pair / instance is
+// therefore counted by exactly one shard.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+namespace ankh_b200 {
+
+/// Interleave (x, y, z) bits: x in bit 3k+2, y in 3k+1, z in 3k.
+std::uint32_t morton3(std::uint32_t x, std::uint32_t y, std::uint32_t z);
+
+/// Morton leaf range [begin, end) owned by `rank` of `world` at `depth`.
+void shard_leaf_range(int depth, int rank, int world, std::int64_t* begin, std::int64_t* end);
+
+/// Owner shard of lex cell `cell` at `level` in a depth-`depth` tree.
+int shard_cell_owner(int level, std::uint32_t cell, int depth, int world);
+
+/// Canonical M2L instances of one (level, offset): Lambda(t) offsets are
+/// s - t in [-2-c, 3-c] per axis with c = t & 1 (octree.cpp:79-87), wrapped
+/// with split_extended (octree.cpp:11-14) when periodic, kept iff
+/// t < s or (t == s and image lex-positive) (fmm.cpp:246-250).  Only targets
+/// owned by `rank` are returned (rank < 0: all), as (t, s) pairs in lex t order.
+struct OffsetInstances {
+  int level = 0;
+  std::array<int, 3> offset{};
+  std::vector<std::uint32_t> t, s;
+};
+void enumerate_offset(OffsetInstances& w, bool periodic, int depth, int rank, int world);
+
+/// All (level, offset) groups with at least one instance owned by `rank`.
+std::vector<OffsetInstances> enumerate_m2l(int depth, bool periodic, int rank, int world,
+                                           int threads);
+
+}  // namespace ankh_b200
