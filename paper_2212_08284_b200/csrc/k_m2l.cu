@@ -17,13 +17,31 @@ namespace ankh_b200 {
 
 namespace {
 
-constexpr int kThreads = 256;          // 8 warps x 8 instances
-constexpr int kStride = kM2LChunk + 4; // smem row stride (doubles): conflict-free fragments
+constexpr int kThreads = 256;           // 8 warps x 8 instances
+constexpr int kChunk = 16;              // node columns per pipeline stage
+constexpr int kStride = kChunk + 4;     // smem row stride (doubles): conflict-free fragments
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
 template <int KP8>
@@ -36,56 +54,62 @@ __global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp
                                                   const uint2* __restrict__ inst, int K, int Kp,
                                                   double* __restrict__ far_partial) {
   constexpr int kp = 8 * KP8;
-  extern __shared__ double sm[];
-  double* sL = sm;                       // kp x kStride
-  double* sR = sL + kp * kStride;        // kp x kStride
-  double* sT = sR + kp * kStride;        // 64 x kStride (targets)
-  double* sS = sT + kM2LTile * kStride;  // 64 x kStride (sources)
+  constexpr int kStage = (2 * kp + 2 * kM2LTile) * kStride;  // doubles per pipeline stage
+  extern __shared__ __align__(16) double sm[];
   __shared__ double red[kThreads / 32];
+  __shared__ uint2 s_inst[kM2LTile];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile_index = tile_ids[blockIdx.x];
   const M2LTile tile = tiles[tile_index];
   const M2LOp op = ops[tile.op];
   const double* Lg = factors + op.factor_off;
-  const double* Rg = Lg + static_cast<long long>(op.kp) * Kp;
+  const double* Rg = Lg + static_cast<long long>(kp) * Kp;
   const double* E = exp + level_off[tile.level];
+  if (tid < kM2LTile) s_inst[tid] = tid < tile.count ? inst[tile.begin + tid] : make_uint2(0u, 0u);
+  __syncthreads();
+
+  // stage chunk [k0, k0 + kChunk) of L, R and the 64 target / source expansions
+  auto issue = [&](int k0, double* st) {
+    double* sL = st;
+    double* sR = sL + kp * kStride;
+    double* sT = sR + kp * kStride;
+    double* sS = sT + kM2LTile * kStride;
+    for (int w = tid; w < kp * (kChunk / 2); w += kThreads) {
+      const int r = w / (kChunk / 2), c = 2 * (w - (kChunk / 2) * (w / (kChunk / 2)));
+      cp_async16(sL + r * kStride + c, Lg + static_cast<long long>(r) * Kp + k0 + c);
+      cp_async16(sR + r * kStride + c, Rg + static_cast<long long>(r) * Kp + k0 + c);
+    }
+    for (int w = tid; w < kM2LTile * kChunk; w += kThreads) {
+      const int q = w / kChunk, c = w - kChunk * (w / kChunk);
+      const int k = k0 + c;
+      const bool ok = q < tile.count && k < K;
+      const uint2 ts = s_inst[q];
+      cp_async8(sT + q * kStride + c, ok ? E + static_cast<long long>(ts.x) * K + k : E, ok);
+      cp_async8(sS + q * kStride + c, ok ? E + static_cast<long long>(ts.y) * K + k : E, ok);
+    }
+  };
 
   double u[KP8][2], v[KP8][2];
 #pragma unroll
   for (int m = 0; m < KP8; ++m) u[m][0] = u[m][1] = v[m][0] = v[m][1] = 0.0;
 
   const int row = lane >> 2, col = lane & 3;
-  for (int k0 = 0; k0 < Kp; k0 += kM2LChunk) {
-    // stage factor columns [k0, k0+32) of L and R (rows beyond op.kp are zero)
-    for (int w = tid; w < kp * kM2LChunk; w += kThreads) {
-      const int r = w / kM2LChunk, c = w - kM2LChunk * (w / kM2LChunk);
-      double lv = 0.0, rv = 0.0;
-      if (r < op.kp) {
-        lv = __ldg(Lg + static_cast<long long>(r) * Kp + k0 + c);
-        rv = __ldg(Rg + static_cast<long long>(r) * Kp + k0 + c);
-      }
-      sL[r * kStride + c] = lv;
-      sR[r * kStride + c] = rv;
-    }
-    // stage expansion columns of the 64 target and source cells
-    for (int w = tid; w < kM2LTile * kM2LChunk; w += kThreads) {
-      const int q = w / kM2LChunk, c = w - kM2LChunk * (w / kM2LChunk);
-      const int k = k0 + c;
-      double tv = 0.0, sv = 0.0;
-      if (q < tile.count && k < K) {
-        const uint2 ts = inst[tile.begin + q];
-        tv = __ldg(E + static_cast<long long>(ts.x) * K + k);
-        sv = __ldg(E + static_cast<long long>(ts.y) * K + k);
-      }
-      sT[q * kStride + c] = tv;
-      sS[q * kStride + c] = sv;
-    }
+  const int nchunks = Kp / kChunk;
+  issue(0, sm);
+  cp_commit();
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) issue((c + 1) * kChunk, sm + ((c + 1) & 1) * kStage);
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    const double* bT = sT + (warp * 8 + row) * kStride + col;
-    const double* bS = sS + (warp * 8 + row) * kStride + col;
+    const double* st = sm + (c & 1) * kStage;
+    const double* sL = st;
+    const double* sR = sL + kp * kStride;
+    const double* bT = sR + kp * kStride + (warp * 8 + row) * kStride + col;
+    const double* bS = bT + kM2LTile * kStride;
 #pragma unroll
-    for (int ks = 0; ks < kM2LChunk / 4; ++ks) {
+    for (int ks = 0; ks < kChunk / 4; ++ks) {
       const double bt = bT[4 * ks];
       const double bs = bS[4 * ks];
 #pragma unroll
@@ -117,7 +141,7 @@ template <int KP8>
 void launch_class(const double* exp, const long long* level_off, const double* factors,
                   const M2LOp* ops, const M2LTile* tiles, int n_tiles, const int* tile_ids,
                   const uint2* inst, int K, int Kp, double* far_partial, cudaStream_t st) {
-  const std::size_t smem = sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
+  const std::size_t smem = 2 * sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_m2l<KP8>, cudaFuncAttributeMaxDynamicSharedMemorySize,

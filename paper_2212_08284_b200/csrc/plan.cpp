@@ -122,6 +122,9 @@ void Plan::build_geometry() {
   const double side = 2.0 * rb / nax;
   const double dmax = 2.0 * std::sqrt(3.0) * side * 1.0001;
   nterms_ = p2p_terms_for(cfg.xi * cfg.xi * dmax * dmax);
+  // CTA size: 128 threads (4 CTAs/SM) for ~32-atom leaves, 256 for denser leaves
+  const double per_leaf = static_cast<double>(n) / n_leaves;
+  p2p_tpb_ = per_leaf <= 36.0 ? 128 : 256;
 }
 
 void Plan::allocate() {
@@ -385,7 +388,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st)
   }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
   // near field: P2P (fmm.cpp:278-327)
-  launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, leaf_begin_,
+  launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_, leaf_begin_,
              leaf_end_, d_near_part_, d_pair_count_, d_res_, st);
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));

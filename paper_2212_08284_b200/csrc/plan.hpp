@@ -126,6 +126,7 @@ class Plan {
   DevResult* d_res_ = nullptr;
   DevResult* h_res_ = nullptr;
   int nterms_ = 14;
+  int p2p_tpb_ = 256;
   std::uint32_t launches_ = 0;
   // timing
   cudaEvent_t ev_[8] = {};
