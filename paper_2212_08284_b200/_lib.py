@@ -7,7 +7,8 @@ import os
 from typing import Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libankh_b200.so")
+# ANKH_B200_LIB selects an alternative in-tree build (kernel A/B experiments)
+LIB_PATH = os.environ.get("ANKH_B200_LIB") or os.path.join(HERE, "libankh_b200.so")
 
 _lib: Optional[ctypes.CDLL] = None
 

@@ -20,6 +20,141 @@ namespace ankh_b200 {
 namespace {
 
 constexpr int kP2MThreads = 128;
+constexpr int kP2MWarps = kP2MThreads / 32;
+
+// Warp-per-leaf P2M.  Each lane first evaluates the 1-D bases of one particle
+// (S^(n) = radius^-n (H D^n) T(local) for the 3 axes) and folds the moments
+// into the z factors:
+//   W0[jk] = y0[j] A0[k] + y1[j] A1[k] + y2[j] A2[k],
+//     A0 = q z0 + mu_z z1 + Th_zz z2,  A1 = mu_y z0 + 2 Th_yz z1,  A2 = Th_yy z0
+//   W1[jk] = y0[j] B0[k] + y1[j] B1[k],  B0 = mu_x z0 + 2 Th_xz z1,  B1 = 2 Th_xy z0
+//   W2[jk] = y0[j] C0[k],                C0 = Th_xx z0
+// (the 10 terms of chebyshev.cpp:173-200 regrouped by derivative order);
+// then lanes own (j, k) columns and accumulate Q[i, jk] += sum_m Sx_m[i] W_m[jk]
+// over the leaf's particles in registers.  No CTA barriers.
+template <int L>
+struct P2MWShape {
+  static constexpr int L2 = L * L, K = L2 * L;
+  static constexpr int QJ = (L2 + 31) / 32;       // (j,k) columns per lane
+  static constexpr int PER = 12 * L;              // staged doubles per particle
+  static constexpr std::size_t smem_doubles = 3 * L2 + kP2MWarps * 32 * PER;
+};
+
+template <int L>
+__global__ void __launch_bounds__(kP2MThreads) k_p2m_w(const double* __restrict__ part,
+                                                       const unsigned* __restrict__ leaf_off,
+                                                       int depth, double rb,
+                                                       const double* __restrict__ hd_g,
+                                                       double* __restrict__ exp_leaf) {
+  using Sh = P2MWShape<L>;
+  constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER;
+  extern __shared__ double sm[];
+  double* hd = sm;  // 3 L^2
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // per particle: sx[3][L] | sy[3][L] | A0 A1 A2 B0 B1 C0 [L]
+  double* st = hd + 3 * L2 + warp * 32 * PER;
+  for (int w = threadIdx.x; w < 3 * L2; w += kP2MThreads) hd[w] = hd_g[w];
+  __syncthreads();
+  const int n = 1 << depth;
+  const unsigned n_leaves = 1u << (3 * depth);
+  const unsigned leaf = blockIdx.x * kP2MWarps + warp;
+  if (leaf >= n_leaves) return;
+  const unsigned begin = leaf_off[leaf];
+  const int cnt = static_cast<int>(leaf_off[leaf + 1] - begin);
+  double* out = exp_leaf + static_cast<std::size_t>(leaf) * K;
+  // cell_geometry (octree.cpp:18-25)
+  const double rad = rb / n;
+  const int ci0 = static_cast<int>(leaf) / (n * n), ci1 = (static_cast<int>(leaf) / n) % n,
+            ci2 = static_cast<int>(leaf) % n;
+  const double c0 = -rb + rad * (2 * ci0 + 1), c1 = -rb + rad * (2 * ci1 + 1),
+               c2 = -rb + rad * (2 * ci2 + 1);
+  const double inv_rad = 1.0 / rad;
+
+  double acc[Sh::QJ][L];
+  int jj[Sh::QJ], kk[Sh::QJ];
+#pragma unroll
+  for (int q = 0; q < Sh::QJ; ++q) {
+    const int jk = min(lane + 32 * q, L2 - 1);
+    jj[q] = jk / L;
+    kk[q] = jk - L * (jk / L);
+#pragma unroll
+    for (int i = 0; i < L; ++i) acc[q][i] = 0.0;
+  }
+
+  for (int p0 = 0; p0 < cnt; p0 += 32) {
+    const int pc = min(32, cnt - p0);
+    __syncwarp();
+    if (lane < pc) {
+      const double2* r = reinterpret_cast<const double2*>(part + static_cast<std::size_t>(begin + p0 + lane) * kRec);
+      const double2 v0 = __ldg(r), v1 = __ldg(r + 1), v2 = __ldg(r + 2), v3 = __ldg(r + 3),
+                    v4 = __ldg(r + 4), v5 = __ldg(r + 5), v6 = __ldg(r + 6);
+      const double q = v1.y, mx = v2.x, my = v2.y, mz = v3.x, txx = v3.y, txy = v4.x,
+                   txz = v4.y, tyy = v5.x, tyz = v5.y, tzz = v6.x;
+      const double loc[3] = {(v0.x - c0) * inv_rad, (v0.y - c1) * inv_rad, (v1.x - c2) * inv_rad};
+      double* dst = st + lane * PER;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        double t[L];
+        t[0] = 1.0;
+        if (L > 1) t[1] = loc[ax];
+#pragma unroll
+        for (int m = 2; m < L; ++m) t[m] = 2.0 * loc[ax] * t[m - 1] - t[m - 2];
+        double b[3][L];
+        double scale = 1.0;
+#pragma unroll
+        for (int nd = 0; nd < 3; ++nd) {
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            double v = 0.0;
+#pragma unroll
+            for (int m = 0; m < L; ++m) v += hd[nd * L2 + i * L + m] * t[m];
+            b[nd][i] = scale * v;
+          }
+          scale *= inv_rad;
+        }
+        if (ax < 2) {
+#pragma unroll
+          for (int nd = 0; nd < 3; ++nd)
+#pragma unroll
+            for (int i = 0; i < L; ++i) dst[(ax * 3 + nd) * L + i] = b[nd][i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            const double z0 = b[0][i], z1 = b[1][i], z2 = b[2][i];
+            dst[6 * L + i] = q * z0 + mz * z1 + tzz * z2;             // A0
+            dst[7 * L + i] = my * z0 + (2.0 * tyz) * z1;              // A1
+            dst[8 * L + i] = tyy * z0;                                // A2
+            dst[9 * L + i] = mx * z0 + (2.0 * txz) * z1;              // B0
+            dst[10 * L + i] = (2.0 * txy) * z0;                       // B1
+            dst[11 * L + i] = txx * z0;                               // C0
+          }
+        }
+      }
+    }
+    __syncwarp();
+    for (int p = 0; p < pc; ++p) {
+      const double* s = st + p * PER;
+#pragma unroll
+      for (int q = 0; q < Sh::QJ; ++q) {
+        const int j = jj[q], k = kk[q];
+        const double y0 = s[3 * L + j], y1 = s[4 * L + j], y2 = s[5 * L + j];
+        const double w0 = y0 * s[6 * L + k] + y1 * s[7 * L + k] + y2 * s[8 * L + k];
+        const double w1 = y0 * s[9 * L + k] + y1 * s[10 * L + k];
+        const double w2 = y0 * s[11 * L + k];
+#pragma unroll
+        for (int i = 0; i < L; ++i) acc[q][i] += s[i] * w0 + s[L + i] * w1 + s[2 * L + i] * w2;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < Sh::QJ; ++q) {
+    const int jk = lane + 32 * q;
+    if (jk < L2) {
+#pragma unroll
+      for (int i = 0; i < L; ++i) out[i * L2 + jk] = acc[q][i];
+    }
+  }
+}
 
 template <int L>
 struct P2MShape {
@@ -230,15 +365,30 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
 template <int L>
 void p2m_order(const double* part, const unsigned* leaf_off, int depth, double rb,
                const double* hd, double* exp_leaf, const DevResult* res, cudaStream_t st) {
-  const std::size_t smem = sizeof(double) * P2MShape<L>::smem_doubles;
+  if (L > 6) {  // register budget of the warp-per-leaf variant: block-per-leaf instead
+    const std::size_t smem = sizeof(double) * P2MShape<L>::smem_doubles;
+    static bool attr_b = false;
+    if (!attr_b) {
+      cudaFuncSetAttribute(k_p2m<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      attr_b = true;
+    }
+    k_p2m<L><<<1u << (3 * depth), kP2MThreads, smem, st>>>(part, leaf_off, depth, rb, hd, exp_leaf,
+                                                           res);
+    return;
+  }
+  constexpr int LW = L > 6 ? 6 : L;  // (never launched with L > 6)
+  const std::size_t smem = sizeof(double) * P2MWShape<LW>::smem_doubles;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_p2m<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_p2m_w<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
   const unsigned leaves = 1u << (3 * depth);
-  k_p2m<L><<<leaves, kP2MThreads, smem, st>>>(part, leaf_off, depth, rb, hd, exp_leaf, res);
+  k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(part, leaf_off,
+                                                                             depth, rb, hd,
+                                                                             exp_leaf);
 }
 
 template <int L>
