@@ -41,7 +41,7 @@ struct P2MWShape {
 };
 
 template <int L>
-__global__ void __launch_bounds__(kP2MThreads) k_p2m_w(const double* __restrict__ part,
+__global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restrict__ part,
                                                        const unsigned* __restrict__ leaf_off,
                                                        int depth, double rb,
                                                        const double* __restrict__ hd_g,
@@ -90,43 +90,58 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m_w(const double* __restrict_
                     v4 = __ldg(r + 4), v5 = __ldg(r + 5), v6 = __ldg(r + 6);
       const double q = v1.y, mx = v2.x, my = v2.y, mz = v3.x, txx = v3.y, txy = v4.x,
                    txz = v4.y, tyy = v5.x, tyz = v5.y, tzz = v6.x;
-      const double loc[3] = {(v0.x - c0) * inv_rad, (v0.y - c1) * inv_rad, (v1.x - c2) * inv_rad};
+      const double lx = (v0.x - c0) * inv_rad, ly = (v0.y - c1) * inv_rad,
+                   lz = (v1.x - c2) * inv_rad;
       double* dst = st + lane * PER;
+      double tx[L], ty[L], tz[L];
+      tx[0] = ty[0] = tz[0] = 1.0;
+      if (L > 1) {
+        tx[1] = lx;
+        ty[1] = ly;
+        tz[1] = lz;
+      }
 #pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        double t[L];
-        t[0] = 1.0;
-        if (L > 1) t[1] = loc[ax];
+      for (int m = 2; m < L; ++m) {
+        tx[m] = 2.0 * lx * tx[m - 1] - tx[m - 2];
+        ty[m] = 2.0 * ly * ty[m - 1] - ty[m - 2];
+        tz[m] = 2.0 * lz * tz[m - 1] - tz[m - 2];
+      }
+      double scale = 1.0;
 #pragma unroll
-        for (int m = 2; m < L; ++m) t[m] = 2.0 * loc[ax] * t[m - 1] - t[m - 2];
-        double b[3][L];
-        double scale = 1.0;
+      for (int nd = 0; nd < 3; ++nd) {
+        double zb[L];
 #pragma unroll
-        for (int nd = 0; nd < 3; ++nd) {
+        for (int i = 0; i < L; ++i) {
+          double vx = 0.0, vy = 0.0, vz = 0.0;
 #pragma unroll
-          for (int i = 0; i < L; ++i) {
-            double v = 0.0;
-#pragma unroll
-            for (int m = 0; m < L; ++m) v += hd[nd * L2 + i * L + m] * t[m];
-            b[nd][i] = scale * v;
+          for (int m = 0; m < L; ++m) {
+            const double h = hd[nd * L2 + i * L + m];
+            vx += h * tx[m];
+            vy += h * ty[m];
+            vz += h * tz[m];
           }
-          scale *= inv_rad;
+          dst[nd * L + i] = scale * vx;            // x basis S^(nd)
+          dst[(3 + nd) * L + i] = scale * vy;      // y basis
+          zb[i] = scale * vz;
         }
-        if (ax < 2) {
+        scale *= inv_rad;
+        // fold the moments into the z factors (A0 A1 A2 B0 B1 C0)
 #pragma unroll
-          for (int nd = 0; nd < 3; ++nd)
-#pragma unroll
-            for (int i = 0; i < L; ++i) dst[(ax * 3 + nd) * L + i] = b[nd][i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < L; ++i) {
-            const double z0 = b[0][i], z1 = b[1][i], z2 = b[2][i];
-            dst[6 * L + i] = q * z0 + mz * z1 + tzz * z2;             // A0
-            dst[7 * L + i] = my * z0 + (2.0 * tyz) * z1;              // A1
-            dst[8 * L + i] = tyy * z0;                                // A2
-            dst[9 * L + i] = mx * z0 + (2.0 * txz) * z1;              // B0
-            dst[10 * L + i] = (2.0 * txy) * z0;                       // B1
-            dst[11 * L + i] = txx * z0;                               // C0
+        for (int i = 0; i < L; ++i) {
+          const double z = zb[i];
+          if (nd == 0) {
+            dst[6 * L + i] = q * z;
+            dst[7 * L + i] = my * z;
+            dst[8 * L + i] = tyy * z;
+            dst[9 * L + i] = mx * z;
+            dst[10 * L + i] = (2.0 * txy) * z;
+            dst[11 * L + i] = txx * z;
+          } else if (nd == 1) {
+            dst[6 * L + i] += mz * z;
+            dst[7 * L + i] += (2.0 * tyz) * z;
+            dst[9 * L + i] += (2.0 * txz) * z;
+          } else {
+            dst[6 * L + i] += tzz * z;
           }
         }
       }

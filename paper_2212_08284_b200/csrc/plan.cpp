@@ -72,6 +72,9 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
     pending_msg_ = "order_cheb > 10 is not supported by the B200 engine";
   }
   ANKH_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  ANKH_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+  ANKH_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  ANKH_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   for (auto& e : ev_) ANKH_CUDA(cudaEventCreate(&e));
   if (pending_code_ != 0) {
     depth = 1;  // validation-only plan
@@ -98,6 +101,12 @@ Plan::~Plan() {
   if (h_res_) cudaFreeHost(h_res_);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (side_stream_) {
+    cudaStreamSynchronize(side_stream_);
+    cudaStreamDestroy(side_stream_);
+  }
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -369,12 +378,24 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st)
     launches_ = launches;
     return;
   }
+  // The far-field chain (P2M -> M2M -> M2L -> periodic) and the near field
+  // (P2P) only share the sorted particle records: without phase timing they
+  // run concurrently on two streams (P2P on the FP64 pipe, M2L on the DMMA
+  // sub-pipe; P2M/M2M are latency-bound and hide under P2P).  With phase
+  // timing they run back to back so each phase's events bracket one kernel set.
+  const bool do_periodic = periodic && include_self_;
+  cudaStream_t far = st;
+  if (!timing) {
+    ANKH_CUDA(cudaEventRecord(ev_fork_, st));
+    ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
+    far = side_stream_;
+  }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[1], st));
   // interpolation: P2M + M2M (fmm.cpp:181-236)
-  launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, st);
+  launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, far);
   ++launches;
   for (int l = depth - 1; l >= 0; --l) {
-    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, st);
+    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, far);
     ++launches;
   }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[2], st));
@@ -383,21 +404,26 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st)
     const auto r = class_range_[c];
     if (r.second == 0) continue;
     launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c,
-               d_tile_ids_ + r.first, d_inst_, K, Kp, d_far_part_, st);
+               d_tile_ids_ + r.first, d_inst_, K, Kp, d_far_part_, far);
     ++launches;
   }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
+  // periodic far images (fmm.cpp:421-427), counted once (rank 0)
+  if (!timing && do_periodic) {
+    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, far);
+    ++launches;
+  }
+  if (!timing) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
   launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_, leaf_begin_,
              leaf_end_, d_near_part_, d_pair_count_, d_res_, st);
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));
-  // periodic far images (fmm.cpp:421-427), counted once (rank 0)
-  const bool do_periodic = periodic && include_self_;
-  if (do_periodic) {
+  if (timing && do_periodic) {
     launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, st);
     ++launches;
   }
+  if (!timing) ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[5], st));
   launch_finalize(d_near_part_, leaf_end_ - leaf_begin_, d_pair_count_, d_far_part_, n_tiles_,
                   d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,

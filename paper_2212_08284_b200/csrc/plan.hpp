@@ -85,6 +85,8 @@ class Plan {
 
   int device_ = 0;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t side_stream_ = nullptr;  // far-field chain, concurrent with P2P
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   cudaStream_t last_stream_ = nullptr;
   std::vector<void*> allocs_;
   bool csr_only_ = false;
