@@ -87,6 +87,10 @@ class Plan {
   cudaStream_t stream_ = nullptr;
   cudaStream_t side_stream_ = nullptr;  // far-field chain, concurrent with P2P
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  // CUDA-graph replay of launch_all for repeated inputs
+  cudaGraphExec_t graph_exec_ = nullptr;
+  const double *graph_pos_ = nullptr, *graph_src_ = nullptr;
+  const double *graph_warm_pos_ = nullptr, *graph_warm_src_ = nullptr;
   cudaStream_t last_stream_ = nullptr;
   std::vector<void*> allocs_;
   bool csr_only_ = false;
