@@ -65,10 +65,12 @@ void launch_m2l(const double* exp, const long long* level_off, const double* fac
                 const int* tile_ids, const uint2* inst, int K, int Kp, double* far_partial,
                 cudaStream_t st);
 void launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
-                double period, double xi, int nterms, int tpb, int leaf_begin, int leaf_end,
+                double period, double xi, int nterms, int tpb, int cap, int leaf_begin,
+                int leaf_end,
                 double* near_partial, unsigned long long* pair_count, DevResult* res,
                 cudaStream_t st);
 int p2p_terms_for(double s_max);
+int p2p_max_cap();
 void launch_periodic_gen(double* gen, int order, double box_radius, double xi, int p,
                          cudaStream_t st);
 void launch_periodic_eval(const double* root, const double* to_equi, const double* spec_re,

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <numeric>
@@ -133,9 +134,15 @@ void Plan::build_geometry() {
   const double side = 2.0 * rb / nax;
   const double dmax = 2.0 * std::sqrt(3.0) * side * 1.0001;
   nterms_ = p2p_terms_for(cfg.xi * cfg.xi * dmax * dmax);
-  // CTA size: 128 threads (4 CTAs/SM) for ~32-atom leaves, 256 for denser leaves
+  // P2P CTA: 256 threads (2 CTAs/SM, 16 warps), staged-source capacity sized
+  // so a leaf's own + 13 neighbour leaves (~14 x mean occupancy) fit in one
+  // pass for almost every leaf.  ANKH_P2P_TPB / ANKH_P2P_CAP override (tuning).
   const double per_leaf = static_cast<double>(n) / n_leaves;
-  p2p_tpb_ = per_leaf <= 36.0 ? 128 : 256;
+  p2p_tpb_ = 256;
+  p2p_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.45 / 32.0)) * 32;
+  p2p_cap_ = std::max(256, std::min(p2p_cap_, 960));
+  if (const char* e = std::getenv("ANKH_P2P_TPB")) p2p_tpb_ = std::atoi(e) == 128 ? 128 : 256;
+  if (const char* e = std::getenv("ANKH_P2P_CAP")) p2p_cap_ = std::max(64, std::atoi(e));
 }
 
 void Plan::allocate() {
@@ -417,8 +424,8 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st)
   }
   if (!timing) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
-  launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_, leaf_begin_,
-             leaf_end_, d_near_part_, d_pair_count_, d_res_, st);
+  launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_,
+             p2p_cap_, leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, st);
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));
   if (timing && do_periodic) {

@@ -133,6 +133,7 @@ class Plan {
   DevResult* h_res_ = nullptr;
   int nterms_ = 14;
   int p2p_tpb_ = 256;
+  int p2p_cap_ = 512;
   std::uint32_t launches_ = 0;
   // timing
   cudaEvent_t ev_[8] = {};
