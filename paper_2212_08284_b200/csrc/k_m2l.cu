@@ -6,9 +6,10 @@
 //     e += (L M_t) . (R M_s)
 // As a grouped GEMM: a CTA takes 64 instances of one operator, streams the
 // factor rows (padded to kp = 8*KP8) and the 2 x 64 gathered expansions
-// through shared memory in 32-column chunks, and each warp accumulates
-// U = L [M_t...] and V = R [M_s...] for its 8 instances in DMMA fragments
-// (rank rows = M dim, instances = N dim, nodes = K dim).  The energy of the
+// through shared memory in 16-node chunks (2-stage cp.async pipeline), and
+// each warp accumulates U = L [M_t...] and V = R [M_s...] for its 8*NTW
+// instances in DMMA fragments (rank rows = M dim, instances = N dim, nodes =
+// K dim; every factor fragment feeds NTW instance tiles).  The energy of the
 // tile is sum(U o V), reduced in a fixed order into one partial per tile.
 // FP64-pipe bound: 4kK + 2k flops per instance.
 #include "kernels.cuh"
@@ -17,7 +18,6 @@ namespace ankh_b200 {
 
 namespace {
 
-constexpr int kThreads = 256;           // 8 warps x 8 instances
 constexpr int kChunk = 16;              // node columns per pipeline stage
 constexpr int kStride = kChunk + 4;     // smem row stride (doubles): conflict-free fragments
 
@@ -44,19 +44,24 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int KP8>
-__global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp,
-                                                  const long long* __restrict__ level_off,
-                                                  const double* __restrict__ factors,
-                                                  const M2LOp* __restrict__ ops,
-                                                  const M2LTile* __restrict__ tiles,
-                                                  const int* __restrict__ tile_ids,
-                                                  const uint2* __restrict__ inst, int K, int Kp,
-                                                  double* __restrict__ far_partial) {
+// KP8 = padded rank / 8 (DMMA M tiles), NTW = 8-instance N tiles per warp.
+// A warp reuses each factor fragment for its NTW instance tiles; the CTA has
+// 64 / (8 NTW) warps and covers one 64-instance tile of one operator.
+template <int KP8, int NTW>
+__global__ void __launch_bounds__(kM2LTile * 4 / NTW) k_m2l(const double* __restrict__ exp,
+                                                          const long long* __restrict__ level_off,
+                                                          const double* __restrict__ factors,
+                                                          const M2LOp* __restrict__ ops,
+                                                          const M2LTile* __restrict__ tiles,
+                                                          const int* __restrict__ tile_ids,
+                                                          const uint2* __restrict__ inst, int K,
+                                                          int Kp, double* __restrict__ far_partial) {
   constexpr int kp = 8 * KP8;
+  constexpr int kThr = kM2LTile * 4 / NTW;  // 32 lanes per 8 NTW instances
+  constexpr int kWarps = kThr / 32;
   constexpr int kStage = (2 * kp + 2 * kM2LTile) * kStride;  // doubles per pipeline stage
   extern __shared__ __align__(16) double sm[];
-  __shared__ double red[kThreads / 32];
+  __shared__ double red[kWarps];
   __shared__ uint2 s_inst[kM2LTile];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -66,7 +71,8 @@ __global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp
   const double* Lg = factors + op.factor_off;
   const double* Rg = Lg + static_cast<long long>(kp) * Kp;
   const double* E = exp + level_off[tile.level];
-  if (tid < kM2LTile) s_inst[tid] = tid < tile.count ? inst[tile.begin + tid] : make_uint2(0u, 0u);
+  for (int q = tid; q < kM2LTile; q += kThr)
+    s_inst[q] = q < tile.count ? inst[tile.begin + q] : make_uint2(0u, 0u);
   __syncthreads();
 
   // stage chunk [k0, k0 + kChunk) of L, R and the 64 target / source expansions
@@ -75,12 +81,12 @@ __global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp
     double* sR = sL + kp * kStride;
     double* sT = sR + kp * kStride;
     double* sS = sT + kM2LTile * kStride;
-    for (int w = tid; w < kp * (kChunk / 2); w += kThreads) {
+    for (int w = tid; w < kp * (kChunk / 2); w += kThr) {
       const int r = w / (kChunk / 2), c = 2 * (w - (kChunk / 2) * (w / (kChunk / 2)));
       cp_async16(sL + r * kStride + c, Lg + static_cast<long long>(r) * Kp + k0 + c);
       cp_async16(sR + r * kStride + c, Rg + static_cast<long long>(r) * Kp + k0 + c);
     }
-    for (int w = tid; w < kM2LTile * kChunk; w += kThreads) {
+    for (int w = tid; w < kM2LTile * kChunk; w += kThr) {
       const int q = w / kChunk, c = w - kChunk * (w / kChunk);
       const int k = k0 + c;
       const bool ok = q < tile.count && k < K;
@@ -90,9 +96,11 @@ __global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp
     }
   };
 
-  double u[KP8][2], v[KP8][2];
+  double u[NTW][KP8][2], v[NTW][KP8][2];
 #pragma unroll
-  for (int m = 0; m < KP8; ++m) u[m][0] = u[m][1] = v[m][0] = v[m][1] = 0.0;
+  for (int t = 0; t < NTW; ++t)
+#pragma unroll
+    for (int m = 0; m < KP8; ++m) u[t][m][0] = u[t][m][1] = v[t][m][0] = v[t][m][1] = 0.0;
 
   const int row = lane >> 2, col = lane & 3;
   const int nchunks = Kp / kChunk;
@@ -106,25 +114,34 @@ __global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp
     const double* st = sm + (c & 1) * kStage;
     const double* sL = st;
     const double* sR = sL + kp * kStride;
-    const double* bT = sR + kp * kStride + (warp * 8 + row) * kStride + col;
+    const double* bT = sR + kp * kStride + (warp * 8 * NTW + row) * kStride + col;
     const double* bS = bT + kM2LTile * kStride;
 #pragma unroll
     for (int ks = 0; ks < kChunk / 4; ++ks) {
-      const double bt = bT[4 * ks];
-      const double bs = bS[4 * ks];
+      double bt[NTW], bs[NTW];
+#pragma unroll
+      for (int t = 0; t < NTW; ++t) {
+        bt[t] = bT[t * 8 * kStride + 4 * ks];
+        bs[t] = bS[t * 8 * kStride + 4 * ks];
+      }
 #pragma unroll
       for (int m = 0; m < KP8; ++m) {
         const double al = sL[(8 * m + row) * kStride + 4 * ks + col];
         const double ar = sR[(8 * m + row) * kStride + 4 * ks + col];
-        dmma(u[m], al, bt);
-        dmma(v[m], ar, bs);
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) {
+          dmma(u[t][m], al, bt[t]);
+          dmma(v[t][m], ar, bs[t]);
+        }
       }
     }
     __syncthreads();
   }
   double e = 0.0;
 #pragma unroll
-  for (int m = 0; m < KP8; ++m) e += u[m][0] * v[m][0] + u[m][1] * v[m][1];
+  for (int t = 0; t < NTW; ++t)
+#pragma unroll
+    for (int m = 0; m < KP8; ++m) e += u[t][m][0] * v[t][m][0] + u[t][m][1] * v[t][m][1];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
   if (lane == 0) red[warp] = e;
@@ -132,7 +149,7 @@ __global__ void __launch_bounds__(kThreads) k_m2l(const double* __restrict__ exp
   if (tid == 0) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+    for (int w = 0; w < kWarps; ++w) t += red[w];
     far_partial[tile_index] = t;
   }
 }
@@ -141,15 +158,18 @@ template <int KP8>
 void launch_class(const double* exp, const long long* level_off, const double* factors,
                   const M2LOp* ops, const M2LTile* tiles, int n_tiles, const int* tile_ids,
                   const uint2* inst, int K, int Kp, double* far_partial, cudaStream_t st) {
+  // two instance tiles per warp for the common small-rank classes (register budget)
+  constexpr int NTW = KP8 <= 5 ? 2 : 1;
+  constexpr int kThr = kM2LTile * 4 / NTW;
   const std::size_t smem = 2 * sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_m2l<KP8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_m2l<KP8, NTW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
-  k_m2l<KP8><<<n_tiles, kThreads, smem, st>>>(exp, level_off, factors, ops, tiles, tile_ids, inst,
-                                              K, Kp, far_partial);
+  k_m2l<KP8, NTW><<<n_tiles, kThr, smem, st>>>(exp, level_off, factors, ops, tiles, tile_ids,
+                                               inst, K, Kp, far_partial);
 }
 
 }  // namespace
