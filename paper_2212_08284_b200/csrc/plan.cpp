@@ -139,7 +139,7 @@ void Plan::build_geometry() {
   // pass for almost every leaf.  ANKH_P2P_TPB / ANKH_P2P_CAP override (tuning).
   const double per_leaf = static_cast<double>(n) / n_leaves;
   p2p_tpb_ = 256;
-  p2p_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.45 / 32.0)) * 32;
+  p2p_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.3 / 32.0)) * 32;
   p2p_cap_ = std::max(256, std::min(p2p_cap_, 960));
   if (const char* e = std::getenv("ANKH_P2P_TPB")) p2p_tpb_ = std::atoi(e) == 128 ? 128 : 256;
   if (const char* e = std::getenv("ANKH_P2P_CAP")) p2p_cap_ = std::max(64, std::atoi(e));
