@@ -27,15 +27,16 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
-               "r"(valid ? 8 : 0));
-}
-
 __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
+// 16-byte copy, zero-filled when !valid (src is not read then)
+__device__ __forceinline__ void cp_async16z(double* dst, const double* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src),
+               "r"(valid ? 16 : 0));
 }
 
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(kM2LTile * 4 / NTW) k_m2l(const double* __rest
   constexpr int kStage = (2 * kp + 2 * kM2LTile) * kStride;  // doubles per pipeline stage
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[kWarps];
-  __shared__ uint2 s_inst[kM2LTile];
+  __shared__ const double* s_row[2 * kM2LTile];  // expansion row of each target / source
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile_index = tile_ids[blockIdx.x];
@@ -70,29 +71,29 @@ __global__ void __launch_bounds__(kM2LTile * 4 / NTW) k_m2l(const double* __rest
   const M2LOp op = ops[tile.op];
   const double* Lg = factors + op.factor_off;
   const double* Rg = Lg + static_cast<long long>(kp) * Kp;
-  const double* E = exp + level_off[tile.level];
-  for (int q = tid; q < kM2LTile; q += kThr)
-    s_inst[q] = q < tile.count ? inst[tile.begin + q] : make_uint2(0u, 0u);
+  const double* E = exp + level_off[tile.level];  // rows of Kp doubles, zero tail
+  for (int q = tid; q < kM2LTile; q += kThr) {
+    const uint2 ts = q < tile.count ? inst[tile.begin + q] : make_uint2(0u, 0u);
+    s_row[q] = E + static_cast<long long>(ts.x) * Kp;
+    s_row[kM2LTile + q] = E + static_cast<long long>(ts.y) * Kp;
+  }
   __syncthreads();
 
   // stage chunk [k0, k0 + kChunk) of L, R and the 64 target / source expansions
   auto issue = [&](int k0, double* st) {
     double* sL = st;
     double* sR = sL + kp * kStride;
-    double* sT = sR + kp * kStride;
-    double* sS = sT + kM2LTile * kStride;
+    double* sT = sR + kp * kStride;  // followed by the 64 source rows (sS)
     for (int w = tid; w < kp * (kChunk / 2); w += kThr) {
       const int r = w / (kChunk / 2), c = 2 * (w - (kChunk / 2) * (w / (kChunk / 2)));
       cp_async16(sL + r * kStride + c, Lg + static_cast<long long>(r) * Kp + k0 + c);
       cp_async16(sR + r * kStride + c, Rg + static_cast<long long>(r) * Kp + k0 + c);
     }
-    for (int w = tid; w < kM2LTile * kChunk; w += kThr) {
-      const int q = w / kChunk, c = w - kChunk * (w / kChunk);
-      const int k = k0 + c;
-      const bool ok = q < tile.count && k < K;
-      const uint2 ts = s_inst[q];
-      cp_async8(sT + q * kStride + c, ok ? E + static_cast<long long>(ts.x) * K + k : E, ok);
-      cp_async8(sS + q * kStride + c, ok ? E + static_cast<long long>(ts.y) * K + k : E, ok);
+    // 2 x 64 rows x (kChunk / 2) 16-B pieces; sT and sS are contiguous in smem
+    for (int w = tid; w < 2 * kM2LTile * (kChunk / 2); w += kThr) {
+      const int q = w / (kChunk / 2), c = 2 * (w - (kChunk / 2) * (w / (kChunk / 2)));
+      const bool ok = (q & (kM2LTile - 1)) < tile.count;
+      cp_async16z(sT + q * kStride + c, s_row[q] + k0 + c, ok);
     }
   };
 

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
                                                        const double* __restrict__ hd_g,
                                                        double* __restrict__ exp_leaf) {
   using Sh = P2MWShape<L>;
-  constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER;
+  constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER, KS = exp_stride(K);
   extern __shared__ double sm[];
   double* hd = sm;  // 3 L^2
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
   if (leaf >= n_leaves) return;
   const unsigned begin = leaf_off[leaf];
   const int cnt = static_cast<int>(leaf_off[leaf + 1] - begin);
-  double* out = exp_leaf + static_cast<std::size_t>(leaf) * K;
+  double* out = exp_leaf + static_cast<std::size_t>(leaf) * KS;
   // cell_geometry (octree.cpp:18-25)
   const double rad = rb / n;
   const int ci0 = static_cast<int>(leaf) / (n * n), ci1 = (static_cast<int>(leaf) / n) % n,
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
                                                      double* __restrict__ exp_leaf,
                                                      const DevResult* __restrict__ res) {
   using Sh = P2MShape<L>;
-  constexpr int L2 = Sh::L2, K = Sh::K, PB = Sh::PB, RS = Sh::RS;
+  constexpr int L2 = Sh::L2, K = Sh::K, PB = Sh::PB, RS = Sh::RS, KS = exp_stride(K);
   extern __shared__ double sm[];
   double* hd = sm;              // 3 L^2
   double* rec = hd + 3 * L2;    // PB x RS
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
   const int n = 1 << depth;
   const unsigned begin = leaf_off[leaf];
   const int cnt = static_cast<int>(leaf_off[leaf + 1] - begin);
-  double* out = exp_leaf + static_cast<std::size_t>(leaf) * K;
+  double* out = exp_leaf + static_cast<std::size_t>(leaf) * KS;
   if (cnt == 0) {
     for (int o = tid; o < K; o += kP2MThreads) out[o] = 0.0;
     return;
@@ -311,7 +311,7 @@ template <int L>
 __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ child,
                                                      double* __restrict__ parent, int level,
                                                      const double* __restrict__ m2m_g) {
-  constexpr int L2 = L * L, K = L2 * L;
+  constexpr int L2 = L * L, K = L2 * L, KS = exp_stride(K);
   extern __shared__ double sm[];
   double* M = sm;               // 2 x L x L: M[c][i][a] = T_c(i, a)
   double* V = M + 2 * L2;       // 8 x K children
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
     const int cx = c >> 2, cy = (c >> 1) & 1, cz = c & 1;
     const std::size_t ch =
         (static_cast<std::size_t>(2 * pi + cx) * nc + (2 * pj + cy)) * nc + (2 * pk + cz);
-    V[w] = __ldg(child + ch * K + e);
+    V[w] = __ldg(child + ch * KS + e);
   }
   __syncthreads();
   // z: S1[(cx,cy)][a,b,k] = sum_cz sum_c' Mz[cz](k,c') V[(cx,cy,cz)][a,b,c']
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
   }
   __syncthreads();
   // x: out[i,j,k] = sum_cx sum_a Mx[cx](i,a) S2[cx][a,j,k]
-  double* out = parent + static_cast<std::size_t>(pcell) * K;
+  double* out = parent + static_cast<std::size_t>(pcell) * KS;
   for (int e = threadIdx.x; e < K; e += kM2MThreads) {
     const int i = e / L2, jk = e - L2 * (e / L2);
     double acc = 0.0;

@@ -22,6 +22,11 @@ constexpr int kM2LChunk = 32;     // node columns per staged chunk
 constexpr int kMaxKp8 = 16;       // ranks up to 128
 constexpr int kP2PThreads = 256;
 
+/// Row stride (doubles) of one cell's expansion in HBM: K = L^3 rounded up to
+/// 32 (zero tail), so every row starts 256-B aligned and the M2L stager moves
+/// 16-B pieces without bounds checks.
+__host__ __device__ constexpr int exp_stride(int k) { return (k + 31) / 32 * 32; }
+
 struct DevResult {
   double e_self, e_near, e_far, e_periodic;
   unsigned long long near_pairs;

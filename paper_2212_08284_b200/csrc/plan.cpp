@@ -82,7 +82,7 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
     L = 2;
   }
   K = L * L * L;
-  Kp = ceil_div(K, kM2LChunk) * kM2LChunk;
+  Kp = exp_stride(K);  // expansion row stride == factor column stride
   nax = 1 << depth;
   n_leaves = 1 << (3 * depth);
   build_geometry();
@@ -159,8 +159,11 @@ void Plan::allocate() {
   d_temp_ = dalloc(temp_bytes_);
   d_part_ = static_cast<double*>(dalloc(nn * kRec * sizeof(double)));
   level_off_.assign(depth + 2, 0);
-  for (int l = 0; l <= depth; ++l) level_off_[l + 1] = level_off_[l] + (1ll << (3 * l)) * K;
+  // expansion rows padded to Kp = exp_stride(K) doubles; the zero tail is
+  // written once here and never touched by the kernels
+  for (int l = 0; l <= depth; ++l) level_off_[l + 1] = level_off_[l] + (1ll << (3 * l)) * Kp;
   d_exp_ = static_cast<double*>(dalloc(level_off_[depth + 1] * sizeof(double)));
+  ANKH_CUDA(cudaMemsetAsync(d_exp_, 0, level_off_[depth + 1] * sizeof(double), stream_));
   d_level_off_ = static_cast<long long*>(dalloc(level_off_.size() * sizeof(long long)));
   ANKH_CUDA(cudaMemcpyAsync(d_level_off_, level_off_.data(), level_off_.size() * sizeof(long long),
                             cudaMemcpyHostToDevice, stream_));
@@ -555,8 +558,13 @@ void Plan::result(ankh_report_v1* out) {
 
 void Plan::expansions(double* out, std::size_t count) {
   ANKH_CUDA(cudaStreamSynchronize(last_stream_ ? last_stream_ : stream_));
+  // strip the row padding: out holds K doubles per cell, levels 0..depth
   const std::size_t total = static_cast<std::size_t>(level_off_[depth + 1]);
-  ANKH_CUDA(cudaMemcpy(out, d_exp_, std::min(count, total) * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double> padded(total);
+  ANKH_CUDA(cudaMemcpy(padded.data(), d_exp_, total * sizeof(double), cudaMemcpyDeviceToHost));
+  const std::size_t cells = total / static_cast<std::size_t>(Kp);
+  for (std::size_t c = 0; c < cells && (c + 1) * K <= count; ++c)
+    std::memcpy(out + c * K, padded.data() + c * Kp, K * sizeof(double));
 }
 
 void Plan::m2l_factors(int level, const int* offset, double* lmat, double* rmat, int max_rank,
