@@ -92,8 +92,30 @@ def kats():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--config", type=int, default=None,
+                    help="only BASELINE config 3 or 4 (config 4: evaluation 0 of the rescale series)")
     args = ap.parse_args()
     threads = os.cpu_count() or 1
+    if args.config is not None:
+        pos, src, rb, c = inputs.make_config(args.config)
+        L = c.orders[0]
+        scale = 1.0
+        if args.config == 4:
+            scale = float(inputs.rescale_factors(c.seed, c.evaluations)[0])
+            src = src.copy()
+            src[:, 1:4] *= scale
+        rep = R.fmm_energy(pos, src, rb, order_cheb=L, order_equi=L, threads=threads)
+        doc = {"generator": "tests/golden/make_golden.py --config %d" % args.config,
+               "reference": "oracle/_ref/libankh_ref.so",
+               "system": {"name": f"{c.name}_L{L}", "config_index": args.config, "n": pos.shape[0],
+                          "box_radius": rb, "seed": c.seed, "dipole_scale": scale,
+                          "config": dict(order_cheb=L, order_equi=L), "sha256": sha(pos, src),
+                          "energies": energies(rep), "ref_wall_times": rep["wall_times"],
+                          "ref_threads": threads}}
+        with open(os.path.join(HERE, f"golden_c{args.config}.json"), "w") as f:
+            json.dump(doc, f, indent=1)
+        print(c.name, doc["system"]["energies"]["e_total"], rep["wall_times"], flush=True)
+        return
     doc = {"generator": "tests/golden/make_golden.py", "reference": "oracle/_ref/libankh_ref.so",
            "kats": kats(), "systems": []}
     for name, n, rb, seed, mp, kw in SMALL_CASES:
