@@ -140,6 +140,29 @@ int ankh_leaf_csr_v1(size_t n, const double* positions, double box_radius, int d
 int ankh_plan_m2l_factors_v1(ankh_plan_v1* plan, int level, const int* offset, double* lmat,
                              double* rmat, int max_rank, int* rank, char* err, size_t errlen);
 
+/* ---- multi-GPU shards (cfg.rank / cfg.world) ----
+ * A shard computes P2M for its Morton leaf rows, P2P for its Morton leaf
+ * range and M2L for the instances whose target it owns.  Two exchanges finish
+ * the job: an all-gather of the Morton-ordered leaf expansions (when
+ * world | 8^depth) and an all-reduce of the energy/counter vector.
+ *
+ * (a) NCCL, inside the plan: rank 0 creates an id, every rank attaches it;
+ *     afterwards ankh_plan_enqueue_v1 / ankh_plan_energy_*_v1 return JOB totals. */
+int ankh_nccl_unique_id_v1(unsigned char* id128, char* err, size_t errlen);
+int ankh_plan_attach_nccl_v1(ankh_plan_v1* plan, const unsigned char* id128, char* err,
+                             size_t errlen);
+/* (b) Caller-driven (in-process shards, other transports): phase 1 runs
+ *     binning..P2M of this shard's rows; the caller fills the other rows of
+ *     the leaf level (ankh_plan_leaf_level_v1: device pointer, row range,
+ *     row stride in doubles); phase 2 runs the rest.  Energies are then this
+ *     shard's partials (sum over shards). */
+int ankh_plan_enqueue_phase_v1(ankh_plan_v1* plan, int phase, const double* d_positions,
+                               const double* d_sources, void* stream, char* err, size_t errlen);
+int ankh_plan_leaf_level_v1(ankh_plan_v1* plan, double** d_leaf_level, int64_t* row_begin,
+                            int64_t* row_end, int* row_stride);
+int ankh_device_copy_v1(void* dst, const void* src, size_t bytes, void* stream, char* err,
+                        size_t errlen);
+
 /* ---- spatial sharding (host only; no device needed) ----
  * Shards own contiguous Morton ranges of leaves; a level-l cell belongs to the
  * shard owning its first descendant leaf.  P2P work is owned by the target

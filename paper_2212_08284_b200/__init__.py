@@ -16,7 +16,10 @@ from .api import (  # noqa: F401
     Plan,
     build_tree_csr,
     default_depth,
+    device_copy,
+    exchange_leaf_levels,
     fmm_energy,
+    nccl_unique_id,
 )
 from ._lib import LIB_PATH, build, lib  # noqa: F401
 

@@ -31,6 +31,11 @@ EXPORTS = [
     "ankh_shard_leaf_range_v1",
     "ankh_shard_cell_owner_v1",
     "ankh_shard_m2l_instances_v1",
+    "ankh_plan_enqueue_phase_v1",
+    "ankh_plan_leaf_level_v1",
+    "ankh_device_copy_v1",
+    "ankh_nccl_unique_id_v1",
+    "ankh_plan_attach_nccl_v1",
 ]
 
 
@@ -80,6 +85,12 @@ def lib() -> ctypes.CDLL:
         L.ankh_shard_cell_owner_v1.argtypes = [c_int, ctypes.c_uint32, c_int, c_int]
         L.ankh_shard_m2l_instances_v1.argtypes = [c_int, c_int, c_int, c_int, U32, U32, U32, I,
                                                   c_size_t, ctypes.POINTER(c_size_t)]
+        L.ankh_plan_enqueue_phase_v1.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p, cp,
+                                                 c_size_t]
+        L.ankh_plan_leaf_level_v1.argtypes = [c_void_p, ctypes.POINTER(c_void_p), I64, I64, I]
+        L.ankh_device_copy_v1.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, cp, c_size_t]
+        L.ankh_nccl_unique_id_v1.argtypes = [ctypes.c_char_p, cp, c_size_t]
+        L.ankh_plan_attach_nccl_v1.argtypes = [c_void_p, ctypes.c_char_p, cp, c_size_t]
         L.ankh_version_v1.argtypes = []
         L.ankh_version_v1.restype = ctypes.c_char_p
         _lib = L

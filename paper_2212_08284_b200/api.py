@@ -39,6 +39,9 @@ __all__ = [
     "default_depth",
     "build_tree_csr",
     "Plan",
+    "nccl_unique_id",
+    "device_copy",
+    "exchange_leaf_levels",
 ]
 
 
@@ -219,6 +222,33 @@ def fmm_energy(system: ParticleSystem, config: Optional[EwaldConfig] = None,
     return EnergyReport._from_c(rep, wall)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast to the other shards)."""
+    buf = ctypes.create_string_buffer(128)
+    err = ctypes.create_string_buffer(512)
+    _check(lib().ankh_nccl_unique_id_v1(buf, err, 512), err)
+    return buf.raw
+
+
+def device_copy(dst_ptr: int, src_ptr: int, nbytes: int, stream: int = 0) -> None:
+    """cudaMemcpyAsync device-to-device (shard leaf-level exchange in one process)."""
+    err = ctypes.create_string_buffer(512)
+    _check(lib().ankh_device_copy_v1(ctypes.c_void_p(dst_ptr), ctypes.c_void_p(src_ptr), int(nbytes),
+                                     ctypes.c_void_p(stream), err, 512), err)
+
+
+def exchange_leaf_levels(plans, stream: int = 0) -> None:
+    """Complete every shard's leaf level from the others' rows (in-process
+    equivalent of the NCCL all-gather; all plans on the current device)."""
+    info = [p.leaf_level() for p in plans]
+    for j, (dst, _, _, stride) in enumerate(info):
+        for i, (src, b, e, _) in enumerate(info):
+            if i == j or e <= b:
+                continue
+            off = b * stride * 8
+            device_copy(dst + off, src + off, (e - b) * stride * 8, stream)
+
+
 def build_tree_csr(positions, box_radius: float, depth: int) -> Tuple[np.ndarray, np.ndarray]:
     """Leaf buckets of build_tree as CSR (offsets[8^depth+1], indices[N]), on the GPU."""
     pos = _as_host(positions, 3)
@@ -307,6 +337,35 @@ class Plan:
         err = ctypes.create_string_buffer(512)
         _check(lib().ankh_plan_energies_device_v1(self._h, ctypes.c_void_p(out.data_ptr()),
                                                   ctypes.c_void_p(stream), err, 512), err)
+
+    # ---- multi-GPU shards -------------------------------------------------
+    def attach_nccl(self, unique_id: bytes) -> None:
+        """Join the NCCL communicator of all shards (``nccl_unique_id()`` from
+        rank 0, broadcast by the caller); reports then carry job totals."""
+        if len(unique_id) != 128:
+            raise InvalidArgument("NCCL unique id must be 128 bytes")
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_attach_nccl_v1(self._h, unique_id, err, 512), err)
+
+    def enqueue_phase(self, phase: int, positions, sources, stream: int = 0) -> None:
+        """Caller-driven shard exchange: phase 1 = binning..this shard's P2M,
+        phase 2 = M2M..final reduction (after the leaf level is completed)."""
+        self._check_dev(positions, sources)
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_enqueue_phase_v1(self._h, int(phase), ctypes.c_void_p(positions.data_ptr()),
+                                                ctypes.c_void_p(sources.data_ptr()),
+                                                ctypes.c_void_p(stream), err, 512), err)
+
+    def leaf_level(self) -> Tuple[int, int, int, int]:
+        """(device pointer, first row, end row, row stride in doubles) of the
+        Morton-ordered leaf expansions; rows [first, end) are this shard's."""
+        ptr = ctypes.c_void_p()
+        b, e = ctypes.c_int64(), ctypes.c_int64()
+        stride = ctypes.c_int()
+        _check(lib().ankh_plan_leaf_level_v1(self._h, ctypes.byref(ptr), ctypes.byref(b),
+                                             ctypes.byref(e), ctypes.byref(stride)),
+               ctypes.create_string_buffer(b"invalid plan"))
+        return int(ptr.value or 0), b.value, e.value, stride.value
 
     def result(self) -> EnergyReport:
         rep = _Report()

@@ -218,6 +218,47 @@ int ankh_plan_energies_device_v1(ankh_plan_v1* plan, double* d_out, void* stream
   });
 }
 
+int ankh_plan_enqueue_phase_v1(ankh_plan_v1* plan, int phase, const double* d_positions,
+                               const double* d_sources, void* stream, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || (phase != 1 && phase != 2)) throw AnkhError(ANKH_INVALID_ARGUMENT, "bad plan or phase");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->plan->enqueue_phase(phase, d_positions, d_sources, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ankh_plan_leaf_level_v1(ankh_plan_v1* plan, double** d_leaf_level, int64_t* row_begin,
+                            int64_t* row_end, int* row_stride) {
+  if (!plan || !d_leaf_level) return ANKH_INVALID_ARGUMENT;
+  *d_leaf_level = plan->plan->leaf_level(row_begin, row_end, row_stride);
+  return ANKH_OK;
+}
+
+int ankh_device_copy_v1(void* dst, const void* src, size_t bytes, void* stream, char* err,
+                        size_t errlen) {
+  return guarded(err, errlen, [&] {
+    ANKH_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
+                              static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int ankh_nccl_unique_id_v1(unsigned char* id128, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!id128) throw AnkhError(ANKH_INVALID_ARGUMENT, "null id buffer");
+    ankh_b200::nccl_unique_id(id128);
+  });
+}
+
+int ankh_plan_attach_nccl_v1(ankh_plan_v1* plan, const unsigned char* id128, char* err,
+                             size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !id128) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or id");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    const ankh_config_v1& c = plan->plan->cfg;
+    plan->plan->attach_collective(ankh_b200::make_nccl_collective(id128, c.rank, c.world));
+  });
+}
+
 int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* begin, int64_t* end) {
   if (depth < 1 || depth > 8 || world < 1 || rank < 0 || rank >= world || !begin || !end)
     return ANKH_INVALID_ARGUMENT;

@@ -1,0 +1,102 @@
+#include "collective.hpp"
+
+#include <dlfcn.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "plan.hpp"
+
+namespace ankh_b200 {
+
+namespace {
+
+// The subset of nccl.h used here (stable NCCL 2.x ABI).
+using ncclComm_t = void*;
+struct NcclUniqueId {
+  char internal[128];
+};
+enum { kNcclSuccess = 0, kNcclFloat64 = 8, kNcclSum = 0 };
+
+struct NcclApi {
+  int (*GetUniqueId)(NcclUniqueId*) = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, NcclUniqueId, int) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  int (*AllGather)(const void*, void*, std::size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, std::size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string failure;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      failure = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* name) {
+      void* p = dlsym(h, name);
+      if (!p) failure = std::string("NCCL symbol missing: ") + name;
+      return p;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  });
+  if (!failure.empty()) throw AnkhError(ANKH_CUDA_ERROR, failure);
+  return api;
+}
+
+void check(int r, const char* what) {
+  if (r != kNcclSuccess)
+    throw AnkhError(ANKH_CUDA_ERROR, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+class NcclCollective final : public Collective {
+ public:
+  NcclCollective(const unsigned char id[128], int rank, int world) : rank_(rank), world_(world) {
+    NcclUniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    check(nccl().CommInitRank(&comm_, world, uid, rank), "ncclCommInitRank");
+  }
+  ~NcclCollective() override {
+    if (comm_) nccl().CommDestroy(comm_);
+  }
+  void allgather_inplace(double* recv, std::size_t count, cudaStream_t st) override {
+    check(nccl().AllGather(recv + static_cast<std::size_t>(rank_) * count, recv, count,
+                           kNcclFloat64, comm_, st),
+          "ncclAllGather");
+  }
+  void allreduce_sum(double* buf, std::size_t count, cudaStream_t st) override {
+    check(nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, comm_, st), "ncclAllReduce");
+  }
+  int rank() const override { return rank_; }
+  int world() const override { return world_; }
+
+ private:
+  ncclComm_t comm_ = nullptr;
+  int rank_, world_;
+};
+
+}  // namespace
+
+void nccl_unique_id(unsigned char out[128]) {
+  NcclUniqueId uid;
+  check(nccl().GetUniqueId(&uid), "ncclGetUniqueId");
+  std::memcpy(out, uid.internal, 128);
+}
+
+Collective* make_nccl_collective(const unsigned char id[128], int rank, int world) {
+  return new NcclCollective(id, rank, world);
+}
+
+}  // namespace ankh_b200

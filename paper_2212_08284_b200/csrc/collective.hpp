@@ -1,0 +1,30 @@
+// Shard collectives of the multi-GPU plan.  The path has exactly two exchange
+// steps: the all-gather of the Morton-ordered leaf expansions
+// after the sharded P2M, and the all-reduce of the energy/counter vector.
+// NCCL is resolved at run time (dlopen of libnccl.so.2 -- in a PyTorch process
+// the already-loaded NCCL is reused), so the library has no link-time NCCL
+// dependency and single-GPU users never touch it.
+#pragma once
+
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace ankh_b200 {
+
+class Collective {
+ public:
+  virtual ~Collective() = default;
+  /// recv holds world * count doubles; this rank's contribution already sits at
+  /// recv + rank * count (in-place all-gather).
+  virtual void allgather_inplace(double* recv, std::size_t count, cudaStream_t st) = 0;
+  virtual void allreduce_sum(double* buf, std::size_t count, cudaStream_t st) = 0;
+  virtual int rank() const = 0;
+  virtual int world() const = 0;
+};
+
+/// 128-byte NCCL unique id for rank 0 to broadcast (throws AnkhError on failure).
+void nccl_unique_id(unsigned char out[128]);
+/// Communicator over `world` ranks (one GPU each, current device).
+Collective* make_nccl_collective(const unsigned char id[128], int rank, int world);
+
+}  // namespace ankh_b200

@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
                                                        const unsigned* __restrict__ leaf_off,
                                                        int depth, double rb,
                                                        const double* __restrict__ hd_g,
-                                                       double* __restrict__ exp_leaf) {
+                                                       double* __restrict__ exp_leaf,
+                                                       unsigned m_begin, unsigned m_end) {
   using Sh = P2MWShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER, KS = exp_stride(K);
   extern __shared__ double sm[];
@@ -56,12 +57,13 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
   for (int w = threadIdx.x; w < 3 * L2; w += kP2MThreads) hd[w] = hd_g[w];
   __syncthreads();
   const int n = 1 << depth;
-  const unsigned n_leaves = 1u << (3 * depth);
-  const unsigned leaf = blockIdx.x * kP2MWarps + warp;
-  if (leaf >= n_leaves) return;
+  // leaves are visited (and their expansions stored) in Morton order
+  const unsigned m = m_begin + blockIdx.x * kP2MWarps + warp;
+  if (m >= m_end) return;
+  const unsigned leaf = morton_to_lex(m, n);
   const unsigned begin = leaf_off[leaf];
   const int cnt = static_cast<int>(leaf_off[leaf + 1] - begin);
-  double* out = exp_leaf + static_cast<std::size_t>(leaf) * KS;
+  double* out = exp_leaf + static_cast<std::size_t>(m) * KS;
   // cell_geometry (octree.cpp:18-25)
   const double rad = rb / n;
   const int ci0 = static_cast<int>(leaf) / (n * n), ci1 = (static_cast<int>(leaf) / n) % n,
@@ -186,7 +188,8 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
                                                      int depth, double rb,
                                                      const double* __restrict__ hd_g,
                                                      double* __restrict__ exp_leaf,
-                                                     const DevResult* __restrict__ res) {
+                                                     const DevResult* __restrict__ res,
+                                                     unsigned m_begin) {
   using Sh = P2MShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PB = Sh::PB, RS = Sh::RS, KS = exp_stride(K);
   extern __shared__ double sm[];
@@ -195,11 +198,12 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
   double* S = rec + PB * RS;    // PB x 3 axes x 3 orders x L
   double* W = S + PB * 9 * L;   // PB x 3 x L^2
   const int tid = threadIdx.x;
-  const unsigned leaf = blockIdx.x;
   const int n = 1 << depth;
+  const unsigned m = m_begin + blockIdx.x;  // Morton leaf
+  const unsigned leaf = morton_to_lex(m, n);
   const unsigned begin = leaf_off[leaf];
   const int cnt = static_cast<int>(leaf_off[leaf + 1] - begin);
-  double* out = exp_leaf + static_cast<std::size_t>(leaf) * KS;
+  double* out = exp_leaf + static_cast<std::size_t>(m) * KS;
   if (cnt == 0) {
     for (int o = tid; o < K; o += kP2MThreads) out[o] = 0.0;
     return;
@@ -317,17 +321,14 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
   double* V = M + 2 * L2;       // 8 x K children
   double* S1 = V + 8 * K;       // 4 x K  (cx, cy) after z
   double* S2 = S1 + 4 * K;      // 2 x K  (cx) after y
-  const int n = 1 << level, nc = 2 * n;
+  (void)level;
+  // Morton order: the children of parent p are rows 8p + (cx<<2 | cy<<1 | cz)
   const unsigned pcell = blockIdx.x;
-  const int pi = static_cast<int>(pcell) / (n * n), pj = (static_cast<int>(pcell) / n) % n,
-            pk = static_cast<int>(pcell) % n;
+  const double* ch0 = child + static_cast<std::size_t>(pcell) * 8 * KS;
   for (int w = threadIdx.x; w < 2 * L2; w += kM2MThreads) M[w] = m2m_g[w];
   for (int w = threadIdx.x; w < 8 * K; w += kM2MThreads) {
     const int c = w / K, e = w - K * (w / K);
-    const int cx = c >> 2, cy = (c >> 1) & 1, cz = c & 1;
-    const std::size_t ch =
-        (static_cast<std::size_t>(2 * pi + cx) * nc + (2 * pj + cy)) * nc + (2 * pk + cz);
-    V[w] = __ldg(child + ch * KS + e);
+    V[w] = __ldg(ch0 + c * KS + e);
   }
   __syncthreads();
   // z: S1[(cx,cy)][a,b,k] = sum_cz sum_c' Mz[cz](k,c') V[(cx,cy,cz)][a,b,c']
@@ -379,7 +380,10 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
 
 template <int L>
 void p2m_order(const double* part, const unsigned* leaf_off, int depth, double rb,
-               const double* hd, double* exp_leaf, const DevResult* res, cudaStream_t st) {
+               const double* hd, double* exp_leaf, const DevResult* res, unsigned m_begin,
+               unsigned m_end, cudaStream_t st) {
+  if (m_end <= m_begin) return;
+  const unsigned leaves = m_end - m_begin;
   if (L > 6) {  // register budget of the warp-per-leaf variant: block-per-leaf instead
     const std::size_t smem = sizeof(double) * P2MShape<L>::smem_doubles;
     static bool attr_b = false;
@@ -388,8 +392,8 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
                            static_cast<int>(smem));
       attr_b = true;
     }
-    k_p2m<L><<<1u << (3 * depth), kP2MThreads, smem, st>>>(part, leaf_off, depth, rb, hd, exp_leaf,
-                                                           res);
+    k_p2m<L><<<leaves, kP2MThreads, smem, st>>>(part, leaf_off, depth, rb, hd, exp_leaf, res,
+                                                m_begin);
     return;
   }
   constexpr int LW = L > 6 ? 6 : L;  // (never launched with L > 6)
@@ -400,10 +404,8 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
                          static_cast<int>(smem));
     attr = true;
   }
-  const unsigned leaves = 1u << (3 * depth);
-  k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(part, leaf_off,
-                                                                             depth, rb, hd,
-                                                                             exp_leaf);
+  k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(
+      part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end);
 }
 
 template <int L>
@@ -439,8 +441,9 @@ void m2m_order(const double* child, double* parent, int parent_level, const doub
 
 void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
                 double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
-                cudaStream_t st) {
-#define ANKH_P2M(N) p2m_order<N>(part, leaf_off, depth, box_radius, hd, exp_leaf, res, st)
+                unsigned m_begin, unsigned m_end, cudaStream_t st) {
+#define ANKH_P2M(N) \
+  p2m_order<N>(part, leaf_off, depth, box_radius, hd, exp_leaf, res, m_begin, m_end, st)
   ANKH_ORDER_SWITCH(order, ANKH_P2M)
 #undef ANKH_P2M
 }

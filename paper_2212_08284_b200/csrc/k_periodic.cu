@@ -208,11 +208,11 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    res->e_near = e_near;
-    res->e_far = e_far;
-    res->e_self = self_scale * self_acc;  // -xi/sqrt(pi) * acc (kernel.cpp:212)
-    res->e_periodic = use_periodic ? periodic[0] : 0.0;
-    res->near_pairs = redu[0];
+    res->red[kENear] = e_near;
+    res->red[kEFar] = e_far;
+    res->red[kESelf] = self_scale * self_acc;  // -xi/sqrt(pi) * acc (kernel.cpp:212)
+    res->red[kEPeriodic] = use_periodic ? periodic[0] : 0.0;
+    res->red[kNearPairs] = static_cast<double>(redu[0]);
   }
 }
 

@@ -22,18 +22,37 @@ constexpr int kM2LChunk = 32;     // node columns per staged chunk
 constexpr int kMaxKp8 = 16;       // ranks up to 128
 constexpr int kP2PThreads = 256;
 
+/// Morton decode: every 3rd bit (x in bit 3k+2, y in 3k+1, z in 3k), as
+/// shard.cpp's morton3 encodes.  Expansions at every level are stored in
+/// Morton order (children of cell m are 8m..8m+7; a shard's cells are one
+/// contiguous slice); particles and leaf CSR stay in the reference's lex order.
+__host__ __device__ inline unsigned morton_compact3(unsigned v) {
+  v &= 0x09249249u;
+  v = (v ^ (v >> 2)) & 0x030c30c3u;
+  v = (v ^ (v >> 4)) & 0x0300f00fu;
+  v = (v ^ (v >> 8)) & 0x030000ffu;
+  v = (v ^ (v >> 16)) & 0x000003ffu;
+  return v;
+}
+__host__ __device__ inline unsigned morton_to_lex(unsigned m, int n) {
+  const unsigned x = morton_compact3(m >> 2), y = morton_compact3(m >> 1), z = morton_compact3(m);
+  return (x * static_cast<unsigned>(n) + y) * static_cast<unsigned>(n) + z;
+}
+
 /// Row stride (doubles) of one cell's expansion in HBM: K = L^3 rounded up to
 /// 32 (zero tail), so every row starts 256-B aligned and the M2L stager moves
 /// 16-B pieces without bounds checks.
 __host__ __device__ constexpr int exp_stride(int k) { return (k + 31) / 32 * 32; }
 
+// Everything a shard contributes additively sits in red[] so one all-reduce
+// (sum) combines shards: energies, the pair counter (exact in a double up to
+// 2^53) and the error flags (> 0 means raised somewhere).
+enum RedSlot { kESelf = 0, kENear, kEFar, kEPeriodic, kNearPairs, kDuplicate, kCoincident, kRedCount = 8 };
+
 struct DevResult {
-  double e_self, e_near, e_far, e_periodic;
-  unsigned long long near_pairs;
-  unsigned long long min_nonfinite;  // lowest index with a non-finite value
+  double red[kRedCount];
+  unsigned long long min_nonfinite;  // lowest index with a non-finite value (same on every shard)
   unsigned long long min_outside;    // lowest finite index outside the box
-  int duplicate;                     // exact duplicate positions found
-  int coincident;                    // r == 0 under an image shift
   int any_multipole;                 // some particle has mu or Theta != 0
 };
 
@@ -62,7 +81,7 @@ void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, un
                  const unsigned* counts, unsigned* offsets, int n_leaves, cudaStream_t st);
 void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
                 double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
-                cudaStream_t st);
+                unsigned m_begin, unsigned m_end, cudaStream_t st);
 void launch_m2m(const double* child, double* parent, int parent_level, int order,
                 const double* m2m, cudaStream_t st);
 void launch_m2l(const double* exp, const long long* level_off, const double* factors,

@@ -129,6 +129,12 @@ void Plan::build_geometry() {
   leaf_begin_ = static_cast<int>(lb);
   leaf_end_ = static_cast<int>(le);
   include_self_ = cfg.rank == 0;
+  // P2M is split across shards when the Morton leaf slices are equal-sized
+  // (world | 8^E) so one in-place all-gather completes the leaf level;
+  // otherwise every shard computes all leaf expansions.
+  shard_upward_ = cfg.world > 1 && (static_cast<long long>(n_leaves) % cfg.world) == 0;
+  p2m_begin_ = shard_upward_ ? lb : 0;
+  p2m_end_ = shard_upward_ ? le : n_leaves;
   // P2P polynomial length from the largest possible near distance
   // (2 leaf sides per axis): s_max = xi^2 (2 sqrt(3) * 2 r_B / n)^2
   const double side = 2.0 * rb / nax;
@@ -219,8 +225,14 @@ void Plan::build_m2l() {
     work[i].level = groups[i].level;
     work[i].o = groups[i].offset;
     work[i].inst.resize(groups[i].t.size());
+    // expansions are stored in Morton order: instance cells become Morton rows,
+    // and a tile's 64 instances are Morton-contiguous targets (L2 locality)
+    const unsigned nl = 1u << groups[i].level;
+    auto to_morton = [nl](unsigned c) { return morton3(c / (nl * nl), (c / nl) % nl, c % nl); };
     for (std::size_t k = 0; k < groups[i].t.size(); ++k)
-      work[i].inst[k] = make_uint2(groups[i].t[k], groups[i].s[k]);
+      work[i].inst[k] = make_uint2(to_morton(groups[i].t[k]), to_morton(groups[i].s[k]));
+    std::sort(work[i].inst.begin(), work[i].inst.end(),
+              [](const uint2& a, const uint2& b) { return a.x < b.x; });
   }
   groups.clear();
   // factors: exact SVD path uses the signed-permutation symmetry of the block
@@ -370,42 +382,54 @@ void Plan::validate_only(const double* d_pos, const double* d_src, cudaStream_t 
   launches_ = 3;
 }
 
-void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st) {
-  const bool timing = cfg.phase_timing != 0;
+void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st, int mode) {
+  const bool timing = cfg.phase_timing != 0 && mode == 0;
   std::uint32_t launches = 0;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[0], st));
-  ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
-  launch_init_result(d_res_, st);
-  ++launches;
-  // binning + sort + gather (build_tree, octree.cpp:27-45)
-  const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
-  launch_bin(d_pos, d_src, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_, d_self_part_,
-             d_res_, st);
-  ++launches;
-  launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 3 * depth, d_counts_,
-              d_off_, n_leaves, st);
-  launch_gather(d_pos, d_src, d_idx2_, n, d_part_, st);
-  ++launches;
+  if (mode != 2) {
+    ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
+    launch_init_result(d_res_, st);
+    ++launches;
+    // binning + sort + gather (build_tree, octree.cpp:27-45)
+    const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
+    launch_bin(d_pos, d_src, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_,
+               d_self_part_, d_res_, st);
+    ++launches;
+    launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 3 * depth, d_counts_,
+                d_off_, n_leaves, st);
+    launch_gather(d_pos, d_src, d_idx2_, n, d_part_, st);
+    ++launches;
+  }
   if (csr_only_) {
     launches_ = launches;
     return;
   }
   // The far-field chain (P2M -> M2M -> M2L -> periodic) and the near field
   // (P2P) only share the sorted particle records: without phase timing they
-  // run concurrently on two streams (P2P on the FP64 pipe, M2L on the DMMA
-  // sub-pipe; P2M/M2M are latency-bound and hide under P2P).  With phase
-  // timing they run back to back so each phase's events bracket one kernel set.
+  // run concurrently on two streams (P2M/M2M are latency-bound and hide under
+  // P2P).  With phase timing -- or when the caller drives the two halves
+  // itself (mode 1/2, in-process shard exchange) -- they run back to back.
+  const bool serial = timing || mode != 0;
   const bool do_periodic = periodic && include_self_;
   cudaStream_t far = st;
-  if (!timing) {
+  if (!serial) {
     ANKH_CUDA(cudaEventRecord(ev_fork_, st));
     ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
     far = side_stream_;
   }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[1], st));
-  // interpolation: P2M + M2M (fmm.cpp:181-236)
-  launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, far);
-  ++launches;
+  // interpolation: P2M over this shard's Morton leaf range (fmm.cpp:181-201) ...
+  if (mode != 2) {
+    launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_,
+               static_cast<unsigned>(p2m_begin_), static_cast<unsigned>(p2m_end_), far);
+    ++launches;
+  }
+  if (mode == 1) {
+    launches_ = launches;
+    return;
+  }
+  // ... the leaf level completed by the shard exchange, then M2M (fmm.cpp:203-236)
+  if (mode == 0) exchange_leaves(far);
   for (int l = depth - 1; l >= 0; --l) {
     launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, far);
     ++launches;
@@ -421,30 +445,42 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st)
   }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
   // periodic far images (fmm.cpp:421-427), counted once (rank 0)
-  if (!timing && do_periodic) {
+  if (!serial && do_periodic) {
     launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, far);
     ++launches;
   }
-  if (!timing) ANKH_CUDA(cudaEventRecord(ev_join_, far));
+  if (!serial) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
   launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_,
              p2p_cap_, leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, st);
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));
-  if (timing && do_periodic) {
+  if (serial && do_periodic) {
     launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, st);
     ++launches;
   }
-  if (!timing) ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
+  if (!serial) ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[5], st));
   launch_finalize(d_near_part_, leaf_end_ - leaf_begin_, d_pair_count_, d_far_part_, n_tiles_,
                   d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
                   include_self_ ? 1 : 0, d_res_, st);
   ++launches;
+  // shards: one all-reduce of the energy / counter / flag vector (the path's
+  // only exchange besides the leaf all-gather)
+  if (coll_) coll_->allreduce_sum(d_res_->red, kRedCount, st);
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[6], st));
   ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
   ANKH_CUDA(cudaGetLastError());
   launches_ = launches;
+}
+
+void Plan::exchange_leaves(cudaStream_t st) {
+  if (!coll_ || !shard_upward_) return;
+  // in-place all-gather of the Morton-ordered leaf level: rank r owns rows
+  // [r n_leaves / world, (r+1) n_leaves / world)
+  double* leaf_level = d_exp_ + level_off_[depth];
+  const std::size_t count = static_cast<std::size_t>(p2m_end_ - p2m_begin_) * Kp;
+  coll_->allgather_inplace(leaf_level, count, st);
 }
 
 void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
@@ -522,18 +558,19 @@ void Plan::result(ankh_report_v1* out) {
                     std::string("fmm_energy: invalid system: ") +
                         (nf ? "non-finite coordinate or moment" : "outside box"));
   }
-  if (r.duplicate)
+  if (r.red[kDuplicate] > 0.0)
     throw AnkhError(ANKH_INVALID_ARGUMENT, "fmm_energy: invalid system: duplicate position");
   if (pending_code_ != 0) throw AnkhError(pending_code_, pending_msg_);
-  if (r.coincident) throw AnkhError(ANKH_DOMAIN_ERROR, "pair_interaction: coincident points");
-  out->e_self = r.e_self;
-  out->e_near = r.e_near;
-  out->e_far = r.e_far;
-  out->e_periodic_far = r.e_periodic;
+  if (r.red[kCoincident] > 0.0)
+    throw AnkhError(ANKH_DOMAIN_ERROR, "pair_interaction: coincident points");
+  out->e_self = r.red[kESelf];
+  out->e_near = r.red[kENear];
+  out->e_far = r.red[kEFar];
+  out->e_periodic_far = r.red[kEPeriodic];
   out->e_reciprocal = 0.0;
   // EnergyReport::component_sum order (types.hpp:132-134)
   out->e_total = out->e_self + out->e_near + out->e_far + out->e_periodic_far + out->e_reciprocal;
-  out->near_pairs = r.near_pairs;
+  out->near_pairs = static_cast<std::uint64_t>(r.red[kNearPairs]);
   out->far_instances = 0;
   out->gpu_launches = launches_;
   if (cfg.world <= 1) {
@@ -558,13 +595,52 @@ void Plan::result(ankh_report_v1* out) {
 
 void Plan::expansions(double* out, std::size_t count) {
   ANKH_CUDA(cudaStreamSynchronize(last_stream_ ? last_stream_ : stream_));
-  // strip the row padding: out holds K doubles per cell, levels 0..depth
+  // reference layout: levels 0..depth, lex cell order, K doubles per cell
+  // (device rows are Morton-ordered and padded to Kp)
   const std::size_t total = static_cast<std::size_t>(level_off_[depth + 1]);
   std::vector<double> padded(total);
   ANKH_CUDA(cudaMemcpy(padded.data(), d_exp_, total * sizeof(double), cudaMemcpyDeviceToHost));
-  const std::size_t cells = total / static_cast<std::size_t>(Kp);
-  for (std::size_t c = 0; c < cells && (c + 1) * K <= count; ++c)
-    std::memcpy(out + c * K, padded.data() + c * Kp, K * sizeof(double));
+  std::size_t o = 0;
+  for (int l = 0; l <= depth; ++l) {
+    const unsigned nl = 1u << l;
+    for (unsigned c = 0; c < (1u << (3 * l)); ++c, o += K) {
+      if (o + K > count) return;
+      const unsigned m = morton3(c / (nl * nl), (c / nl) % nl, c % nl);
+      std::memcpy(out + o, padded.data() + level_off_[l] + static_cast<std::size_t>(m) * Kp,
+                  K * sizeof(double));
+    }
+  }
+}
+
+void Plan::enqueue_phase(int phase, const double* d_pos, const double* d_src, cudaStream_t st) {
+  if (!st) st = stream_;
+  last_stream_ = st;
+  if (phase == 1) evaluated_ = true;
+  if (n == 0 || pending_code_ != 0) {
+    if (phase == 1) enqueue(d_pos, d_src, st);
+    return;
+  }
+  launch_all(d_pos, d_src, st, phase == 1 ? 1 : 2);
+}
+
+double* Plan::leaf_level(std::int64_t* begin, std::int64_t* end, int* row_stride) {
+  if (begin) *begin = p2m_begin_;
+  if (end) *end = p2m_end_;
+  if (row_stride) *row_stride = Kp;
+  return d_exp_ + level_off_[depth];
+}
+
+void Plan::attach_collective(Collective* c) {
+  if (c && (c->world() != cfg.world || c->rank() != cfg.rank)) {
+    delete c;
+    throw AnkhError(ANKH_INVALID_ARGUMENT, "collective rank/world does not match the plan's shard");
+  }
+  coll_.reset(c);
+  if (graph_exec_) {  // recapture with the collectives in the graph
+    cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+    graph_pos_ = graph_src_ = graph_warm_pos_ = graph_warm_src_ = nullptr;
+  }
 }
 
 void Plan::m2l_factors(int level, const int* offset, double* lmat, double* rmat, int max_rank,
@@ -597,7 +673,7 @@ void Plan::energies_to_device(double* d_out, cudaStream_t st) {
     ANKH_CUDA(cudaMemsetAsync(d_out, 0, 4 * sizeof(double), st));
     return;
   }
-  static_assert(offsetof(DevResult, e_self) == 0 && offsetof(DevResult, e_periodic) == 24,
+  static_assert(offsetof(DevResult, red) == 0 && kESelf == 0 && kEPeriodic == 3,
                 "DevResult energy layout");
   ANKH_CUDA(cudaMemcpyAsync(d_out, d_res_, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }

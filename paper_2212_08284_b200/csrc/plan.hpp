@@ -4,11 +4,13 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "../../include/ankh_b200.h"
+#include "collective.hpp"
 #include "kernels.cuh"
 
 namespace ankh_b200 {
@@ -60,6 +62,18 @@ class Plan {
   /// Enqueue a device copy of {e_self, e_near, e_far, e_periodic} (4 doubles).
   void energies_to_device(double* d_out, cudaStream_t st);
 
+  /// Shard exchange driven by the caller (in-process shards, tests): phase 1
+  /// runs validation/binning/sort/gather and this shard's P2M; the caller then
+  /// completes the Morton leaf level (rows outside [p2m_begin, p2m_end)); phase
+  /// 2 runs M2M, M2L, P2P, the periodic term and the final reduction.
+  void enqueue_phase(int phase, const double* d_pos, const double* d_src, cudaStream_t st);
+  /// Device pointer to the Morton-ordered leaf level (rows of Kp doubles) and
+  /// this shard's P2M row range.
+  double* leaf_level(std::int64_t* begin, std::int64_t* end, int* row_stride);
+  /// Attach an NCCL (or other) collective: the plan then all-gathers the leaf
+  /// level and all-reduces the result itself; reports carry job totals.
+  void attach_collective(Collective* c);
+
   cudaStream_t stream() const { return stream_; }
 
   // ---- geometry (public for introspection) ----
@@ -80,8 +94,14 @@ class Plan {
   void build_periodic();
   void allocate();
   void* dalloc(std::size_t bytes);
-  void launch_all(const double* d_pos, const double* d_src, cudaStream_t st);
+  /// mode 0: whole evaluation; 1: up to this shard's P2M; 2: from M2M on.
+  void launch_all(const double* d_pos, const double* d_src, cudaStream_t st, int mode = 0);
   void validate_only(const double* d_pos, const double* d_src, cudaStream_t st);
+  void exchange_leaves(cudaStream_t st);
+
+  std::unique_ptr<Collective> coll_;
+  bool shard_upward_ = false;               // P2M split across shards (+ all-gather)
+  std::int64_t p2m_begin_ = 0, p2m_end_ = 0;  // Morton leaf rows this shard computes
 
   int device_ = 0;
   cudaStream_t stream_ = nullptr;
