@@ -230,17 +230,26 @@ def main():
     # ---- plan (geometry-only precompute, not timed) ----
     t0 = time.perf_counter()
     plan = ankh.Plan(n, rb, ecfg, threads=0, device=local, rank=rank, world=world, phase_timing=False)
+
+    def attach(p):
+        # the shards' exchanges (leaf-level all-gather, result all-reduce) run
+        # inside the plan on its own NCCL communicator; torch.distributed only
+        # carries the 128-byte id
+        if dist is None:
+            return
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(ankh.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        p.attach_nccl(bytes(uid.cpu().numpy().tobytes()))
+
+    attach(plan)
     plan_s = time.perf_counter() - t0
     dp = torch.from_numpy(pos).cuda()
     ds = torch.from_numpy(src).cuda()
-    ebuf = torch.zeros(4, dtype=torch.float64, device="cuda")
 
     def step():
         plan.enqueue(dp, ds, sptr)
-        if dist is not None:
-            plan.energies_to(ebuf, sptr)
-            with torch.cuda.stream(stream):
-                dist.all_reduce(ebuf)
 
     fp64_peak = ankh.lib().ankh_probe_fp64_tflops_v1(8192)
     for _ in range(max(3, args.warmup)):
@@ -266,19 +275,15 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    res = plan.result()
-    if dist is not None:
-        torch.cuda.synchronize()
-        e = ebuf.cpu().numpy()
-        e_total = float(e.sum())
-    else:
-        e_total = res.e_total
+    res = plan.result()  # job totals (NCCL all-reduce inside the plan when world > 1)
+    e_total = res.e_total
     ms_per_step = ms / args.steps
     value = 1000.0 / ms_per_step
     launches_per_step = res.gpu_launches
 
     # ---- roofline pass: per-phase CUDA events on the launching stream ----
     plan_t = ankh.Plan(n, rb, ecfg, threads=0, device=local, rank=rank, world=world, phase_timing=True)
+    attach(plan_t)
     phase = {k: [] for k in ("precompute", "interpolation", "far_field", "near_field", "periodic_far", "self")}
     pairs = 0
     far_flops = plan_t_far = 0.0
@@ -309,11 +314,7 @@ def main():
         def e2e_step():
             if world == 1:
                 return ankh.fmm_energy(sys_, ecfg).e_total
-            r2 = plan.energy(hpos, hsrc)  # host buffers through the plan C-ABI
-            v = torch.tensor([r2.e_self, r2.e_near, r2.e_far, r2.e_periodic_far],
-                             dtype=torch.float64, device="cuda")
-            dist.all_reduce(v)
-            return float(v.sum().item())
+            return plan.energy(hpos, hsrc).e_total  # host buffers through the plan C-ABI; job total
 
         for _ in range(2):
             e2e_step()
@@ -329,9 +330,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e = float(t.item())
         e2e = {"value": k2 / t_e2e, "unit": "evals/s", "h2d_bytes_per_step": int(pos.nbytes + src.nbytes),
-               "d2h_bytes_per_step": 72 if world == 1 else 72 + 32, "steps": k2,
+               "d2h_bytes_per_step": 72, "steps": k2,
                "api": "ankh_fmm_energy_v1 (one-shot drop-in, plan cache warm)" if world == 1
-               else "ankh_plan_energy_v1 per rank + NCCL all-reduce"}
+               else "ankh_plan_energy_v1 per rank (NCCL exchanges inside the plan)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -60,14 +60,14 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
   // leaves are visited (and their expansions stored) in Morton order
   const unsigned m = m_begin + blockIdx.x * kP2MWarps + warp;
   if (m >= m_end) return;
-  const unsigned leaf = morton_to_lex(m, n);
+  const int ci0 = static_cast<int>(morton_compact3(m >> 2)),
+            ci1 = static_cast<int>(morton_compact3(m >> 1)), ci2 = static_cast<int>(morton_compact3(m));
+  const unsigned leaf = (static_cast<unsigned>(ci0) * n + ci1) * n + ci2;
   const unsigned begin = leaf_off[leaf];
   const int cnt = static_cast<int>(leaf_off[leaf + 1] - begin);
   double* out = exp_leaf + static_cast<std::size_t>(m) * KS;
   // cell_geometry (octree.cpp:18-25)
   const double rad = rb / n;
-  const int ci0 = static_cast<int>(leaf) / (n * n), ci1 = (static_cast<int>(leaf) / n) % n,
-            ci2 = static_cast<int>(leaf) % n;
   const double c0 = -rb + rad * (2 * ci0 + 1), c1 = -rb + rad * (2 * ci1 + 1),
                c2 = -rb + rad * (2 * ci2 + 1);
   const double inv_rad = 1.0 / rad;

@@ -47,7 +47,11 @@ __host__ __device__ constexpr int exp_stride(int k) { return (k + 31) / 32 * 32;
 // Everything a shard contributes additively sits in red[] so one all-reduce
 // (sum) combines shards: energies, the pair counter (exact in a double up to
 // 2^53) and the error flags (> 0 means raised somewhere).
-enum RedSlot { kESelf = 0, kENear, kEFar, kEPeriodic, kNearPairs, kDuplicate, kCoincident, kRedCount = 8 };
+// slots [0, kRedShared) are all-reduced across shards; the rest stay per shard
+enum RedSlot {
+  kESelf = 0, kENear, kEFar, kEPeriodic, kDuplicate, kCoincident, kRedShared,
+  kNearPairs = kRedShared, kRedCount = 8
+};
 
 struct DevResult {
   double red[kRedCount];

@@ -467,7 +467,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   ++launches;
   // shards: one all-reduce of the energy / counter / flag vector (the path's
   // only exchange besides the leaf all-gather)
-  if (coll_) coll_->allreduce_sum(d_res_->red, kRedCount, st);
+  if (coll_) coll_->allreduce_sum(d_res_->red, kRedShared, st);
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[6], st));
   ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
   ANKH_CUDA(cudaGetLastError());
@@ -492,6 +492,10 @@ void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
     validate_only(d_pos, d_src, st);
     return;
   }
+  if (shard_upward_ && !coll_)
+    throw AnkhError(ANKH_RUNTIME_ERROR,
+                    "sharded plan (world > 1) needs ankh_plan_attach_nccl_v1 or the "
+                    "ankh_plan_enqueue_phase_v1 exchange");
   // Repeated evaluations on the same input buffers replay a CUDA graph of the
   // whole launch sequence (captured on the second such call, after the first
   // has set every kernel attribute); phase timing keeps plain launches.
