@@ -91,8 +91,6 @@ __global__ void __launch_bounds__(256) k_gather(const double* __restrict__ pos,
 #pragma unroll
   for (int k = 0; k < 10; ++k) r[3 + k] = src[10 * i + k];
   r[13] = (r[7] + r[10]) + r[12];  // SymMat3::trace (types.hpp:57)
-  r[14] = 0.0;
-  r[15] = 0.0;
   double2* out = reinterpret_cast<double2*>(part + j * kRec);
 #pragma unroll
   for (int k = 0; k < kRec / 2; ++k) out[k] = make_double2(r[2 * k], r[2 * k + 1]);
@@ -103,6 +101,7 @@ __global__ void k_init_result(DevResult* res) {
   res->min_nonfinite = ~0ull;
   res->min_outside = ~0ull;
   res->any_multipole = 0;
+  res->p2p_next = 0;
 }
 
 // Exact-duplicate scan over (key, index)-sorted particles: duplicates share a

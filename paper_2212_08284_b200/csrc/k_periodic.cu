@@ -183,7 +183,8 @@ __device__ double block_sum(double v, double* red) {
 
 __global__ void __launch_bounds__(kFinThreads) k_finalize(
     const double* __restrict__ near_partial, int n_near,
-    const unsigned long long* __restrict__ pair_count, const double* __restrict__ far_partial,
+    const unsigned long long* __restrict__ pair_count, int n_count,
+    const double* __restrict__ far_partial,
     int n_far, const double* __restrict__ self_partial, int n_self, double self_scale,
     const double* __restrict__ periodic, int use_periodic, int include_self, DevResult* res) {
   __shared__ double red[kFinThreads];
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(
   const double self_acc = block_sum(a, red);
   unsigned long long c = 0;
   if (pair_count)
-    for (int i = threadIdx.x; i < n_near; i += kFinThreads) c += pair_count[i];
+    for (int i = threadIdx.x; i < n_count; i += kFinThreads) c += pair_count[i];
   redu[threadIdx.x] = c;
   __syncthreads();
   for (int s = kFinThreads / 2; s > 0; s >>= 1) {
@@ -238,10 +239,11 @@ void launch_periodic_eval(const double* root, const double* to_equi, const doubl
 }
 
 void launch_finalize(const double* near_partial, int n_near, const unsigned long long* pair_count,
-                     const double* far_partial, int n_far, const double* self_partial,
+                     int n_count, const double* far_partial, int n_far, const double* self_partial,
                      int n_self, double self_scale, const double* periodic, int use_periodic,
                      int include_self, DevResult* res, cudaStream_t st) {
-  k_finalize<<<1, kFinThreads, 0, st>>>(near_partial, n_near, pair_count, far_partial, n_far,
+  k_finalize<<<1, kFinThreads, 0, st>>>(near_partial, n_near, pair_count, n_count, far_partial,
+                                        n_far,
                                         self_partial, n_self, self_scale, periodic, use_periodic,
                                         include_self, res);
 }

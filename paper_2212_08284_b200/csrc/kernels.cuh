@@ -1,12 +1,13 @@
 // Device-side declarations shared by the sm_100a kernels and the host plan.
 //
 // HBM layout (all float64 unless noted):
-//   part    : N x 16   particle records sorted by lex leaf id, ascending input
+//   part    : N x 14   particle records sorted by lex leaf id, ascending input
 //                      index inside a leaf (== build_tree bucket order,
 //                      octree.cpp:27-45): x y z q mux muy muz Txx Txy Txz Tyy
-//                      Tyz Tzz tr(Theta) 0 0   (128 B, 16-B aligned)
+//                      Tyz Tzz tr(Theta)   (112 B, 16-B aligned; a leaf's
+//                      records are one contiguous byte range for bulk copies)
 //   leaf_off: 8^E + 1  uint32 leaf CSR offsets into `part`
-//   exp     : sum_l 8^l x K   expansions, level-major, lex cell order
+//   exp     : sum_l 8^l x Kp  expansions, level-major, Morton cell order
 //   factors : per M2L operator, L (kp x Kp) then R (kp x Kp), zero padded
 //   inst    : uint2 (t, s) canonical M2L instances grouped by operator
 #pragma once
@@ -16,7 +17,7 @@
 
 namespace ankh_b200 {
 
-constexpr int kRec = 16;          // doubles per particle record
+constexpr int kRec = 14;          // doubles per particle record (112 B: x y z q mu Theta tr)
 constexpr int kM2LTile = 64;      // instances per M2L CTA
 constexpr int kM2LChunk = 32;     // node columns per staged chunk
 constexpr int kMaxKp8 = 16;       // ranks up to 128
@@ -58,6 +59,7 @@ struct DevResult {
   unsigned long long min_nonfinite;  // lowest index with a non-finite value (same on every shard)
   unsigned long long min_outside;    // lowest finite index outside the box
   int any_multipole;                 // some particle has mu or Theta != 0
+  unsigned p2p_next;                 // dynamic leaf counter of the pipelined P2P kernel
 };
 
 struct M2LTile {
@@ -92,11 +94,16 @@ void launch_m2l(const double* exp, const long long* level_off, const double* fac
                 const M2LOp* ops, const M2LTile* tiles, int n_tiles_class, int kp8,
                 const int* tile_ids, const uint2* inst, int K, int Kp, double* far_partial,
                 cudaStream_t st);
-void launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
-                double period, double xi, int nterms, int tpb, int cap, int leaf_begin,
-                int leaf_end,
-                double* near_partial, unsigned long long* pair_count, DevResult* res,
-                cudaStream_t st);
+/// Near field.  pipe = 0: one CTA per target leaf (near_partial[leaf]);
+/// pipe = 1: persistent CTAs fed by a 2-slot bulk-copy ring, dynamic leaf
+/// scheduling, near_partial[leaf * p2p_pipe_warps(tpb) + warp].  Returns the
+/// number of near partials written.
+int launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
+               double period, double xi, int nterms, int tpb, int cap, int pipe, int leaf_begin,
+               int leaf_end, double* near_partial, unsigned long long* pair_count, DevResult* res,
+               cudaStream_t st);
+int p2p_pipe_warps(int tpb);
+int p2p_pipe_max_cap();
 int p2p_terms_for(double s_max);
 int p2p_max_cap();
 void launch_periodic_gen(double* gen, int order, double box_radius, double xi, int p,
@@ -104,7 +111,7 @@ void launch_periodic_gen(double* gen, int order, double box_radius, double xi, i
 void launch_periodic_eval(const double* root, const double* to_equi, const double* spec_re,
                           int order, double* out, cudaStream_t st);
 void launch_finalize(const double* near_partial, int n_near, const unsigned long long* pair_count,
-                     const double* far_partial, int n_far, const double* self_partial,
+                     int n_count, const double* far_partial, int n_far, const double* self_partial,
                      int n_self, double self_scale, const double* periodic, int use_periodic,
                      int include_self, DevResult* res, cudaStream_t st);
 void launch_init_result(DevResult* res, cudaStream_t st);

@@ -148,7 +148,14 @@ void Plan::build_geometry() {
   p2p_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.3 / 32.0)) * 32;
   p2p_cap_ = std::max(256, std::min(p2p_cap_, 960));
   if (const char* e = std::getenv("ANKH_P2P_TPB")) p2p_tpb_ = std::atoi(e) == 128 ? 128 : 256;
-  if (const char* e = std::getenv("ANKH_P2P_CAP")) p2p_cap_ = std::max(64, std::atoi(e));
+  // pipelined P2P (ANKH_P2P_PIPE=1): a 2-slot ring of p2p_pipe_cap_ staged sources
+  p2p_pipe_ = 0;
+  p2p_pipe_cap_ = 320;
+  if (const char* e = std::getenv("ANKH_P2P_PIPE")) p2p_pipe_ = std::atoi(e) != 0 ? 1 : 0;
+  if (const char* e = std::getenv("ANKH_P2P_CAP")) {
+    p2p_cap_ = std::max(64, std::atoi(e));
+    p2p_pipe_cap_ = std::min(p2p_cap_, p2p_pipe_max_cap());
+  }
 }
 
 void Plan::allocate() {
@@ -175,7 +182,8 @@ void Plan::allocate() {
                             cudaMemcpyHostToDevice, stream_));
   n_self_blocks_ = static_cast<int>((nn + 255) / 256);
   d_self_part_ = static_cast<double*>(dalloc(n_self_blocks_ * sizeof(double)));
-  d_near_part_ = static_cast<double*>(dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(double)));
+  d_near_part_ = static_cast<double*>(dalloc(std::max(leaf_end_ - leaf_begin_, 1) *
+                                             std::max(p2p_pipe_warps(p2p_tpb_), 1) * sizeof(double)));
   d_pair_count_ = static_cast<unsigned long long*>(
       dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(unsigned long long)));
   d_per_ = static_cast<double*>(dalloc(sizeof(double)));
@@ -451,8 +459,10 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   }
   if (!serial) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
-  launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_,
-             p2p_cap_, leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, st);
+  const int n_near_parts =
+      launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_,
+                 p2p_pipe_ ? p2p_pipe_cap_ : p2p_cap_, p2p_pipe_, leaf_begin_, leaf_end_,
+                 d_near_part_, d_pair_count_, d_res_, st);
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));
   if (serial && do_periodic) {
@@ -461,7 +471,8 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   }
   if (!serial) ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[5], st));
-  launch_finalize(d_near_part_, leaf_end_ - leaf_begin_, d_pair_count_, d_far_part_, n_tiles_,
+  launch_finalize(d_near_part_, n_near_parts, d_pair_count_, leaf_end_ - leaf_begin_, d_far_part_,
+                  n_tiles_,
                   d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
                   include_self_ ? 1 : 0, d_res_, st);
   ++launches;

@@ -154,6 +154,8 @@ class Plan {
   int nterms_ = 14;
   int p2p_tpb_ = 256;
   int p2p_cap_ = 512;
+  int p2p_pipe_ = 0;
+  int p2p_pipe_cap_ = 320;
   std::uint32_t launches_ = 0;
   // timing
   cudaEvent_t ev_[8] = {};
