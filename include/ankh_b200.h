@@ -178,6 +178,15 @@ int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, ui
                                 uint32_t* t, uint32_t* s, int32_t* offset, size_t capacity,
                                 size_t* count);
 
+/* Near-field radial polynomials the plan uses for a given s_max = xi^2 d_max^2
+ * (d_max = the largest near-pair distance, 2 sqrt(3) leaf sides): coefficients
+ * (14 each, in s = xi^2 r^2) of P(s) = erf(sqrt s)/sqrt s and
+ * G(s) = (2/sqrt(pi)) exp(-s) -- the reference's erfc_screen / radial
+ * (kernel.cpp:14-51) -- valid for s <= *s_lim, and the fit's measured max
+ * relative error.  Diagnostics (no reference counterpart); host only. */
+int ankh_radial_fit_v1(double s_max, int* nterms, double* s_lim, double* p, double* g,
+                       double* max_err);
+
 /* Measured FP64 (DFMA) throughput of the current device in TFLOP/s: the
  * roofline denominator for the FP64-bound kernels (no reference counterpart). */
 double ankh_probe_fp64_tflops_v1(int iters);

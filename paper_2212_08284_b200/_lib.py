@@ -36,6 +36,7 @@ EXPORTS = [
     "ankh_device_copy_v1",
     "ankh_nccl_unique_id_v1",
     "ankh_plan_attach_nccl_v1",
+    "ankh_radial_fit_v1",
 ]
 
 
@@ -91,6 +92,7 @@ def lib() -> ctypes.CDLL:
         L.ankh_device_copy_v1.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, cp, c_size_t]
         L.ankh_nccl_unique_id_v1.argtypes = [ctypes.c_char_p, cp, c_size_t]
         L.ankh_plan_attach_nccl_v1.argtypes = [c_void_p, ctypes.c_char_p, cp, c_size_t]
+        L.ankh_radial_fit_v1.argtypes = [c_double, I, D, D, D, D]
         L.ankh_version_v1.argtypes = []
         L.ankh_version_v1.restype = ctypes.c_char_p
         _lib = L

@@ -5,6 +5,7 @@
 #include <memory>
 #include <mutex>
 
+#include "host_numerics.hpp"
 #include "plan.hpp"
 #include "shard.hpp"
 
@@ -289,6 +290,21 @@ int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, ui
       }
     }
     *count = c;
+    return ANKH_OK;
+  } catch (...) {
+    return ANKH_RUNTIME_ERROR;
+  }
+}
+
+int ankh_radial_fit_v1(double s_max, int* nterms, double* s_lim, double* p, double* g,
+                       double* max_err) {
+  try {
+    const ankh_b200::RadialFit f = ankh_b200::fit_radial(s_max);
+    if (nterms) *nterms = f.nterms;
+    if (s_lim) *s_lim = f.s_lim;
+    if (max_err) *max_err = f.max_err;
+    if (p) std::memcpy(p, f.p, sizeof f.p);
+    if (g) std::memcpy(g, f.g, sizeof f.g);
     return ANKH_OK;
   } catch (...) {
     return ANKH_RUNTIME_ERROR;

@@ -21,6 +21,113 @@ void cheb_values(int order, double x, double* t) {
 }
 }  // namespace
 
+namespace {
+using LD = long double;
+const LD kTwoOverSqrtPiL = 1.12837916709551257389615890312154517L;
+
+LD p_exact(LD s) {  // erf(sqrt s)/sqrt s = (2/sqrt(pi)) sum (-s)^n / (n! (2n+1)), s <= 0.25
+  LD term = kTwoOverSqrtPiL, sum = 0.0L;
+  for (int n = 0; n < 40; ++n) {
+    sum += term / (2 * n + 1);
+    term *= -s / (n + 1);
+  }
+  return sum;
+}
+LD g_exact(LD s) { return kTwoOverSqrtPiL * std::exp(-s); }
+
+// Interpolate f at n Chebyshev nodes of [0, a]; monomial coefficients in s.
+bool cheb_fit(LD (*f)(LD), LD a, int n, double* out) {
+  std::vector<LD> u(n), y(n), m(static_cast<std::size_t>(n) * n);
+  const LD pi = 3.14159265358979323846264338327950288L;
+  for (int i = 0; i < n; ++i) {
+    u[i] = (std::cos((2 * i + 1) * pi / (2 * n)) + 1.0L) / 2.0L;  // nodes of [0, 1]
+    y[i] = f(u[i] * a);
+    LD p = 1.0L;
+    for (int k = 0; k < n; ++k) {
+      m[static_cast<std::size_t>(i) * n + k] = p;
+      p *= u[i];
+    }
+  }
+  // Gaussian elimination with partial pivoting (n <= 12)
+  std::vector<LD> c = y;
+  std::vector<LD> a2 = m;
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (std::fabs(a2[static_cast<std::size_t>(r) * n + col]) >
+          std::fabs(a2[static_cast<std::size_t>(piv) * n + col]))
+        piv = r;
+    if (a2[static_cast<std::size_t>(piv) * n + col] == 0.0L) return false;
+    if (piv != col) {
+      for (int k = 0; k < n; ++k)
+        std::swap(a2[static_cast<std::size_t>(piv) * n + k], a2[static_cast<std::size_t>(col) * n + k]);
+      std::swap(c[piv], c[col]);
+    }
+    for (int r = col + 1; r < n; ++r) {
+      const LD f2 = a2[static_cast<std::size_t>(r) * n + col] / a2[static_cast<std::size_t>(col) * n + col];
+      for (int k = col; k < n; ++k)
+        a2[static_cast<std::size_t>(r) * n + k] -= f2 * a2[static_cast<std::size_t>(col) * n + k];
+      c[r] -= f2 * c[col];
+    }
+  }
+  for (int r = n - 1; r >= 0; --r) {
+    for (int k = r + 1; k < n; ++k) c[r] -= a2[static_cast<std::size_t>(r) * n + k] * c[k];
+    c[r] /= a2[static_cast<std::size_t>(r) * n + r];
+  }
+  LD scale = 1.0L;
+  for (int k = 0; k < n; ++k) {
+    out[k] = static_cast<double>(c[k] / scale);  // u = s / a
+    scale *= a;
+  }
+  return true;
+}
+
+// max relative error of the double-coefficient polynomial on [0, a]
+LD fit_error(LD (*f)(LD), const double* c, int n, LD a) {
+  LD worst = 0.0L;
+  for (int i = 0; i <= 2000; ++i) {
+    const LD s = a * i / 2000;
+    LD h = c[n - 1];
+    for (int k = n - 2; k >= 0; --k) h = h * s + c[k];
+    worst = std::max(worst, std::fabs((h - f(s)) / f(s)));
+  }
+  return worst;
+}
+}  // namespace
+
+RadialFit fit_radial(double s_max) {
+  RadialFit r{};
+  if (s_max <= 0.25) {
+    const LD a = std::max(static_cast<LD>(s_max), 1e-12L);
+    for (int n : {6, 7, 8, 9, 10, 12}) {
+      double p[14] = {}, g[14] = {};
+      if (!cheb_fit(p_exact, a, n, p) || !cheb_fit(g_exact, a, n, g)) continue;
+      const LD e = std::max(fit_error(p_exact, p, n, a), fit_error(g_exact, g, n, a));
+      if (e <= 2e-16L) {
+        r.nterms = n;
+        r.s_lim = s_max;
+        r.max_err = static_cast<double>(e);
+        std::copy(p, p + 14, r.p);
+        std::copy(g, g + 14, r.g);
+        return r;
+      }
+    }
+  }
+  // Maclaurin, 14 terms (truncation < 1e-18 for s <= 0.25), libm beyond
+  r.nterms = 14;
+  r.s_lim = 0.25;
+  LD tp = kTwoOverSqrtPiL, tg = kTwoOverSqrtPiL;
+  for (int k = 0; k < 14; ++k) {
+    r.p[k] = static_cast<double>(tp / (2 * k + 1));
+    r.g[k] = static_cast<double>(tg);
+    tp *= -1.0L / (k + 1);
+    tg *= -1.0L / (k + 1);
+  }
+  r.max_err = static_cast<double>(
+      std::max(fit_error(p_exact, r.p, 14, 0.25L), fit_error(g_exact, r.g, 14, 0.25L)));
+  return r;
+}
+
 double erfc_screen(double z) {
   if (z >= 0.0 && z <= 0.5) {
     const double z2 = z * z;

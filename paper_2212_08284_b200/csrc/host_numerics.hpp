@@ -12,6 +12,23 @@
 
 namespace ankh_b200 {
 
+/// P2P radial polynomials in s = xi^2 r^2 on [0, s_max] (s_max from the
+/// plan's largest near distance): P(s) = erf(sqrt s) / sqrt s and
+/// G(s) = (2/sqrt(pi)) exp(-s), so that erfc(xi r) / r = 1/r - xi P(s) and
+/// the Gaussian factor of radial (kernel.cpp:26-38) is xi G(s).  Fitted in
+/// long double at Chebyshev nodes with the fewest terms (from 6..10, 12) whose
+/// double coefficients stay within 2e-16 relative error of both functions on
+/// a dense grid -- the accuracy of the reference's own series, with fewer
+/// terms than a Maclaurin polynomial.  Beyond s_max = 0.25 (huge leaves):
+/// 14-term Maclaurin up to s = 0.25 and libm erfc / exp past it (nterms 14).
+struct RadialFit {
+  int nterms;
+  double s_lim;     // polynomial valid for s <= s_lim
+  double max_err;   // measured max relative error of the fit on [0, s_lim]
+  double p[14], g[14];
+};
+RadialFit fit_radial(double s_max);
+
 /// kernel.cpp:14-23, 48-51: 13-term Maclaurin erf for 0 <= z <= 0.5, else erfc.
 double erfc_screen(double z);
 

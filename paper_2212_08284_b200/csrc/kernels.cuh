@@ -94,17 +94,24 @@ void launch_m2l(const double* exp, const long long* level_off, const double* fac
                 const M2LOp* ops, const M2LTile* tiles, int n_tiles_class, int kp8,
                 const int* tile_ids, const uint2* inst, int K, int Kp, double* far_partial,
                 cudaStream_t st);
+/// Radial polynomials of the near field in s = xi^2 r^2 (host_numerics.hpp
+/// fit_radial): P(s) = erf(sqrt s)/sqrt s, G(s) = (2/sqrt(pi)) exp(-s).
+struct P2PRadial {
+  int nterms;    // 6..10, 12: fitted on [0, s_lim], no range test; 14: libm past s_lim
+  double s_lim;
+  double p[14], g[14];
+};
+
 /// Near field.  pipe = 0: one CTA per target leaf (near_partial[leaf]);
-/// pipe = 1: persistent CTAs fed by a 2-slot bulk-copy ring, dynamic leaf
-/// scheduling, near_partial[leaf * p2p_pipe_warps(tpb) + warp].  Returns the
+/// pipe = 1: persistent CTAs fed by a bulk-copy ring, dynamic leaf
+/// scheduling, near_partial[leaf * p2p_pipe_warps(256) + warp].  Returns the
 /// number of near partials written.
 int launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
-               double period, double xi, int nterms, int tpb, int cap, int pipe, int leaf_begin,
+               double period, double xi, const P2PRadial& rad, int cap, int pipe, int leaf_begin,
                int leaf_end, double* near_partial, unsigned long long* pair_count, DevResult* res,
                cudaStream_t st);
 int p2p_pipe_warps(int tpb);
 int p2p_pipe_max_cap();
-int p2p_terms_for(double s_max);
 int p2p_max_cap();
 void launch_periodic_gen(double* gen, int order, double box_radius, double xi, int p,
                          cudaStream_t st);

@@ -139,15 +139,20 @@ void Plan::build_geometry() {
   // (2 leaf sides per axis): s_max = xi^2 (2 sqrt(3) * 2 r_B / n)^2
   const double side = 2.0 * rb / nax;
   const double dmax = 2.0 * std::sqrt(3.0) * side * 1.0001;
-  nterms_ = p2p_terms_for(cfg.xi * cfg.xi * dmax * dmax);
-  // P2P CTA: 256 threads (2 CTAs/SM, 16 warps), staged-source capacity sized
+  {
+    const RadialFit f = fit_radial(cfg.xi * cfg.xi * dmax * dmax);
+    radial_.nterms = f.nterms;
+    radial_.s_lim = f.s_lim;
+    std::copy(f.p, f.p + 14, radial_.p);
+    std::copy(f.g, f.g + 14, radial_.g);
+  }
+  // P2P CTA: 256 threads (3 CTAs/SM, 24 warps), staged-source capacity sized
   // so a leaf's own + 13 neighbour leaves (~14 x mean occupancy) fit in one
-  // pass for almost every leaf.  ANKH_P2P_TPB / ANKH_P2P_CAP override (tuning).
+  // pass for almost every leaf.  ANKH_P2P_CAP overrides (tuning).
   const double per_leaf = static_cast<double>(n) / n_leaves;
   p2p_tpb_ = 256;
   p2p_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.3 / 32.0)) * 32;
   p2p_cap_ = std::max(256, std::min(p2p_cap_, 960));
-  if (const char* e = std::getenv("ANKH_P2P_TPB")) p2p_tpb_ = std::atoi(e) == 128 ? 128 : 256;
   // pipelined P2P (ANKH_P2P_PIPE=1): a 2-slot ring of p2p_pipe_cap_ staged sources
   p2p_pipe_ = 0;
   p2p_pipe_cap_ = 320;
@@ -460,7 +465,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   if (!serial) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
   const int n_near_parts =
-      launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, nterms_, p2p_tpb_,
+      launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
                  p2p_pipe_ ? p2p_pipe_cap_ : p2p_cap_, p2p_pipe_, leaf_begin_, leaf_end_,
                  d_near_part_, d_pair_count_, d_res_, st);
   ++launches;

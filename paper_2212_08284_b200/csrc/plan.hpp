@@ -151,7 +151,7 @@ class Plan {
   int n_self_blocks_ = 0;
   DevResult* d_res_ = nullptr;
   DevResult* h_res_ = nullptr;
-  int nterms_ = 14;
+  P2PRadial radial_{};  // near-field radial polynomials (fit_radial)
   int p2p_tpb_ = 256;
   int p2p_cap_ = 512;
   int p2p_pipe_ = 0;

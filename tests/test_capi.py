@@ -90,3 +90,36 @@ def test_product_does_not_import_oracle():
                     text = f.read()
                 assert "ankh_oracle" not in text and "libankh_ref" not in text, fn
                 assert "import ref" not in text, fn
+
+
+@pytest.mark.parametrize("s_max, want_nt", [(0.0212, 6), (0.0556, 7), (0.0718, 8), (0.167, 9),
+                                            (0.25, 9), (0.4, 14)])
+def test_radial_fit_is_roundoff_accurate(s_max, want_nt):
+    """The near-field radial polynomials (host fit, no GPU needed) reproduce
+    erf(sqrt s)/sqrt s and (2/sqrt pi) exp(-s) -- the functions behind
+    erfc_screen / radial, kernel.cpp:14-51 -- to 2e-16 relative on the plan's
+    range, checked here independently in numpy long double."""
+    import ctypes
+    import math
+
+    L = ankh.lib()
+    nt, sl, err = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+    p = (ctypes.c_double * 14)()
+    g = (ctypes.c_double * 14)()
+    assert L.ankh_radial_fit_v1(s_max, ctypes.byref(nt), ctypes.byref(sl), p, g, ctypes.byref(err)) == 0
+    assert nt.value == want_nt
+    ld = np.longdouble
+    two_sqrtpi = ld(2) / np.sqrt(ld(math.pi))
+    s = np.linspace(0, min(s_max, sl.value), 997).astype(ld)
+    ps = np.zeros_like(s)
+    term = np.full_like(s, two_sqrtpi)
+    for k in range(40):
+        ps += term / (2 * k + 1)
+        term *= -s / (k + 1)
+    gs = two_sqrtpi * np.exp(-s)
+    for coef, ref in ((p, ps), (g, gs)):
+        h = np.full_like(s, ld(coef[nt.value - 1]))
+        for k in range(nt.value - 2, -1, -1):
+            h = h * s + ld(coef[k])
+        assert float(np.max(np.abs((h - ref) / ref))) < 2.5e-16
+    assert err.value < 2.5e-16
