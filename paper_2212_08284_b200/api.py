@@ -204,8 +204,6 @@ def fmm_energy(system: ParticleSystem, config: Optional[EwaldConfig] = None,
     ``threads`` only sizes the host precompute pool (<= 0: all cores); the
     geometry-only plan is cached inside the library across calls.
     """
-    import time
-
     config = config or EwaldConfig()
     pos = _as_host(system.positions, 3)
     src = _as_host(system.sources, 10)
@@ -213,13 +211,11 @@ def fmm_energy(system: ParticleSystem, config: Optional[EwaldConfig] = None,
         raise InvalidArgument("fmm_energy: invalid system: positions and sources must have equal length")
     rep = _Report()
     err = ctypes.create_string_buffer(512)
-    t0 = time.perf_counter()
     code = lib().ankh_fmm_energy_v1(pos.shape[0], _ptr(pos), _ptr(src), float(system.box_radius),
                                     ctypes.byref(config._c(threads=threads)), ctypes.byref(rep),
                                     err, 512)
-    wall = time.perf_counter() - t0
     _check(code, err)
-    return EnergyReport._from_c(rep, wall)
+    return EnergyReport._from_c(rep)
 
 
 def nccl_unique_id() -> bytes:

@@ -1,4 +1,5 @@
 // C-ABI of libankh_b200.so (declared in include/ankh_b200.h).
+#include <chrono>
 #include <cstring>
 #include <vector>
 #include <list>
@@ -90,6 +91,7 @@ int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
     if (!cfg || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null config or report");
     if (n > 0 && (!positions || !sources)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
     ankh_b200::validate_config(*cfg);
+    const auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> lock(g_cache_mu);
     Plan* plan = nullptr;
     for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
@@ -107,6 +109,8 @@ int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
     }
     plan->enqueue_host(positions, sources, nullptr);
     plan->result(out);
+    // wall_times["total"]: the whole call, as fmm.cpp:433 times it
+    out->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 

@@ -606,9 +606,13 @@ void Plan::result(ankh_report_v1* out) {
     out->t_near_field = ms[3] * 1e-3;
     out->t_periodic_far = ms[4] * 1e-3;
     out->t_self = ms[5] * 1e-3;  // finalize (self energy is fused into binning)
+    float all = 0.f;
+    ANKH_CUDA(cudaEventElapsedTime(&all, ev_[0], ev_[6]));
+    out->t_total = all * 1e-3;  // the evaluation on the device
   }
   if (!precompute_reported) {
     out->t_precompute += precompute_seconds;
+    out->t_total += precompute_seconds;  // the plan build is part of the first call
     precompute_reported = true;
   }
 }

@@ -179,18 +179,44 @@ def write_particle_file(path: str, positions: np.ndarray, sources: np.ndarray, b
         np.savetxt(f, rows, fmt="%.17g")
 
 
+class ParticleFileError(ValueError):
+    """Malformed particle file (SPEC ParticleFile invariants); names the line."""
+
+
 def read_particle_file(path: str) -> Tuple[np.ndarray, np.ndarray, float]:
-    with open(path) as f:
-        lines = [ln for ln in f if ln.strip() and not ln.lstrip().startswith("#")]
-    head = lines[0].split()
-    n, r_b = int(head[0]), float(head[1])
+    """Parse a SPEC particle file: '#' comment lines, 'N r_B', then exactly N
+    rows of 13 finite decimals.  Errors name the 1-based file line."""
+    header = None
     rows = []
-    for lineno, ln in enumerate(lines[1:], start=2):
-        toks = ln.split()
-        if len(toks) != 13:
-            raise ValueError(f"particle file line {lineno}: expected 13 values, got {len(toks)}")
-        rows.append([float(t) for t in toks])
+    with open(path) as f:
+        for lineno, ln in enumerate(f, start=1):
+            s = ln.strip()
+            if not s or s.startswith("#"):
+                continue
+            toks = s.split()
+            if header is None:
+                if len(toks) != 2:
+                    raise ParticleFileError(f"line {lineno}: header must be 'N r_B', got {len(toks)} values")
+                try:
+                    header = (int(toks[0]), float(toks[1]))
+                except ValueError:
+                    raise ParticleFileError(f"line {lineno}: header must be 'N r_B'") from None
+                if header[0] < 0 or not np.isfinite(header[1]):
+                    raise ParticleFileError(f"line {lineno}: invalid header values")
+                continue
+            if len(toks) != 13:
+                raise ParticleFileError(f"line {lineno}: expected 13 values, got {len(toks)}")
+            try:
+                vals = [float(t) for t in toks]
+            except ValueError:
+                raise ParticleFileError(f"line {lineno}: not a decimal number") from None
+            if not all(np.isfinite(vals)):
+                raise ParticleFileError(f"line {lineno}: non-finite value")
+            rows.append(vals)
+    if header is None:
+        raise ParticleFileError("missing header line 'N r_B'")
+    n, r_b = header
     if len(rows) != n:
-        raise ValueError(f"particle file: header says {n} rows, found {len(rows)}")
+        raise ParticleFileError(f"header says {n} rows, found {len(rows)}")
     arr = np.asarray(rows, dtype=np.float64).reshape(n, 13)
     return np.ascontiguousarray(arr[:, :3]), np.ascontiguousarray(arr[:, 3:]), r_b
