@@ -47,6 +47,52 @@ CONFIG_INDEX = 3
 P2P_FLOP_PER_PAIR = 229.0
 
 
+def hbm_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return None
+
+
+def phase_rooflines(n, L, depth, ph_ms, pairs, far_flops, fp64_peak, hbm_peak, multipoles=True):
+    """% of roofline per phase, with SURVEY.md §8d's algorithmic counts
+    (each add/mul/... of the reference formula = 1 flop; bytes = compulsory
+    traffic).  Phase times are CUDA-event times on the launching stream (phase
+    timing serialises the far-field chain and the near field)."""
+    K = L ** 3
+    cells = sum(8 ** l for l in range(depth + 1))
+    children = cells - 1
+    t = 10 if multipoles else 1
+    p2m_flops = n * (9 * (3 * (L - 2) + 2 * L * L + L) + t * (L + L * L + 2 * L ** 3))
+    m2m_flops = children * (6 * L ** 4 + L ** 3)
+    rows = {
+        "bin_sort_gather": ("hbm", 256.0 * n, ph_ms["precompute"],
+                            "256 B/atom (SURVEY §8d): read x + moments, keys/index sort, 112-B records out"),
+        "p2m_m2m": ("fp64", float(p2m_flops + m2m_flops), ph_ms["interpolation"],
+                    "P2M N[9(3(L-2)+2L^2+L)+10(L+L^2+2L^3)] + M2M (6L^4+L^3)/child"),
+        "m2l": ("fp64", float(far_flops), ph_ms["far_field"], "sum over instances 4kK+2k"),
+        "p2p": ("fp64", P2P_FLOP_PER_PAIR * pairs, ph_ms["near_field"], "229 flop per unordered pair"),
+        "finalize": ("latency", None, ph_ms["self"],
+                     "final fixed-order reduction (self energy is fused into binning)"),
+        "periodic_far": ("latency", None, ph_ms["periodic_far"], "one CTA, (2L-1)^3 DFT"),
+    }
+    out = {}
+    for k, (bound, work, ms, note) in rows.items():
+        d = {"bound": bound, "ms": ms, "note": note}
+        if work is not None and ms and ms > 0:
+            if bound == "fp64":
+                ach = work / (ms * 1e-3) / 1e12
+                d.update({"work_flop": work, "achieved": ach, "unit": "TFLOP/s", "peak": fp64_peak,
+                          "frac": ach / fp64_peak if fp64_peak else None})
+            else:
+                ach = work / (ms * 1e-3) / 1e9
+                d.update({"work_bytes": work, "achieved": ach, "unit": "GB/s", "peak": hbm_peak,
+                          "frac": ach / hbm_peak if hbm_peak else None})
+        out[k] = d
+    return out
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -361,6 +407,8 @@ def main():
                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": p2p_tflops / fp64_peak if fp64_peak else None,
                          "traffic": traffic, "peak_source": "in-process DFMA probe (ankh_probe_fp64_tflops_v1)",
                          "algorithmic": f"{P2P_FLOP_PER_PAIR:.0f} flop/pair x {pairs} pairs per launch"},
+            "phase_rooflines": phase_rooflines(n, L, plan.info()["depth"], ph_ms, pairs, far_flops,
+                                               fp64_peak, hbm_peak_gbs()),
             "roofline_m2l": {"kernel": "k_m2l (DMMA)", "bound": "fp64", "achieved": m2l_tflops, "peak": fp64_peak,
                              "unit": "TFLOP/s", "frac": (m2l_tflops / fp64_peak) if (m2l_tflops and fp64_peak) else None,
                              "algorithmic": "sum over instances 4kK+2k flop"},

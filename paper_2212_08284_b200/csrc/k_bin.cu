@@ -4,9 +4,11 @@
 // self_energy (kernel.cpp:206-213).  Binning is bit-exact with the reference:
 // shifted = (x + r_B) * inv_side with inv_side = n / (2 r_B) computed on the
 // host exactly as octree.cpp:35, IEEE round-to-nearest add and multiply (no
-// FMA contraction), floor, clamp to [0, n-1].  The stable LSD radix sort keeps
-// ascending particle index inside each leaf, which is the reference's bucket
-// order.  All of it is HBM-bound (~24+80+8 B read, ~136 B written per atom).
+// FMA contraction), floor, clamp to [0, n-1].  Particles are bucketed by a
+// counting sort (leaf histogram and arrival slots from k_bin, a scan, a
+// scatter) and each leaf's indices are put back in ascending order, which is
+// the reference's bucket order (bit-exact leaf CSR).  All of it is HBM-bound
+// (104 B read, 8 B of keys/slots, 112-B records written per atom).
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -60,10 +62,12 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
       mp = (s[1] != 0.0 || s[2] != 0.0 || s[3] != 0.0 || th2 != 0.0);
     }
     keys[i] = key;
-    idx[i] = static_cast<unsigned>(i);
-    if (counts) atomicAdd(&counts[key], 1u);
+    // counting sort: idx receives the particle's arrival slot in its leaf
+    // (ascending order inside the leaf is restored by k_leaf_gather);
+    // without counts (validation path) idx is the identity for the radix sort
+    idx[i] = counts ? atomicAdd(&counts[key], 1u) : static_cast<unsigned>(i);
   }
-  if (__any_sync(0xffffffffu, mp) && (threadIdx.x & 31) == 0) atomicOr(&res->any_multipole, 1);
+  if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
   // deterministic block reduction
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
@@ -77,13 +81,23 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
   }
 }
 
-__global__ void __launch_bounds__(256) k_gather(const double* __restrict__ pos,
-                                                const double* __restrict__ src,
-                                                const unsigned* __restrict__ idx_sorted,
-                                                std::size_t n, double* __restrict__ part) {
-  const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (j >= n) return;
-  const std::size_t i = idx_sorted[j];
+// Counting-sort scatter: particle i goes to offsets[key] + slot (leaf order is
+// final, order inside a leaf is arrival order).
+__global__ void __launch_bounds__(256) k_scatter(const unsigned* __restrict__ keys,
+                                                 const unsigned* __restrict__ slots,
+                                                 const unsigned* __restrict__ offsets,
+                                                 std::size_t n, unsigned* __restrict__ unsorted) {
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (i >= n) return;
+  unsorted[offsets[keys[i]] + slots[i]] = static_cast<unsigned>(i);
+}
+
+constexpr int kLeafThreads = 128;
+constexpr int kLeafSmem = 512;  // leaves up to this size are sorted in shared memory
+
+__device__ __forceinline__ void write_record(const double* __restrict__ pos,
+                                             const double* __restrict__ src, std::size_t i,
+                                             double* __restrict__ rec) {
   double r[kRec];
   r[0] = pos[3 * i];
   r[1] = pos[3 * i + 1];
@@ -91,9 +105,64 @@ __global__ void __launch_bounds__(256) k_gather(const double* __restrict__ pos,
 #pragma unroll
   for (int k = 0; k < 10; ++k) r[3 + k] = src[10 * i + k];
   r[13] = (r[7] + r[10]) + r[12];  // SymMat3::trace (types.hpp:57)
-  double2* out = reinterpret_cast<double2*>(part + j * kRec);
+  double2* out = reinterpret_cast<double2*>(rec);
 #pragma unroll
   for (int k = 0; k < kRec / 2; ++k) out[k] = make_double2(r[2 * k], r[2 * k + 1]);
+}
+
+// One CTA per leaf: put the leaf's particle indices in ascending order (the
+// reference's bucket order, octree.cpp:42 -- indices are unique, so a rank is
+// a position) and gather its records.  Small leaves: rank sort in shared
+// memory; large ones: bottom-up merge passes in global memory (ping-pong
+// between the leaf's slices of `unsorted` and `scratch`).
+__global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
+    const double* __restrict__ pos, const double* __restrict__ src,
+    const unsigned* __restrict__ offsets, unsigned* __restrict__ unsorted,
+    unsigned* __restrict__ scratch, unsigned* __restrict__ sorted, double* __restrict__ part) {
+  __shared__ unsigned a[kLeafSmem], b[kLeafSmem];
+  const unsigned leaf = blockIdx.x;
+  const unsigned base = offsets[leaf];
+  const int c = static_cast<int>(offsets[leaf + 1] - base);
+  if (c == 0) return;
+  const unsigned* order;
+  if (c <= kLeafSmem) {
+    for (int e = threadIdx.x; e < c; e += kLeafThreads) a[e] = unsorted[base + e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < c; e += kLeafThreads) {
+      const unsigned v = a[e];
+      int rank = 0;
+      for (int j = 0; j < c; ++j) rank += a[j] < v;
+      b[rank] = v;
+      sorted[base + rank] = v;
+    }
+    __syncthreads();
+    order = b;
+  } else {
+    unsigned* x = unsorted + base;
+    unsigned* y = scratch + base;
+    for (int w = 1; w < c; w *= 2) {
+      for (int p = threadIdx.x; p < c; p += kLeafThreads) {
+        const int run = p / w, rs = run * w, ps = (run ^ 1) * w;
+        const int plen = ps < c ? min(w, c - ps) : 0;
+        const unsigned v = x[p];
+        int lo = 0, hi = plen;  // elements of the partner run below v
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (x[ps + mid] < v) lo = mid + 1; else hi = mid;
+        }
+        y[min(rs, ps) + (p - rs) + lo] = v;
+      }
+      __syncthreads();
+      unsigned* t = x;
+      x = y;
+      y = t;
+    }
+    for (int p = threadIdx.x; p < c; p += kLeafThreads) sorted[base + p] = x[p];
+    __syncthreads();
+    order = sorted + base;
+  }
+  for (int p = threadIdx.x; p < c; p += kLeafThreads)
+    write_record(pos, src, order[p], part + static_cast<std::size_t>(base + p) * kRec);
 }
 
 __global__ void k_init_result(DevResult* res) {
@@ -144,11 +213,18 @@ void launch_bin(const double* pos, const double* src, std::size_t n, double box_
                                 counts, self_partial, res);
 }
 
-void launch_gather(const double* pos, const double* src, const unsigned* idx_sorted, std::size_t n,
-                   double* part, cudaStream_t st) {
+void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
+                          const unsigned* keys, const unsigned* slots, const unsigned* counts,
+                          unsigned* offsets, unsigned* unsorted, unsigned* scratch,
+                          unsigned* sorted, std::size_t n, int n_leaves, double* part,
+                          cudaStream_t st) {
+  std::size_t bytes = temp_bytes;
+  cub::DeviceScan::ExclusiveSum(temp, bytes, counts, offsets, n_leaves + 1, st);
   if (n == 0) return;
-  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  k_gather<<<blocks, 256, 0, st>>>(pos, src, idx_sorted, n, part);
+  k_scatter<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, slots, offsets, n,
+                                                                    unsorted);
+  k_leaf_gather<<<static_cast<unsigned>(n_leaves), kLeafThreads, 0, st>>>(
+      pos, src, offsets, unsorted, scratch, sorted, part);
 }
 
 std::size_t sort_temp_bytes(std::size_t n, int n_leaves) {

@@ -79,8 +79,6 @@ struct M2LOp {
 void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
                 double inv_side, int n_axis, double xi, unsigned* keys, unsigned* idx,
                 unsigned* counts, double* self_partial, DevResult* res, cudaStream_t st);
-void launch_gather(const double* pos, const double* src, const unsigned* idx_sorted, std::size_t n,
-                   double* part, cudaStream_t st);
 std::size_t sort_temp_bytes(std::size_t n, int n_leaves);
 void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
                  const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
@@ -122,6 +120,14 @@ void launch_finalize(const double* near_partial, int n_near, const unsigned long
                      int n_self, double self_scale, const double* periodic, int use_periodic,
                      int include_self, DevResult* res, cudaStream_t st);
 void launch_init_result(DevResult* res, cudaStream_t st);
+/// Counting sort into leaves (after launch_bin with counts): scan -> offsets,
+/// scatter, per-leaf ascending order (sorted = the leaf CSR's index array) and
+/// the gather of 112-B records.  unsorted / scratch: N uints each.
+void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
+                          const unsigned* keys, const unsigned* slots, const unsigned* counts,
+                          unsigned* offsets, unsigned* unsorted, unsigned* scratch,
+                          unsigned* sorted, std::size_t n, int n_leaves, double* part,
+                          cudaStream_t st);
 double probe_fp64_tflops(int iters);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);

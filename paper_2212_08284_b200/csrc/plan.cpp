@@ -408,10 +408,11 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     launch_bin(d_pos, d_src, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_,
                d_self_part_, d_res_, st);
     ++launches;
-    launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 3 * depth, d_counts_,
-                d_off_, n_leaves, st);
-    launch_gather(d_pos, d_src, d_idx2_, n, d_part_, st);
-    ++launches;
+    // counting sort by leaf: d_idx_ holds the arrival slots, d_keys2_ the
+    // scattered indices, d_idx2_ the leaf CSR's ascending indices
+    launch_bucket_gather(d_temp_, temp_bytes_, d_pos, d_src, d_keys_, d_idx_, d_counts_, d_off_,
+                         d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_part_, st);
+    launches += 2;
   }
   if (csr_only_) {
     launches_ = launches;

@@ -128,6 +128,15 @@ def test_leaf_csr_bit_exact(cuda, ref):
         offs, idx = ankh.build_tree_csr(pos, rb, depth)
         o2, i2 = ref.leaf_csr(pos, rb, depth)
         assert np.array_equal(offs, o2) and np.array_equal(idx, i2)
+    # leaves larger than the shared-memory sort (global merge passes):
+    # ~2,500 per leaf, and one cluster of 5,000 in a single leaf
+    big, _ = inputs.random_system(20000, 3.0, seed=5)
+    clustered = np.concatenate([inputs.random_system(5000, 0.1, seed=6)[0] + 1.5,
+                                inputs.random_system(300, 3.0, seed=7)[0]])
+    for pos, rb, depth in [(big, 3.0, 1), (clustered, 3.0, 3)]:
+        offs, idx = ankh.build_tree_csr(pos, rb, depth)
+        o2, i2 = ref.leaf_csr(pos, rb, depth)
+        assert np.array_equal(offs, o2) and np.array_equal(idx, i2)
 
 
 def test_expansions_per_level(cuda, ref):
