@@ -55,7 +55,8 @@ def hbm_peak_gbs():
         return None
 
 
-def phase_rooflines(n, L, depth, ph_ms, pairs, far_flops, fp64_peak, hbm_peak, multipoles=True):
+def phase_rooflines(n, L, depth, ph_ms, pairs, far_flops, fp64_peak, hbm_peak, dmma_peak=None,
+                    multipoles=True):
     """% of roofline per phase, with SURVEY.md §8d's algorithmic counts
     (each add/mul/... of the reference formula = 1 flop; bytes = compulsory
     traffic).  Phase times are CUDA-event times on the launching stream (phase
@@ -71,7 +72,7 @@ def phase_rooflines(n, L, depth, ph_ms, pairs, far_flops, fp64_peak, hbm_peak, m
                             "256 B/atom (SURVEY §8d): read x + moments, keys/index sort, 112-B records out"),
         "p2m_m2m": ("fp64", float(p2m_flops + m2m_flops), ph_ms["interpolation"],
                     "P2M N[9(3(L-2)+2L^2+L)+10(L+L^2+2L^3)] + M2M (6L^4+L^3)/child"),
-        "m2l": ("fp64", float(far_flops), ph_ms["far_field"], "sum over instances 4kK+2k"),
+        "m2l": ("dmma", float(far_flops), ph_ms["far_field"], "sum over instances 4kK+2k"),
         "p2p": ("fp64", P2P_FLOP_PER_PAIR * pairs, ph_ms["near_field"], "229 flop per unordered pair"),
         "finalize": ("latency", None, ph_ms["self"],
                      "final fixed-order reduction (self energy is fused into binning)"),
@@ -81,10 +82,11 @@ def phase_rooflines(n, L, depth, ph_ms, pairs, far_flops, fp64_peak, hbm_peak, m
     for k, (bound, work, ms, note) in rows.items():
         d = {"bound": bound, "ms": ms, "note": note}
         if work is not None and ms and ms > 0:
-            if bound == "fp64":
+            if bound in ("fp64", "dmma"):
+                peak = dmma_peak if (bound == "dmma" and dmma_peak) else fp64_peak
                 ach = work / (ms * 1e-3) / 1e12
-                d.update({"work_flop": work, "achieved": ach, "unit": "TFLOP/s", "peak": fp64_peak,
-                          "frac": ach / fp64_peak if fp64_peak else None})
+                d.update({"work_flop": work, "achieved": ach, "unit": "TFLOP/s", "peak": peak,
+                          "frac": ach / peak if peak else None})
             else:
                 ach = work / (ms * 1e-3) / 1e9
                 d.update({"work_bytes": work, "achieved": ach, "unit": "GB/s", "peak": hbm_peak,
@@ -298,6 +300,7 @@ def main():
         plan.enqueue(dp, ds, sptr)
 
     fp64_peak = ankh.lib().ankh_probe_fp64_tflops_v1(8192)
+    dmma_peak = ankh.lib().ankh_probe_dmma_tflops_v1(0, 8192)  # m8n8k4, the M2L kernel's shape
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -408,9 +411,10 @@ def main():
                          "traffic": traffic, "peak_source": "in-process DFMA probe (ankh_probe_fp64_tflops_v1)",
                          "algorithmic": f"{P2P_FLOP_PER_PAIR:.0f} flop/pair x {pairs} pairs per launch"},
             "phase_rooflines": phase_rooflines(n, L, plan.info()["depth"], ph_ms, pairs, far_flops,
-                                               fp64_peak, hbm_peak_gbs()),
-            "roofline_m2l": {"kernel": "k_m2l (DMMA)", "bound": "fp64", "achieved": m2l_tflops, "peak": fp64_peak,
-                             "unit": "TFLOP/s", "frac": (m2l_tflops / fp64_peak) if (m2l_tflops and fp64_peak) else None,
+                                               fp64_peak, hbm_peak_gbs(), dmma_peak),
+            "roofline_m2l": {"kernel": "k_m2l (DMMA)", "bound": "fp64 tensor (DMMA)", "achieved": m2l_tflops,
+                             "peak": dmma_peak, "peak_source": "in-process DMMA m8n8k4 probe (ankh_probe_dmma_tflops_v1)",
+                             "unit": "TFLOP/s", "frac": (m2l_tflops / dmma_peak) if (m2l_tflops and dmma_peak) else None,
                              "algorithmic": "sum over instances 4kK+2k flop"},
             "e2e": e2e,
             "cpu_baseline": cpu,

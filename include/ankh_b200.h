@@ -191,6 +191,11 @@ int ankh_radial_fit_v1(double s_max, int* nterms, double* s_lim, double* p, doub
  * roofline denominator for the FP64-bound kernels (no reference counterpart). */
 double ankh_probe_fp64_tflops_v1(int iters);
 
+/* Measured FP64 tensor-core (DMMA) throughput in TFLOP/s for the MMA shape
+ * 0 = m8n8k4 (the M2L kernel's), 1 = m16n8k8, 2 = m16n8k16: the roofline
+ * denominator for k_m2l (no reference counterpart). */
+double ankh_probe_dmma_tflops_v1(int shape, int iters);
+
 /* Library version string. */
 const char* ankh_version_v1(void);
 

@@ -315,6 +315,14 @@ int ankh_radial_fit_v1(double s_max, int* nterms, double* s_lim, double* p, doub
   }
 }
 
+double ankh_probe_dmma_tflops_v1(int shape, int iters) {
+  try {
+    return ankh_b200::probe_dmma_tflops(shape, iters > 0 ? iters : 4096);
+  } catch (...) {
+    return 0.0;
+  }
+}
+
 double ankh_probe_fp64_tflops_v1(int iters) {
   try {
     return ankh_b200::probe_fp64_tflops(iters > 0 ? iters : 4096);

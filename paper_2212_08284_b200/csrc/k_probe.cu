@@ -25,7 +25,86 @@ __global__ void __launch_bounds__(256) k_dfma(double* out, int iters, double b, 
   for (int k = 0; k < 8; ++k) s += a[k];
   if (s == 12345.678) out[0] = s;  // keep the chains live
 }
+
+// FP64 tensor-core (DMMA) peak: SHAPE 0 = m8n8k4 (256 FMA / instruction),
+// 1 = m16n8k8 (1024), 2 = m16n8k16 (2048; sm_90+ shapes).  8 independent
+// accumulators per warp, register operands only.
+template <int SHAPE>
+__global__ void __launch_bounds__(256) k_dmma(double* out, int iters) {
+  double a[8], b[4], c[8][4];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1e-3 * (threadIdx.x + k);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) b[k] = 1e-3 * (threadIdx.x - k);
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[t][k] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (SHAPE == 0) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[t][0]), "+d"(c[t][1])
+                     : "d"(a[0]), "d"(b[0]));
+      } else if (SHAPE == 1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+            "{%8,%9}, {%0,%1,%2,%3};\n"
+            : "+d"(c[t][0]), "+d"(c[t][1]), "+d"(c[t][2]), "+d"(c[t][3])
+            : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+      } else {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+            "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+            : "+d"(c[t][0]), "+d"(c[t][1]), "+d"(c[t][2]), "+d"(c[t][3])
+            : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]),
+              "d"(a[7]), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+      }
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += c[t][k];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int SHAPE>
+double time_dmma(int iters, int sms, double* d) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 4;
+  k_dmma<SHAPE><<<blocks, 256>>>(d, iters / 4 + 1);
+  cudaEventRecord(e0);
+  k_dmma<SHAPE><<<blocks, 256>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double fma_per = SHAPE == 0 ? 256.0 : (SHAPE == 1 ? 1024.0 : 2048.0);
+  const double flops = 2.0 * fma_per * 8 * static_cast<double>(iters) * blocks * (256 / 32);
+  return ms > 0 ? flops / (ms * 1e-3) / 1e12 : 0.0;
+}
 }  // namespace
+
+double probe_dmma_tflops(int shape, int iters) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  cudaMalloc(&d, sizeof(double));
+  double r = 0.0;
+  if (shape == 0) r = time_dmma<0>(iters, sms, d);
+  else if (shape == 1) r = time_dmma<1>(iters / 4, sms, d);
+  else r = time_dmma<2>(iters / 8, sms, d);
+  cudaFree(d);
+  return r;
+}
 
 double probe_fp64_tflops(int iters) {
   int dev = 0, sms = 0;

@@ -129,6 +129,7 @@ void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos,
                           unsigned* sorted, std::size_t n, int n_leaves, double* part,
                           cudaStream_t st);
 double probe_fp64_tflops(int iters);
+double probe_dmma_tflops(int shape, int iters);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);
 
