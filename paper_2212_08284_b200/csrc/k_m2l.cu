@@ -6,7 +6,8 @@
 //     e += (L M_t) . (R M_s)
 // As a grouped GEMM: a CTA takes 64 instances of one operator, streams the
 // factor rows (padded to kp = 8*KP8) and the 2 x 64 gathered expansions
-// through shared memory in 16-node chunks (2-stage cp.async pipeline), and
+// through shared memory in kChunk-node chunks (kStages-deep cp.async
+// pipeline, one CTA barrier per chunk), and
 // each warp accumulates U = L [M_t...] and V = R [M_s...] for its 8*NTW
 // instances in DMMA fragments (rank rows = M dim, instances = N dim, nodes =
 // K dim; every factor fragment feeds NTW instance tiles).  The energy of the
@@ -18,8 +19,15 @@ namespace ankh_b200 {
 
 namespace {
 
-constexpr int kChunk = 16;              // node columns per pipeline stage
-constexpr int kStride = kChunk + 4;     // smem row stride (doubles): conflict-free fragments
+#ifndef ANKH_M2L_CHUNK
+#define ANKH_M2L_CHUNK 8
+#endif
+#ifndef ANKH_M2L_STAGES
+#define ANKH_M2L_STAGES 2
+#endif
+constexpr int kChunk = ANKH_M2L_CHUNK;   // node columns per pipeline stage
+constexpr int kStages = ANKH_M2L_STAGES; // cp.async pipeline depth
+constexpr int kStride = kChunk + 4;      // smem row stride (doubles): fragment loads in the minimal 2 wavefronts
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -105,14 +113,20 @@ __global__ void __launch_bounds__(kM2LTile * 4 / NTW) k_m2l(const double* __rest
 
   const int row = lane >> 2, col = lane & 3;
   const int nchunks = Kp / kChunk;
-  issue(0, sm);
-  cp_commit();
-  for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) issue((c + 1) * kChunk, sm + ((c + 1) & 1) * kStage);
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nchunks) issue(s * kChunk, sm + s * kStage);
     cp_commit();
-    cp_wait<1>();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    // chunk c has landed once at most kStages - 2 younger groups are pending;
+    // the barrier also retires every reader of the buffer refilled next
+    cp_wait<kStages - 2>();
     __syncthreads();
-    const double* st = sm + (c & 1) * kStage;
+    if (c + kStages - 1 < nchunks)
+      issue((c + kStages - 1) * kChunk, sm + ((c + kStages - 1) % kStages) * kStage);
+    cp_commit();
+    const double* st = sm + (c % kStages) * kStage;
     const double* sL = st;
     const double* sR = sL + kp * kStride;
     const double* bT = sR + kp * kStride + (warp * 8 * NTW + row) * kStride + col;
@@ -136,7 +150,6 @@ __global__ void __launch_bounds__(kM2LTile * 4 / NTW) k_m2l(const double* __rest
         }
       }
     }
-    __syncthreads();
   }
   double e = 0.0;
 #pragma unroll
@@ -162,7 +175,7 @@ void launch_class(const double* exp, const long long* level_off, const double* f
   // two instance tiles per warp for the common small-rank classes (register budget)
   constexpr int NTW = KP8 <= 5 ? 2 : 1;
   constexpr int kThr = kM2LTile * 4 / NTW;
-  const std::size_t smem = 2 * sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
+  const std::size_t smem = kStages * sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_m2l<KP8, NTW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
