@@ -20,6 +20,14 @@ namespace ankh_b200 {
 namespace {
 
 constexpr int kP2MThreads = 128;
+
+// hd[n] = H D^n (chebyshev.cpp:85-115) for n = 0..2 depends only on the
+// order L, so it lives in the constant bank (one slot per L = 2..10) and the
+// basis DFMAs read it as an immediate operand instead of loading it per
+// particle.  Written by upload_p2m_basis at plan build (identical bytes for
+// every plan of the same L).
+__host__ __device__ constexpr int hd_slot(int L) { return L <= 2 ? 0 : hd_slot(L - 1) + 3 * (L - 1) * (L - 1); }
+__constant__ double c_hd[hd_slot(11)];
 constexpr int kP2MWarps = kP2MThreads / 32;
 
 // Warp-per-leaf P2M.  Each lane first evaluates the 1-D bases of one particle
@@ -37,7 +45,7 @@ struct P2MWShape {
   static constexpr int L2 = L * L, K = L2 * L;
   static constexpr int QJ = (L2 + 31) / 32;       // (j,k) columns per lane
   static constexpr int PER = 12 * L;              // staged doubles per particle
-  static constexpr std::size_t smem_doubles = 3 * L2 + kP2MWarps * 32 * PER;
+  static constexpr std::size_t smem_doubles = kP2MWarps * 32 * PER;
 };
 
 template <int L>
@@ -50,12 +58,11 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
   using Sh = P2MWShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER, KS = exp_stride(K);
   extern __shared__ double sm[];
-  double* hd = sm;  // 3 L^2
+  const double* hd = c_hd + hd_slot(L);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // per particle: sx[3][L] | sy[3][L] | A0 A1 A2 B0 B1 C0 [L]
-  double* st = hd + 3 * L2 + warp * 32 * PER;
-  for (int w = threadIdx.x; w < 3 * L2; w += kP2MThreads) hd[w] = hd_g[w];
-  __syncthreads();
+  double* st = sm + warp * 32 * PER;
+  (void)hd_g;
   const int n = 1 << depth;
   // leaves are visited (and their expansions stored) in Morton order
   const unsigned m = m_begin + blockIdx.x * kP2MWarps + warp;
@@ -155,11 +162,12 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
       for (int q = 0; q < Sh::QJ; ++q) {
         const int j = jj[q], k = kk[q];
         const double y0 = s[3 * L + j], y1 = s[4 * L + j], y2 = s[5 * L + j];
-        const double w0 = y0 * s[6 * L + k] + y1 * s[7 * L + k] + y2 * s[8 * L + k];
-        const double w1 = y0 * s[9 * L + k] + y1 * s[10 * L + k];
+        const double w0 = fma(y0, s[6 * L + k], fma(y1, s[7 * L + k], y2 * s[8 * L + k]));
+        const double w1 = fma(y0, s[9 * L + k], y1 * s[10 * L + k]);
         const double w2 = y0 * s[11 * L + k];
 #pragma unroll
-        for (int i = 0; i < L; ++i) acc[q][i] += s[i] * w0 + s[L + i] * w1 + s[2 * L + i] * w2;
+        for (int i = 0; i < L; ++i)
+          acc[q][i] = fma(s[i], w0, fma(s[L + i], w1, fma(s[2 * L + i], w2, acc[q][i])));
       }
     }
   }
@@ -407,6 +415,17 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
   k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(
       part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end);
 }
+
+}  // namespace
+
+void upload_p2m_basis(int order, const double* hd, cudaStream_t st) {
+  if (order < 2 || order > 10) return;
+  const int L = order;
+  cudaMemcpyToSymbolAsync(c_hd, hd, sizeof(double) * 3 * L * L, sizeof(double) * hd_slot(L),
+                          cudaMemcpyHostToDevice, st);
+}
+
+namespace {
 
 template <int L>
 void m2m_order(const double* child, double* parent, int parent_level, const double* m2m,

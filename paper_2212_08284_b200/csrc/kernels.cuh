@@ -83,6 +83,8 @@ std::size_t sort_temp_bytes(std::size_t n, int n_leaves);
 void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
                  const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
                  const unsigned* counts, unsigned* offsets, int n_leaves, cudaStream_t st);
+/// hd[n] = H D^n, n = 0..2 (3 x L x L, host order) into the P2M constant bank.
+void upload_p2m_basis(int order, const double* hd, cudaStream_t st);
 void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
                 double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
                 unsigned m_begin, unsigned m_end, cudaStream_t st);

@@ -213,6 +213,8 @@ void Plan::allocate() {
   d_to_equi_ = static_cast<double*>(dalloc(to_equi.size() * sizeof(double)));
   ANKH_CUDA(cudaMemcpyAsync(d_hd_, hd_all.data(), hd_all.size() * sizeof(double),
                             cudaMemcpyHostToDevice, stream_));
+  upload_p2m_basis(L, hd_all.data(), stream_);  // constant-bank copy for the warp P2M
+  ANKH_CUDA(cudaGetLastError());
   ANKH_CUDA(cudaMemcpyAsync(d_m2m_, m2m.data(), m2m.size() * sizeof(double),
                             cudaMemcpyHostToDevice, stream_));
   ANKH_CUDA(cudaMemcpyAsync(d_to_equi_, to_equi.data(), to_equi.size() * sizeof(double),
