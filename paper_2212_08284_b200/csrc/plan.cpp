@@ -1,5 +1,6 @@
 // Host side of the B200 engine: geometry-only precompute and the launch
 // sequence of one energy evaluation (fmm.cpp:383-436 re-planned for HBM).
+#include <cstdio>
 #include "plan.hpp"
 
 #include <algorithm>
@@ -85,11 +86,27 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
   Kp = exp_stride(K);  // expansion row stride == factor column stride
   nax = 1 << depth;
   n_leaves = 1 << (3 * depth);
+  // ANKH_PLAN_TIMING=1: per-stage plan build times on stderr (diagnostics)
+  const bool verbose = std::getenv("ANKH_PLAN_TIMING") != nullptr;
+  auto stamp = [&](const char* what, std::chrono::steady_clock::time_point& t) {
+    if (!verbose) return;
+    ANKH_CUDA(cudaStreamSynchronize(stream_));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ankh plan] %-10s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  };
+  auto ts = std::chrono::steady_clock::now();
+  stamp("setup", ts);
   build_geometry();
+  stamp("geometry", ts);
   allocate();
+  stamp("allocate", ts);
   if (pending_code_ == 0 && n > 0 && !csr_only_) {
     build_m2l();
+    stamp("m2l", ts);
     if (periodic) build_periodic();
+    stamp("periodic", ts);
   }
   ANKH_CUDA(cudaStreamSynchronize(stream_));
   precompute_seconds =
@@ -232,11 +249,20 @@ void Plan::build_m2l() {
     Factors f;
   };
   const int threads = cfg.threads;
+  const bool verbose = std::getenv("ANKH_PLAN_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what) {
+    if (!verbose) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ankh plan]   m2l %-9s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   // canonical instances owned by this shard (shard.cpp, fmm.cpp:244-253)
   std::vector<OffsetInstances> groups =
       enumerate_m2l(depth, periodic, cfg.world > 1 ? cfg.rank : -1, cfg.world, threads);
   std::vector<OffsetWork> work(groups.size());
-  for (std::size_t i = 0; i < groups.size(); ++i) {
+  parallel_for(static_cast<int>(groups.size()), threads, [&](int i) {
     work[i].level = groups[i].level;
     work[i].o = groups[i].offset;
     work[i].inst.resize(groups[i].t.size());
@@ -248,8 +274,10 @@ void Plan::build_m2l() {
       work[i].inst[k] = make_uint2(to_morton(groups[i].t[k]), to_morton(groups[i].s[k]));
     std::sort(work[i].inst.begin(), work[i].inst.end(),
               [](const uint2& a, const uint2& b) { return a.x < b.x; });
-  }
+    groups[i] = OffsetInstances{};  // release as we go
+  });
   groups.clear();
+  stamp("instances");
   // factors: exact SVD path uses the signed-permutation symmetry of the block
   // (one SVD per class, SURVEY.md Decision 3); K > 150 replicates the
   // reference's seeded randomized path per offset.
@@ -288,46 +316,63 @@ void Plan::build_m2l() {
       w.f = compress_m2l(m2l_dense(L, rad, w.o, cfg.xi), K, cfg.svd_tol, m2l_seed(w.level, key));
     });
   }
-  // device operators: row blocks of <= 128 ranks, L then R, zero padded
+  stamp("factors");
+  // device operators: row blocks of <= 128 ranks, L then R, zero padded.
+  // Layout pass (serial, per operator) then a parallel fill.
   std::vector<M2LTile> tiles;
-  std::vector<uint2> inst;
   h_ops_.clear();
-  h_factors_.clear();
   double rank_sum = 0.0;
   far_flops = 0.0;
   m2l_instances = 0;
-  for (const auto& w : work) {
+  struct Block {
+    int work, r0, rows;
+  };
+  std::vector<Block> blocks;
+  std::vector<std::size_t> inst_begin(work.size());
+  std::size_t n_inst = 0, n_fac = 0;
+  for (std::size_t wi = 0; wi < work.size(); ++wi) {
+    const OffsetWork& w = work[wi];
     const int rank = w.f.rank;
     OpInfo info{w.level, offset_key(w.o), rank, static_cast<int>(h_ops_.size()), 0};
-    const int inst_begin = static_cast<int>(inst.size());
-    inst.insert(inst.end(), w.inst.begin(), w.inst.end());
+    inst_begin[wi] = n_inst;
     for (int r0 = 0; r0 < rank; r0 += 8 * kMaxKp8) {
       const int rows = std::min(8 * kMaxKp8, rank - r0);
       const int kp = ceil_div(rows, 8) * 8;
       M2LOp op;
-      op.factor_off = static_cast<long long>(h_factors_.size());
+      op.factor_off = static_cast<long long>(n_fac);
       op.kp = kp;
       op.rank = rows;
-      std::vector<double> blockL(static_cast<std::size_t>(kp) * Kp, 0.0), blockR(blockL.size(), 0.0);
-      for (int r = 0; r < rows; ++r)
-        for (int k = 0; k < K; ++k) {
-          blockL[static_cast<std::size_t>(r) * Kp + k] = w.f.lmat[static_cast<std::size_t>(r0 + r) * K + k];
-          blockR[static_cast<std::size_t>(r) * Kp + k] = w.f.rmat[static_cast<std::size_t>(r0 + r) * K + k];
-        }
-      h_factors_.insert(h_factors_.end(), blockL.begin(), blockL.end());
-      h_factors_.insert(h_factors_.end(), blockR.begin(), blockR.end());
+      n_fac += 2 * static_cast<std::size_t>(kp) * Kp;
       const int op_index = static_cast<int>(h_ops_.size());
       h_ops_.push_back(op);
+      blocks.push_back({static_cast<int>(wi), r0, rows});
       ++info.n_blocks;
       for (int b = 0; b < static_cast<int>(w.inst.size()); b += kM2LTile)
-        tiles.push_back({op_index, w.level, inst_begin + b,
+        tiles.push_back({op_index, w.level, static_cast<int>(n_inst) + b,
                          std::min(kM2LTile, static_cast<int>(w.inst.size()) - b)});
     }
     op_info_[{w.level, info.key}] = info;
     rank_sum += rank;
-    m2l_instances += w.inst.size();
+    n_inst += w.inst.size();
     far_flops += static_cast<double>(w.inst.size()) * (4.0 * rank * K + 2.0 * rank);
   }
+  m2l_instances = n_inst;
+  h_factors_.assign(n_fac, 0.0);
+  std::vector<uint2> inst(n_inst);
+  parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
+    std::copy(work[wi].inst.begin(), work[wi].inst.end(), inst.begin() + inst_begin[wi]);
+  });
+  parallel_for(static_cast<int>(blocks.size()), threads, [&](int bi) {
+    const Block& b = blocks[bi];
+    const Factors& f = work[b.work].f;
+    double* dl = h_factors_.data() + h_ops_[bi].factor_off;
+    double* dr = dl + static_cast<std::size_t>(h_ops_[bi].kp) * Kp;
+    for (int r = 0; r < b.rows; ++r)
+      for (int k = 0; k < K; ++k) {
+        dl[static_cast<std::size_t>(r) * Kp + k] = f.lmat[static_cast<std::size_t>(b.r0 + r) * K + k];
+        dr[static_cast<std::size_t>(r) * Kp + k] = f.rmat[static_cast<std::size_t>(b.r0 + r) * K + k];
+      }
+  });
   m2l_operators = work.size();
   m2l_rank_mean = work.empty() ? 0.0 : rank_sum / work.size();
   n_tiles_ = static_cast<int>(tiles.size());
@@ -342,6 +387,7 @@ void Plan::build_m2l() {
       if (h_ops_[tiles[t].op].kp / 8 == c) ids.push_back(t);
     class_range_[c] = {begin, static_cast<int>(ids.size()) - begin};
   }
+  stamp("pack");
   d_factors_ = static_cast<double*>(dalloc(h_factors_.size() * sizeof(double)));
   d_ops_ = static_cast<M2LOp*>(dalloc(h_ops_.size() * sizeof(M2LOp)));
   d_tiles_ = static_cast<M2LTile*>(dalloc(tiles.size() * sizeof(M2LTile)));
@@ -361,6 +407,7 @@ void Plan::build_m2l() {
                               cudaMemcpyHostToDevice, stream_));
   ANKH_CUDA(cudaMemsetAsync(d_far_part_, 0, std::max<std::size_t>(tiles.size(), 1) * sizeof(double), stream_));
   ANKH_CUDA(cudaStreamSynchronize(stream_));
+  stamp("upload");
 }
 
 // build_periodic_operator (fmm.cpp:333-377): generator on the GPU, its r2c
