@@ -118,9 +118,11 @@ __device__ __forceinline__ void write_record(const double* __restrict__ pos,
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     const double* __restrict__ pos, const double* __restrict__ src,
     const unsigned* __restrict__ offsets, unsigned* __restrict__ unsorted,
-    unsigned* __restrict__ scratch, unsigned* __restrict__ sorted, double* __restrict__ part) {
+    unsigned* __restrict__ scratch, unsigned* __restrict__ sorted,
+    const unsigned char* __restrict__ need, double* __restrict__ part) {
   __shared__ unsigned a[kLeafSmem], b[kLeafSmem];
   const unsigned leaf = blockIdx.x;
+  if (need && !need[leaf]) return;  // another shard's leaf
   const unsigned base = offsets[leaf];
   const int c = static_cast<int>(offsets[leaf + 1] - base);
   if (c == 0) return;
@@ -216,15 +218,15 @@ void launch_bin(const double* pos, const double* src, std::size_t n, double box_
 void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
                           const unsigned* keys, const unsigned* slots, const unsigned* counts,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
-                          unsigned* sorted, std::size_t n, int n_leaves, double* part,
-                          cudaStream_t st) {
+                          unsigned* sorted, std::size_t n, int n_leaves,
+                          const unsigned char* need, double* part, cudaStream_t st) {
   std::size_t bytes = temp_bytes;
   cub::DeviceScan::ExclusiveSum(temp, bytes, counts, offsets, n_leaves + 1, st);
   if (n == 0) return;
   k_scatter<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, slots, offsets, n,
                                                                     unsorted);
   k_leaf_gather<<<static_cast<unsigned>(n_leaves), kLeafThreads, 0, st>>>(
-      pos, src, offsets, unsorted, scratch, sorted, part);
+      pos, src, offsets, unsorted, scratch, sorted, need, part);
 }
 
 std::size_t sort_temp_bytes(std::size_t n, int n_leaves) {

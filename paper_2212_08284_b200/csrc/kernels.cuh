@@ -124,12 +124,13 @@ void launch_finalize(const double* near_partial, int n_near, const unsigned long
 void launch_init_result(DevResult* res, cudaStream_t st);
 /// Counting sort into leaves (after launch_bin with counts): scan -> offsets,
 /// scatter, per-leaf ascending order (sorted = the leaf CSR's index array) and
-/// the gather of 112-B records.  unsorted / scratch: N uints each.
+/// the gather of 112-B records.  unsorted / scratch: N uints each; need
+/// (optional, per lex leaf): only those leaves are sorted and gathered.
 void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
                           const unsigned* keys, const unsigned* slots, const unsigned* counts,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
-                          unsigned* sorted, std::size_t n, int n_leaves, double* part,
-                          cudaStream_t st);
+                          unsigned* sorted, std::size_t n, int n_leaves,
+                          const unsigned char* need, double* part, cudaStream_t st);
 double probe_fp64_tflops(int iters);
 double probe_dmma_tflops(int shape, int iters);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,

@@ -190,6 +190,39 @@ void Plan::allocate() {
   d_idx2_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
   d_counts_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
   d_off_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
+  // A shard gathers particle records only for the leaves it reads: its P2P
+  // targets, their 13 half-shell neighbours (k_p2p's stencil, periodic wrap)
+  // and its P2M rows.  (One shard: every leaf, no mask.)
+  if (cfg.world > 1 && !csr_only_) {
+    std::vector<unsigned char> need(n_leaves, 0);
+    auto lex_of = [&](unsigned m) {
+      return (morton_compact3(m >> 2) * nax + morton_compact3(m >> 1)) * nax + morton_compact3(m);
+    };
+    for (int m = p2m_begin_; m < p2m_end_; ++m) need[lex_of(static_cast<unsigned>(m))] = 1;
+    for (int m = leaf_begin_; m < leaf_end_; ++m) {
+      const unsigned lf = lex_of(static_cast<unsigned>(m));
+      const int a[3] = {static_cast<int>(lf) / (nax * nax), (static_cast<int>(lf) / nax) % nax,
+                        static_cast<int>(lf) % nax};
+      need[lf] = 1;
+      for (int d = 0; d < 13; ++d) {  // the 13 lex-positive directions of k_p2p
+        const int dx = d < 4 ? 0 : 1;
+        const int dy = d == 0 ? 0 : (d < 4 ? 1 : (d - 4) / 3 - 1);
+        const int dz = d == 0 ? 1 : (d < 4 ? d - 2 : (d - 4) % 3 - 1);
+        int b[3] = {a[0] + dx, a[1] + dy, a[2] + dz};
+        bool ok = true;
+        for (int q = 0; q < 3; ++q) {
+          if (b[q] < 0 || b[q] >= nax) {
+            if (!periodic) ok = false;
+            b[q] = (b[q] + nax) % nax;
+          }
+        }
+        if (ok) need[(static_cast<unsigned>(b[0]) * nax + b[1]) * nax + b[2]] = 1;
+      }
+    }
+    d_need_ = static_cast<unsigned char*>(dalloc(need.size()));
+    ANKH_CUDA(cudaMemcpyAsync(d_need_, need.data(), need.size(), cudaMemcpyHostToDevice, stream_));
+    ANKH_CUDA(cudaStreamSynchronize(stream_));
+  }
   temp_bytes_ = sort_temp_bytes(nn, n_leaves);
   d_temp_ = dalloc(temp_bytes_);
   d_part_ = static_cast<double*>(dalloc(nn * kRec * sizeof(double)));
@@ -460,7 +493,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     // counting sort by leaf: d_idx_ holds the arrival slots, d_keys2_ the
     // scattered indices, d_idx2_ the leaf CSR's ascending indices
     launch_bucket_gather(d_temp_, temp_bytes_, d_pos, d_src, d_keys_, d_idx_, d_counts_, d_off_,
-                         d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_part_, st);
+                         d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, d_part_, st);
     launches += 2;
   }
   if (csr_only_) {

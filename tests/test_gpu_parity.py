@@ -308,16 +308,16 @@ def test_config4_series(cuda):
         assert abs(seen[0] - float(want["energies"]["e_total"])) <= 1e-10 * abs(float(want["energies"]["e_total"]))
 
 
-@pytest.mark.parametrize("world", [2, 3, 4, 8])
-def test_inprocess_shards_sum_to_single_gpu(cuda, world):
+@pytest.mark.parametrize("world, p", [(2, 15), (3, 15), (4, 15), (8, 15), (4, 0)])
+def test_inprocess_shards_sum_to_single_gpu(cuda, world, p):
     """Multi-GPU decomposition, exercised as `world` shards on one GPU: each
-    shard's P2M rows (world | 8^E) are exchanged with the same in-place layout
-    the NCCL all-gather uses, and the shards' partial energies sum to the
-    single-shard result."""
+    shard gathers only the leaves it reads, its P2M rows (world | 8^E) are
+    exchanged with the same in-place layout the NCCL all-gather uses, and the
+    shards' partial energies sum to the single-shard result (periodic and open)."""
     torch = cuda
     pos, src, rb, cfg = inputs.make_config(1)  # depth 3: 512 leaves
     n = pos.shape[0]
-    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4, p=p)
     dp, ds = torch.from_numpy(pos).cuda(), torch.from_numpy(src).cuda()
     whole = ankh.Plan(n, rb, ec).energy_device(dp, ds)
     plans = [ankh.Plan(n, rb, ec, rank=r, world=world, phase_timing=False) for r in range(world)]
