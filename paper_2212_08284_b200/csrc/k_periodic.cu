@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(kPerThreads) k_periodic_eval(const double* __r
   if (tid == 0) out[0] = 0.5 * red[0] / static_cast<double>(eb * eb * eb);
 }
 
-constexpr int kFinThreads = 1024;
+constexpr int kFinThreads = 256;
+constexpr int kFinBlocks = 64;  // first level: contiguous slices, fixed order
 
 __device__ double block_sum(double v, double* red) {
   red[threadIdx.x] = v;
@@ -181,40 +182,67 @@ __device__ double block_sum(double v, double* red) {
   return r;
 }
 
-__global__ void __launch_bounds__(kFinThreads) k_finalize(
-    const double* __restrict__ near_partial, int n_near,
-    const unsigned long long* __restrict__ pair_count, int n_count,
-    const double* __restrict__ far_partial,
-    int n_far, const double* __restrict__ self_partial, int n_self, double self_scale,
-    const double* __restrict__ periodic, int use_periodic, int include_self, DevResult* res) {
-  __shared__ double red[kFinThreads];
-  __shared__ unsigned long long redu[kFinThreads];
-  double a = 0.0;
-  for (int i = threadIdx.x; i < n_near; i += kFinThreads) a += near_partial[i];
-  const double e_near = block_sum(a, red);
-  a = 0.0;
-  for (int i = threadIdx.x; i < n_far; i += kFinThreads) a += far_partial[i];
-  const double e_far = block_sum(a, red);
-  a = 0.0;
-  if (include_self)
-    for (int i = threadIdx.x; i < n_self; i += kFinThreads) a += self_partial[i];
-  const double self_acc = block_sum(a, red);
-  unsigned long long c = 0;
-  if (pair_count)
-    for (int i = threadIdx.x; i < n_count; i += kFinThreads) c += pair_count[i];
-  redu[threadIdx.x] = c;
+__device__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* red) {
+  red[threadIdx.x] = v;
   __syncthreads();
   for (int s = kFinThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) redu[threadIdx.x] += redu[threadIdx.x + s];
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
     __syncthreads();
   }
+  const unsigned long long r = red[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ T slice_sum(const T* __restrict__ a, int n) {
+  const int lo = static_cast<int>(static_cast<long long>(n) * blockIdx.x / kFinBlocks);
+  const int hi = static_cast<int>(static_cast<long long>(n) * (blockIdx.x + 1) / kFinBlocks);
+  T acc = 0;
+  if (a)
+    for (int i = lo + threadIdx.x; i < hi; i += kFinThreads) acc += a[i];
+  return acc;
+}
+
+// Level 1: block b sums slice b of every partial array (fixed order per slice).
+__global__ void __launch_bounds__(kFinThreads) k_finalize_slices(
+    const double* __restrict__ near_partial, int n_near,
+    const unsigned long long* __restrict__ pair_count, int n_count,
+    const double* __restrict__ far_partial, int n_far, const double* __restrict__ self_partial,
+    int n_self, double* __restrict__ slices, unsigned long long* __restrict__ slice_pairs) {
+  __shared__ double red[kFinThreads];
+  __shared__ unsigned long long redu[kFinThreads];
+  const double a = block_sum(slice_sum(near_partial, n_near), red);
+  const double b = block_sum(slice_sum(far_partial, n_far), red);
+  const double c = block_sum(slice_sum(self_partial, n_self), red);
+  const unsigned long long p = block_sum_u64(slice_sum(pair_count, n_count), redu);
   if (threadIdx.x == 0) {
-    res->red[kENear] = e_near;
-    res->red[kEFar] = e_far;
-    res->red[kESelf] = self_scale * self_acc;  // -xi/sqrt(pi) * acc (kernel.cpp:212)
-    res->red[kEPeriodic] = use_periodic ? periodic[0] : 0.0;
-    res->red[kNearPairs] = static_cast<double>(redu[0]);
+    slices[3 * blockIdx.x + 0] = a;
+    slices[3 * blockIdx.x + 1] = b;
+    slices[3 * blockIdx.x + 2] = c;
+    slice_pairs[blockIdx.x] = p;
   }
+}
+
+// Level 2: one warp-sized pass over the kFinBlocks slices, in slice order.
+__global__ void k_finalize(const double* __restrict__ slices,
+                           const unsigned long long* __restrict__ slice_pairs, double self_scale,
+                           const double* __restrict__ periodic, int use_periodic,
+                           int include_self, DevResult* res) {
+  if (threadIdx.x != 0) return;
+  double e_near = 0.0, e_far = 0.0, self_acc = 0.0;
+  unsigned long long pairs = 0;
+  for (int b = 0; b < kFinBlocks; ++b) {
+    e_near += slices[3 * b];
+    e_far += slices[3 * b + 1];
+    self_acc += slices[3 * b + 2];
+    pairs += slice_pairs[b];
+  }
+  res->red[kENear] = e_near;
+  res->red[kEFar] = e_far;
+  res->red[kESelf] = include_self ? self_scale * self_acc : 0.0;  // -xi/sqrt(pi) acc (kernel.cpp:212)
+  res->red[kEPeriodic] = use_periodic ? periodic[0] : 0.0;
+  res->red[kNearPairs] = static_cast<double>(pairs);
 }
 
 }  // namespace
@@ -241,11 +269,17 @@ void launch_periodic_eval(const double* root, const double* to_equi, const doubl
 void launch_finalize(const double* near_partial, int n_near, const unsigned long long* pair_count,
                      int n_count, const double* far_partial, int n_far, const double* self_partial,
                      int n_self, double self_scale, const double* periodic, int use_periodic,
-                     int include_self, DevResult* res, cudaStream_t st) {
-  k_finalize<<<1, kFinThreads, 0, st>>>(near_partial, n_near, pair_count, n_count, far_partial,
-                                        n_far,
-                                        self_partial, n_self, self_scale, periodic, use_periodic,
-                                        include_self, res);
+                     int include_self, double* scratch, DevResult* res, cudaStream_t st) {
+  // scratch: kFinBlocks x 3 doubles + kFinBlocks uint64 (finalize_scratch_bytes)
+  unsigned long long* slice_pairs = reinterpret_cast<unsigned long long*>(scratch + 3 * kFinBlocks);
+  k_finalize_slices<<<kFinBlocks, kFinThreads, 0, st>>>(near_partial, n_near, pair_count, n_count,
+                                                        far_partial, n_far,
+                                                        include_self ? self_partial : nullptr,
+                                                        n_self, scratch, slice_pairs);
+  k_finalize<<<1, 32, 0, st>>>(scratch, slice_pairs, self_scale, periodic, use_periodic,
+                               include_self, res);
 }
+
+std::size_t finalize_scratch_bytes() { return kFinBlocks * (3 * sizeof(double) + sizeof(unsigned long long)); }
 
 }  // namespace ankh_b200

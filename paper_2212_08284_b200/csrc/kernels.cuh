@@ -120,7 +120,8 @@ void launch_periodic_eval(const double* root, const double* to_equi, const doubl
 void launch_finalize(const double* near_partial, int n_near, const unsigned long long* pair_count,
                      int n_count, const double* far_partial, int n_far, const double* self_partial,
                      int n_self, double self_scale, const double* periodic, int use_periodic,
-                     int include_self, DevResult* res, cudaStream_t st);
+                     int include_self, double* scratch, DevResult* res, cudaStream_t st);
+std::size_t finalize_scratch_bytes();
 void launch_init_result(DevResult* res, cudaStream_t st);
 /// Counting sort into leaves (after launch_bin with counts): scan -> offsets,
 /// scatter, per-leaf ascending order (sorted = the leaf CSR's index array) and

@@ -190,6 +190,7 @@ void Plan::allocate() {
   d_idx2_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
   d_counts_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
   d_off_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
+  d_fin_scratch_ = static_cast<double*>(dalloc(finalize_scratch_bytes()));
   // A shard gathers particle records only for the leaves it reads: its P2P
   // targets, their 13 half-shell neighbours (k_p2p's stencil, periodic wrap)
   // and its P2M rows.  (One shard: every leaf, no mask.)
@@ -562,8 +563,8 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   launch_finalize(d_near_part_, n_near_parts, d_pair_count_, leaf_end_ - leaf_begin_, d_far_part_,
                   n_tiles_,
                   d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
-                  include_self_ ? 1 : 0, d_res_, st);
-  ++launches;
+                  include_self_ ? 1 : 0, d_fin_scratch_, d_res_, st);
+  launches += 2;
   // shards: one all-reduce of the energy / counter / flag vector (the path's
   // only exchange besides the leaf all-gather)
   if (coll_) coll_->allreduce_sum(d_res_->red, kRedShared, st);

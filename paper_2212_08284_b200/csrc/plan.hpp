@@ -126,6 +126,7 @@ class Plan {
   unsigned *d_keys_ = nullptr, *d_keys2_ = nullptr, *d_idx_ = nullptr, *d_idx2_ = nullptr;
   unsigned *d_counts_ = nullptr, *d_off_ = nullptr;
   unsigned char* d_need_ = nullptr;  // shard: leaves whose records are gathered
+  double* d_fin_scratch_ = nullptr;   // two-level final reduction
   void* d_temp_ = nullptr;
   std::size_t temp_bytes_ = 0;
   double* d_part_ = nullptr;
