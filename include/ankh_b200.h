@@ -166,8 +166,9 @@ int ankh_device_copy_v1(void* dst, const void* src, size_t bytes, void* stream, 
 /* ---- spatial sharding (host only; no device needed) ----
  * Shards own contiguous Morton ranges of leaves; a level-l cell belongs to the
  * shard owning its first descendant leaf.  P2P work is owned by the target
- * leaf, M2L work by the target cell of the reference's canonical instance
- * (fmm.cpp:246-250), so each unordered pair / instance is counted once. */
+ * leaf; a canonical M2L instance (t, s) (fmm.cpp:246-250) by the owner of t or
+ * of s, chosen by a hash of the pair (balanced load), so each unordered pair /
+ * instance is counted once. */
 int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* morton_begin,
                              int64_t* morton_end);
 int ankh_shard_cell_owner_v1(int level, uint32_t lex_cell, int depth, int world);

@@ -28,6 +28,17 @@ void shard_leaf_range(int depth, int rank, int world, std::int64_t* begin, std::
   *end = nl * (rank + 1) / world;
 }
 
+int shard_m2l_owner(int level, std::uint32_t t, std::uint32_t s, int depth, int world) {
+  if (world <= 1) return 0;
+  // the owner of t or of s, by a hash of the pair: every cell has the same
+  // number of interaction partners, so each shard gets half of the instances
+  // of its targets and half of those of its sources -- balanced, whereas the
+  // target alone favours low cell indices under the t < s canonical rule
+  // (12 % excess on 8 shards at config 3)
+  const std::uint32_t h = t * 0x9E3779B1u ^ (s + 0x7F4A7C15u) * 0x85EBCA77u;
+  return shard_cell_owner(level, ((h >> 15) & 1u) ? s : t, depth, world);
+}
+
 int shard_cell_owner(int level, std::uint32_t cell, int depth, int world) {
   if (world <= 1) return 0;
   const int n = 1 << level;
@@ -69,7 +80,7 @@ void enumerate_offset(OffsetInstances& w, bool periodic, int depth, int rank, in
         const std::uint32_t s = static_cast<std::uint32_t>((in[0] * nl + in[1]) * nl + in[2]);
         const bool lexpos = img[0] != 0 ? img[0] > 0 : (img[1] != 0 ? img[1] > 0 : img[2] > 0);
         if (!(t < s || (t == s && lexpos))) continue;
-        if (rank >= 0 && shard_cell_owner(w.level, t, depth, world) != rank) continue;
+        if (rank >= 0 && shard_m2l_owner(w.level, t, s, depth, world) != rank) continue;
         w.t.push_back(t);
         w.s.push_back(s);
       }

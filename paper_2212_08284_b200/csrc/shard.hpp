@@ -3,9 +3,9 @@
 // Shards own contiguous Morton ranges of leaves.  A level-l
 // cell belongs to the shard that owns its first descendant leaf, so for
 // world | 8 every shard owns whole level-1 subtrees.  P2P work is owned by
-// the target leaf, M2L work by the target cell t of the reference's canonical
-// instance (t, s, image) (fmm.cpp:246-250); every unordered pair / instance is
-// therefore counted by exactly one shard.
+// the target leaf; a canonical M2L instance (t, s, image) (fmm.cpp:246-250)
+// by the owner of t or of s, picked by a hash of (t, s) for balance; every
+// unordered pair / instance is therefore counted by exactly one shard.
 #pragma once
 
 #include <array>
@@ -23,11 +23,15 @@ void shard_leaf_range(int depth, int rank, int world, std::int64_t* begin, std::
 /// Owner shard of lex cell `cell` at `level` in a depth-`depth` tree.
 int shard_cell_owner(int level, std::uint32_t cell, int depth, int world);
 
+/// Shard that evaluates the canonical M2L instance (t, s) at `level`.
+int shard_m2l_owner(int level, std::uint32_t t, std::uint32_t s, int depth, int world);
+
 /// Canonical M2L instances of one (level, offset): Lambda(t) offsets are
 /// s - t in [-2-c, 3-c] per axis with c = t & 1 (octree.cpp:79-87), wrapped
 /// with split_extended (octree.cpp:11-14) when periodic, kept iff
-/// t < s or (t == s and image lex-positive) (fmm.cpp:246-250).  Only targets
-/// owned by `rank` are returned (rank < 0: all), as (t, s) pairs in lex t order.
+/// t < s or (t == s and image lex-positive) (fmm.cpp:246-250).  Only instances
+/// owned by `rank` (shard_m2l_owner) are returned (rank < 0: all), as (t, s)
+/// pairs in lex t order.
 struct OffsetInstances {
   int level = 0;
   std::array<int, 3> offset{};
