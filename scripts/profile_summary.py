@@ -53,7 +53,7 @@ def to_unit(v, unit, want):
 
 # launched by bench.py outside the evaluation step: the FP64 peak probe and
 # the plan's geometry-only precompute
-NOT_STEP = ("k_dfma", "k_periodic_gen")
+NOT_STEP = ("k_dfma", "k_dmma", "k_periodic_gen")
 
 
 def launch_share(path):
