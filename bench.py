@@ -222,10 +222,22 @@ def run_reference(args, world, rank):
         "value_including_precompute": 1.0 / t_tot,
         "reference_wall_times_last": wt,
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
+                         "cpu": cpu_model(),
                          "sample": f"full ankh::fmm_energy call on config {args.config} per step; value excludes the per-call precompute (M2L SVDs with the shim's Jacobi SVD), incl. precompute {1.0 / t_tot:.4g} evals/s"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def cpu_baseline_sample(args, pos, src, rb, L):
@@ -240,6 +252,7 @@ def cpu_baseline_sample(args, pos, src, rb, L):
     wt = rep["wall_times"]
     t_eval = wt["total"] - wt["precompute"]
     return {"value": 1.0 / t_eval, "unit": "evals/s", "cores": threads, "kind": "reference",
+            "cpu": cpu_model(),
             "sample": f"one full ankh::fmm_energy call on the same {pos.shape[0]}-atom system "
                       f"(oracle/_ref); evaluation phases only, its per-call precompute "
                       f"({wt['precompute']:.2f} s) excluded; incl. precompute {1.0 / wt['total']:.4g} evals/s",
