@@ -5,9 +5,10 @@ oracle/_ref/libankh_ref.so (oracle/Makefile), are run on seeded inputs from
 paper_2212_08284_b200.inputs.  Inputs are not stored; their sha256 is, so a
 generator drift is detected instead of silently comparing different systems.
 
-    python tests/golden/make_golden.py [--big]
+    python tests/golden/make_golden.py [--big | --high | --config 3|4]
 
---big adds configs 1 and 2 (L = 3..6), which take minutes on the CPU.
+--big adds configs 1 and 2 (L = 3..6), which take minutes on the CPU;
+--high writes the order 8-10 random systems (golden_high.json).
 """
 from __future__ import annotations
 
@@ -38,6 +39,15 @@ SMALL_CASES = [
     ("rand_q_L2_E1_open", 64, 3.0, 6, False, dict(order_cheb=2, order_equi=2, depth=1, p=0)),
     ("rand_mp_L5_E3_open", 1500, 8.0, 7, True, dict(order_cheb=5, order_equi=5, depth=3, p=0)),
     ("rand_mp_L4_E2_xi0.3", 400, 4.0, 8, True, dict(order_cheb=4, order_equi=4, depth=2, p=3, xi=0.3)),
+]
+
+
+# orders above 7: block-per-leaf P2M, large M2L rank classes, randomized SVD
+HIGH_CASES = [
+    ("rand_mp_L8_E2_p15", 600, 5.0, 21, True, dict(order_cheb=8, order_equi=8, depth=2, p=15)),
+    ("rand_mp_L9_E2_p15", 500, 5.0, 22, True, dict(order_cheb=9, order_equi=9, depth=2, p=15)),
+    ("rand_mp_L10_E1_p2", 300, 4.0, 23, True, dict(order_cheb=10, order_equi=10, depth=1, p=2)),
+    ("rand_mp_L8_E2_open", 600, 5.0, 24, True, dict(order_cheb=8, order_equi=8, depth=2, p=0)),
 ]
 
 
@@ -92,6 +102,7 @@ def kats():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--high", action="store_true", help="orders 8-10 only -> golden_high.json")
     ap.add_argument("--config", type=int, default=None,
                     help="only BASELINE config 3 or 4 (config 4: evaluation 0 of the rescale series)")
     args = ap.parse_args()
@@ -118,7 +129,10 @@ def main():
         return
     doc = {"generator": "tests/golden/make_golden.py", "reference": "oracle/_ref/libankh_ref.so",
            "kats": kats(), "systems": []}
-    for name, n, rb, seed, mp, kw in SMALL_CASES:
+    if args.high:
+        doc = {"generator": "tests/golden/make_golden.py --high",
+               "reference": "oracle/_ref/libankh_ref.so", "systems": []}
+    for name, n, rb, seed, mp, kw in (HIGH_CASES if args.high else SMALL_CASES):
         pos, src = inputs.random_system(n, rb, seed=seed, multipoles=mp)
         rep = R.fmm_energy(pos, src, rb, threads=threads, **kw)
         depth = kw["depth"]
@@ -129,7 +143,7 @@ def main():
             "leaf_csr_sha256": hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest(),
         })
         print(name, doc["systems"][-1]["energies"]["e_total"], flush=True)
-    cfgs = [(0, 4)]
+    cfgs = [] if args.high else [(0, 4)]
     if args.big:
         cfgs += [(1, 4), (2, 3), (2, 4), (2, 5), (2, 6)]
     for ci, L in cfgs:
@@ -145,7 +159,7 @@ def main():
             "ref_wall_times": rep["wall_times"], "ref_threads": threads,
         })
         print(c.name, L, doc["systems"][-1]["energies"]["e_total"], rep["wall_times"]["total"], flush=True)
-    name = "golden_big.json" if args.big else "golden.json"
+    name = "golden_high.json" if args.high else ("golden_big.json" if args.big else "golden.json")
     with open(os.path.join(HERE, name), "w") as f:
         json.dump(doc, f, indent=1)
     print("wrote", name)

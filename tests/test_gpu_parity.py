@@ -59,6 +59,7 @@ def _system(case):
 GOLDEN = _load("golden.json")["systems"]
 GOLDEN_BIG = _load("golden_big.json")["systems"] if os.path.exists(
     os.path.join(HERE, "golden", "golden_big.json")) else []
+GOLDEN_HIGH = _load("golden_high.json")["systems"]
 
 
 @pytest.mark.parametrize("case", GOLDEN, ids=[c["name"] for c in GOLDEN])
@@ -68,6 +69,18 @@ def test_golden_small(cuda, case):
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, case["box_radius"]), ankh.EwaldConfig(**kw))
     # random test systems have strongly cancelling components; water boxes do not
     check_energies(rep, case["energies"], scale_total=case["kind"] != "random")
+    offs, idx = ankh.build_tree_csr(pos, case["box_radius"], rep.depth)
+    assert hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest() == case["leaf_csr_sha256"]
+
+
+@pytest.mark.parametrize("case", GOLDEN_HIGH, ids=[c["name"] for c in GOLDEN_HIGH])
+def test_golden_high_orders(cuda, case):
+    """Orders 8-10 (block-per-leaf P2M, M2L rank classes up to 128, the
+    reference's seeded randomized SVD for K > 150) against the reference."""
+    pos, src = _system(case)
+    rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, case["box_radius"]),
+                          ankh.EwaldConfig(**case["config"]))
+    check_energies(rep, case["energies"], scale_total=False)
     offs, idx = ankh.build_tree_csr(pos, case["box_radius"], rep.depth)
     assert hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest() == case["leaf_csr_sha256"]
 
