@@ -260,7 +260,12 @@ namespace {
 
 // One-sided Jacobi on a column-major m x n matrix w (m >= n).  On return the
 // columns of w are U*sigma and v (n x n, column-major) holds V.
-void jacobi_colmajor(std::vector<double>& w, int m, int n, std::vector<double>& v) {
+// skip_rel > 0: pairs of columns whose norms are both below skip_rel times
+// the largest column norm are not rotated -- they only mix directions far
+// below a truncation cutoff (their span, the kept columns and the rank
+// decision are unaffected).
+void jacobi_colmajor(std::vector<double>& w, int m, int n, std::vector<double>& v,
+                     double skip_rel) {
   v.assign(static_cast<std::size_t>(n) * n, 0.0);
   for (int i = 0; i < n; ++i) v[static_cast<std::size_t>(i) * n + i] = 1.0;
   const double eps = 2.220446049250313e-16;
@@ -273,8 +278,15 @@ void jacobi_colmajor(std::vector<double>& w, int m, int n, std::vector<double>& 
   }
   for (int sweep = 0; sweep < 100; ++sweep) {
     bool rotated = false;
+    double skip2 = 0.0;  // squared norms
+    if (skip_rel > 0.0) {
+      double mx = 0.0;
+      for (int j = 0; j < n; ++j) mx = std::max(mx, norms[j]);
+      skip2 = mx * skip_rel * skip_rel;
+    }
     for (int p = 0; p < n - 1; ++p) {
       for (int q = p + 1; q < n; ++q) {
+        if (norms[p] < skip2 && norms[q] < skip2) continue;
         double* wp = w.data() + static_cast<std::size_t>(p) * m;
         double* wq = w.data() + static_cast<std::size_t>(q) * m;
         double gamma = 0.0;
@@ -313,7 +325,7 @@ void jacobi_colmajor(std::vector<double>& w, int m, int n, std::vector<double>& 
 }  // namespace
 
 void svd_thin(const std::vector<double>& a, int m, int n, std::vector<double>& u,
-              std::vector<double>& sigma, std::vector<double>& v) {
+              std::vector<double>& sigma, std::vector<double>& v, double skip_rel) {
   const bool tall = m >= n;
   const int mm = tall ? m : n, nn = tall ? n : m;
   // column-major working copy of (tall ? a : a^T)
@@ -327,7 +339,7 @@ void svd_thin(const std::vector<double>& a, int m, int n, std::vector<double>& u
         w[static_cast<std::size_t>(i) * mm + j] = x;
     }
   std::vector<double> vv;
-  jacobi_colmajor(w, mm, nn, vv);
+  jacobi_colmajor(w, mm, nn, vv, skip_rel);
   std::vector<double> sig(nn);
   for (int j = 0; j < nn; ++j) {
     const double* wj = w.data() + static_cast<std::size_t>(j) * mm;
@@ -459,7 +471,9 @@ Factors compress_m2l(const std::vector<double>& c, int k_full, double svd_tol, s
   Factors f;
   if (k_full <= 150) {
     std::vector<double> u, s, v;
-    svd_thin(c, k_full, k_full, u, s, v);
+    // rank = 1 + #{sigma_i > sigma_0 tol}: directions 1e-3 below the cutoff
+    // need not be resolved among themselves
+    svd_thin(c, k_full, k_full, u, s, v, svd_tol * 1e-3);
     finish(f, u, k_full, s, v, k_full, k_full, svd_tol);
     return f;
   }

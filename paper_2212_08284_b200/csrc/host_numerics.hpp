@@ -83,9 +83,11 @@ Symmetry symmetry_of(const std::array<int, 3>& offset);
 std::vector<int> node_permutation(const Symmetry& s, int order);
 
 /// One-sided Jacobi thin SVD of a (m x n, row-major).  U m x p, V n x p
-/// (row-major), sigma descending, p = min(m, n).
+/// (row-major), sigma descending, p = min(m, n).  skip_rel > 0: directions
+/// with singular values below skip_rel * sigma_0 are not resolved among
+/// themselves (for truncations at a much larger cutoff).
 void svd_thin(const std::vector<double>& a, int m, int n, std::vector<double>& u,
-              std::vector<double>& sigma, std::vector<double>& v);
+              std::vector<double>& sigma, std::vector<double>& v, double skip_rel = 0.0);
 
 /// Real-to-complex DFT of a row-major real array of dims d0 x d1 x d2 in the
 /// FFTW half-complex layout (d2/2+1 on the last axis), unnormalised.  Returns
