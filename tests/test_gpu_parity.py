@@ -132,6 +132,17 @@ def test_large_leaves_chunking(cuda, ref):
     check_energies(rep, want, scale_total=False)
 
 
+def test_own_leaf_larger_than_a_chunk(cuda, ref):
+    """~1,000 particles per leaf: the own leaf spans staged chunks and target
+    passes, so P2P takes its general path (halved target, self skip) instead of
+    the circular half-walk."""
+    pos, src = inputs.random_system(8000, 10.0, seed=12, multipoles=True)
+    kw = dict(order_cheb=3, order_equi=3, depth=1, p=2)
+    want = ref.fmm_energy(pos, src, 10.0, threads=os.cpu_count(), **kw)
+    rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 10.0), ankh.EwaldConfig(**kw))
+    check_energies(rep, want, scale_total=False)
+
+
 def test_leaf_csr_bit_exact(cuda, ref):
     for seed, n, rb, depth in [(0, 5000, 4.0, 3), (1, 777, 1.0, 2), (2, 100, 2.5, 5)]:
         pos, _ = inputs.random_system(n, rb, seed=seed)
