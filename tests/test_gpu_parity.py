@@ -132,6 +132,19 @@ def test_large_leaves_chunking(cuda, ref):
     check_energies(rep, want, scale_total=False)
 
 
+def test_pipelined_p2p_variant_matches(cuda, monkeypatch):
+    """The bulk-copy ring P2P kernel (ANKH_P2P_PIPE=1, an A/B alternative)
+    gives the default kernel's energies to round-off."""
+    pos, src, rb, cfg = inputs.make_config(1)
+    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    want = ankh.Plan(pos.shape[0], rb, ec).energy(pos, src)
+    monkeypatch.setenv("ANKH_P2P_PIPE", "1")
+    got = ankh.Plan(pos.shape[0], rb, ec).energy(pos, src)
+    assert got.near_pairs == want.near_pairs
+    assert abs(got.e_near - want.e_near) <= 1e-12 * abs(want.e_near)
+    assert abs(got.e_total - want.e_total) <= 1e-12 * abs(want.e_total)
+
+
 def test_own_leaf_larger_than_a_chunk(cuda, ref):
     """~1,000 particles per leaf: the own leaf spans staged chunks and target
     passes, so P2P takes its general path (halved target, self skip) instead of
