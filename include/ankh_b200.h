@@ -179,6 +179,18 @@ int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, ui
                                 uint32_t* t, uint32_t* s, int32_t* offset, size_t capacity,
                                 size_t* count);
 
+/* Direct screened lattice sum -- the exact quantity the FMM approximates,
+ * for validation (SPEC's `direct` method; the reference has no direct engine):
+ *   *e_lattice = 1/2 sum_{|I|inf <= p} sum_{i,j: i != j or I != 0}
+ *                pair_interaction(x_i, x_j + 2 r_B I)          (kernel.cpp:157-204)
+ *   *e_self    = self_energy (kernel.cpp:206-213);  e_total = sum of the two.
+ * Cost n^2 (2p+1)^3 pair evaluations on the GPU; refused above
+ * max_pair_evaluations (<= 0: 1e12) with ANKH_RUNTIME_ERROR. */
+int ankh_direct_energy_v1(size_t n, const double* positions, const double* sources,
+                          double box_radius, double xi, int p, int device,
+                          double max_pair_evaluations, double* e_lattice, double* e_self,
+                          char* err, size_t errlen);
+
 /* Near-field radial polynomials the plan uses for a given s_max = xi^2 d_max^2
  * (d_max = the largest near-pair distance, 2 sqrt(3) leaf sides): coefficients
  * (14 each, in s = xi^2 r^2) of P(s) = erf(sqrt s)/sqrt s and

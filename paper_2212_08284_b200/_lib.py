@@ -38,6 +38,7 @@ EXPORTS = [
     "ankh_plan_attach_nccl_v1",
     "ankh_radial_fit_v1",
     "ankh_probe_dmma_tflops_v1",
+    "ankh_direct_energy_v1",
 ]
 
 
@@ -93,6 +94,8 @@ def lib() -> ctypes.CDLL:
         L.ankh_device_copy_v1.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, cp, c_size_t]
         L.ankh_nccl_unique_id_v1.argtypes = [ctypes.c_char_p, cp, c_size_t]
         L.ankh_plan_attach_nccl_v1.argtypes = [c_void_p, ctypes.c_char_p, cp, c_size_t]
+        L.ankh_direct_energy_v1.argtypes = [c_size_t, D, D, c_double, c_double, c_int, c_int,
+                                            c_double, D, D, cp, c_size_t]
         L.ankh_probe_dmma_tflops_v1.argtypes = [c_int, c_int]
         L.ankh_probe_dmma_tflops_v1.restype = c_double
         L.ankh_radial_fit_v1.argtypes = [c_double, I, D, D, D, D]

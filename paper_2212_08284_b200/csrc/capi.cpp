@@ -1,5 +1,7 @@
 // C-ABI of libankh_b200.so (declared in include/ankh_b200.h).
 #include <chrono>
+#include <string>
+#include <cmath>
 #include <cstring>
 #include <vector>
 #include <list>
@@ -298,6 +300,81 @@ int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, ui
   } catch (...) {
     return ANKH_RUNTIME_ERROR;
   }
+}
+
+int ankh_direct_energy_v1(size_t n, const double* positions, const double* sources,
+                          double box_radius, double xi, int p, int device,
+                          double max_pair_evaluations, double* e_lattice, double* e_self,
+                          char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!e_lattice || !e_self) throw AnkhError(ANKH_INVALID_ARGUMENT, "null output");
+    if (n > 0 && (!positions || !sources)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+    if (!(xi > 0.0) || !std::isfinite(xi)) throw AnkhError(ANKH_INVALID_ARGUMENT, "direct: xi must be > 0");
+    if (p < 0) throw AnkhError(ANKH_INVALID_ARGUMENT, "direct: p must be >= 0");
+    if (!(box_radius > 0.0) || !std::isfinite(box_radius))
+      throw AnkhError(ANKH_INVALID_ARGUMENT, "direct: box_radius must be positive and finite");
+    const double side = 2.0 * p + 1.0;
+    const double evals = static_cast<double>(n) * static_cast<double>(n) * side * side * side;
+    const double budget = max_pair_evaluations > 0.0 ? max_pair_evaluations : 1e12;
+    if (evals > budget)
+      throw AnkhError(ANKH_RUNTIME_ERROR, "direct: n^2 (2p+1)^3 = " + std::to_string(evals) +
+                                              " pair evaluations exceed the budget " +
+                                              std::to_string(budget));
+    if (n >= (1u << 30)) throw AnkhError(ANKH_RUNTIME_ERROR, "direct: too many particles");
+    if (device >= 0) ANKH_CUDA(cudaSetDevice(device));
+    // self energy (kernel.cpp:206-213), host, fixed order
+    const double c_mu = 2.0 * xi * xi / 3.0, c_th = 8.0 * xi * xi * xi * xi / 5.0;
+    double acc = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      const double* s = sources + 10 * i;
+      const double mu2 = s[1] * s[1] + s[2] * s[2] + s[3] * s[3];
+      const double th2 = s[4] * s[4] + s[7] * s[7] + s[9] * s[9] +
+                         2.0 * (s[5] * s[5] + s[6] * s[6] + s[8] * s[8]);
+      acc += s[0] * s[0] + c_mu * mu2 + c_th * th2;
+    }
+    *e_self = -xi / std::sqrt(3.14159265358979323846) * acc;
+    *e_lattice = 0.0;
+    if (n == 0) return;
+    const int ni = static_cast<int>(n);
+    const int np = ankh_b200::direct_partials(ni, p);
+    double *d_pos = nullptr, *d_src = nullptr, *d_rec = nullptr, *d_part = nullptr;
+    cudaStream_t st = nullptr;
+    auto cleanup = [&] {
+      if (st) cudaStreamSynchronize(st), cudaStreamDestroy(st);
+      cudaFree(d_pos);
+      cudaFree(d_src);
+      cudaFree(d_rec);
+      cudaFree(d_part);
+    };
+    try {
+      ANKH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      ANKH_CUDA(cudaMalloc(&d_pos, n * 3 * sizeof(double)));
+      ANKH_CUDA(cudaMalloc(&d_src, n * 10 * sizeof(double)));
+      ANKH_CUDA(cudaMalloc(&d_rec, n * ankh_b200::kRec * sizeof(double)));
+      ANKH_CUDA(cudaMalloc(&d_part, np * sizeof(double)));
+      ANKH_CUDA(cudaMemcpyAsync(d_pos, positions, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+      ANKH_CUDA(cudaMemcpyAsync(d_src, sources, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
+      // radial polynomials valid to s = 0.25 with libm beyond (any distance)
+      const ankh_b200::RadialFit f = ankh_b200::fit_radial(1e9);
+      ankh_b200::P2PRadial rad{};
+      rad.nterms = f.nterms;
+      rad.s_lim = f.s_lim;
+      std::memcpy(rad.p, f.p, sizeof rad.p);
+      std::memcpy(rad.g, f.g, sizeof rad.g);
+      ankh_b200::launch_direct(d_pos, d_src, ni, box_radius, xi, p, rad, d_rec, d_part, st);
+      ANKH_CUDA(cudaGetLastError());
+      std::vector<double> part(np);
+      ANKH_CUDA(cudaMemcpyAsync(part.data(), d_part, np * sizeof(double), cudaMemcpyDeviceToHost, st));
+      ANKH_CUDA(cudaStreamSynchronize(st));
+      double e = 0.0;
+      for (double v : part) e += v;
+      *e_lattice = e;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
 }
 
 int ankh_radial_fit_v1(double s_max, int* nterms, double* s_lim, double* p, double* g,

@@ -133,6 +133,11 @@ void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos,
                           unsigned* sorted, std::size_t n, int n_leaves,
                           const unsigned char* need, double* part, cudaStream_t st);
 double probe_fp64_tflops(int iters);
+/// Direct screened lattice sum (k_direct.cu): per-CTA halves of the pair sums
+/// into partial[direct_partials(n, p)]; rec: n x kRec scratch.
+int direct_partials(int n, int p);
+void launch_direct(const double* pos, const double* src, int n, double box_radius, double xi,
+                   int p, const P2PRadial& rad, double* rec, double* partial, cudaStream_t st);
 double probe_dmma_tflops(int shape, int iters);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);

@@ -88,7 +88,7 @@ def test_unavailable_method_is_config_error(tmp_path, capsys):
     assert cli.main(["gen", "--n", "10", "--box-radius", "3", "-o", f]) == 0
     code, out = run(["compare", "-i", f, "--runs", "fmm", "fft:order_cheb=8"], capsys)
     assert code == cli.EXIT_CONFIG and "fft" in out.err
-    code, out = run(["energy", "-i", f, "--method", "direct"], capsys)
+    code, out = run(["energy", "-i", f, "--method", "ewald"], capsys)
     assert code == cli.EXIT_CONFIG
 
 
@@ -97,6 +97,15 @@ def test_budget_guard(tmp_path, capsys):
     assert cli.main(["gen", "--n", "50", "--box-radius", "3", "-o", f]) == 0
     code, out = run(["energy", "-i", f, "--max-atoms", "10"], capsys)
     assert code == cli.EXIT_BUDGET
+
+
+def test_direct_budget_guard(tmp_path, capsys):
+    """The direct lattice sum refuses n^2 (2p+1)^3 above the budget (exit 4)
+    before any device work."""
+    f = str(tmp_path / "s.txt")
+    assert cli.main(["gen", "--n", "2000", "--box-radius", "9", "-o", f]) == 0
+    code, out = run(["energy", "-i", f, "--method", "direct", "--max-pairs", "1e9"], capsys)
+    assert code == cli.EXIT_BUDGET and "budget" in out.err
 
 
 def test_config_error_exit_code(tmp_path, capsys):

@@ -389,3 +389,48 @@ def test_nccl_collective_single_rank(cuda):
     for _ in range(3):  # plain launch, graph capture, graph replay
         rep = plan.energy_device(dp, ds)
         assert rep.e_total == ref_rep.e_total
+
+
+def test_direct_lattice_sum_matches_numpy(cuda):
+    """ankh_direct_energy_v1 against an explicit numpy image sum built from the
+    oracle's pair_interaction (kernel.cpp:157-204) on a tiny system."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
+    import ankh_oracle as O  # checker only
+
+    rb, p, xi = 2.0, 2, 0.3
+    pos, src = inputs.random_system(7, rb, seed=31, multipoles=True)
+    n = pos.shape[0]
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    ii, jj = ii.ravel(), jj.ravel()
+    total = 0.0
+    for ix in range(-p, p + 1):
+        for iy in range(-p, p + 1):
+            for iz in range(-p, p + 1):
+                keep = (ii != jj) | (ix != 0) | (iy != 0) | (iz != 0)
+                a, b = ii[keep], jj[keep]
+                shift = 2.0 * rb * np.array([ix, iy, iz], float)
+                total += 0.5 * float(O.pair_interaction(pos[a], src[a], pos[b] + shift, src[b], xi).sum())
+    rep = ankh.direct_energy(ankh.ParticleSystem(pos, src, rb), xi=xi, p=p)
+    assert abs(rep.e_near - total) <= 1e-12 * abs(total), (rep.e_near, total)
+    assert abs(rep.e_self - O.self_energy(src, xi)) <= 1e-13 * abs(rep.e_self)
+
+
+def test_fmm_converges_to_direct_lattice_sum(cuda):
+    """Physical accuracy of the whole FMM (near field, M2L, periodic far images,
+    self energy) against the direct screened lattice sum it approximates, on
+    SPEC's 648-atom water stand-in at p = 15: the error falls geometrically
+    with the order (SURVEY.md Appendix B measured 1.2e-4 / 6.7e-6 / 7.2e-7 at
+    L = 4 / 6 / 8 on 96 random particles)."""
+    from paper_2212_08284_b200 import cli
+
+    pos, src, rb = cli.gen_system("lattice-jittered", 648, 9.3215, 5, "full")
+    system = ankh.ParticleSystem(pos, src, rb)
+    exact = ankh.direct_energy(system, xi=0.01, p=15).e_total
+    errs = []
+    for L in (4, 6, 8):
+        rep = ankh.fmm_energy(system, ankh.EwaldConfig(order_cheb=L, order_equi=L, depth=2))
+        errs.append(abs(rep.e_total - exact) / abs(exact))
+    assert errs[0] > errs[1] > errs[2], errs
+    assert errs[2] < 1e-6, errs
