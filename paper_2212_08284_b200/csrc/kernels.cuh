@@ -21,7 +21,6 @@ constexpr int kRec = 14;          // doubles per particle record (112 B: x y z q
 constexpr int kM2LTile = 64;      // instances per M2L CTA
 constexpr int kM2LChunk = 32;     // node columns per staged chunk
 constexpr int kMaxKp8 = 16;       // ranks up to 128
-constexpr int kP2PThreads = 256;
 
 /// Morton decode: every 3rd bit (x in bit 3k+2, y in 3k+1, z in 3k), as
 /// shard.cpp's morton3 encodes.  Expansions at every level are stored in

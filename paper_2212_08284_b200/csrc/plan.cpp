@@ -167,7 +167,6 @@ void Plan::build_geometry() {
   // so a leaf's own + 13 neighbour leaves (~14 x mean occupancy) fit in one
   // pass for almost every leaf.  ANKH_P2P_CAP overrides (tuning).
   const double per_leaf = static_cast<double>(n) / n_leaves;
-  p2p_tpb_ = 256;
   p2p_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.3 / 32.0)) * 32;
   p2p_cap_ = std::max(256, std::min(p2p_cap_, 960));
   // pipelined P2P (ANKH_P2P_PIPE=1): a 2-slot ring of p2p_pipe_cap_ staged sources
@@ -239,7 +238,7 @@ void Plan::allocate() {
   n_self_blocks_ = static_cast<int>((nn + 255) / 256);
   d_self_part_ = static_cast<double*>(dalloc(n_self_blocks_ * sizeof(double)));
   d_near_part_ = static_cast<double*>(dalloc(std::max(leaf_end_ - leaf_begin_, 1) *
-                                             std::max(p2p_pipe_warps(p2p_tpb_), 1) * sizeof(double)));
+                                             std::max(p2p_pipe_warps(256), 1) * sizeof(double)));
   d_pair_count_ = static_cast<unsigned long long*>(
       dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(unsigned long long)));
   d_per_ = static_cast<double*>(dalloc(sizeof(double)));

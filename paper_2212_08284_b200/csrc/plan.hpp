@@ -154,7 +154,6 @@ class Plan {
   DevResult* d_res_ = nullptr;
   DevResult* h_res_ = nullptr;
   P2PRadial radial_{};  // near-field radial polynomials (fit_radial)
-  int p2p_tpb_ = 256;
   int p2p_cap_ = 512;
   int p2p_pipe_ = 0;
   int p2p_pipe_cap_ = 320;
