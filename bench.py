@@ -5,12 +5,12 @@
 
 A step is ONE full energy evaluation of BASELINE config 3 (1,029,000-atom
 water box, full multipoles, L = 5, depth 5, periodic p = 15): validation,
-leaf binning + stable sort, P2M, M2M, M2L, P2P, periodic far images, self
+leaf binning + counting sort, P2M, M2M, M2L, P2P, periodic far images, self
 energy and the final reduction.  The geometry-only plan (M2L factors and
 periodic spectrum, which depend on box radius and configuration but not on
 the particles) is built once before timing, as the plan API intends; its
 build time is reported separately.  Inputs (positions + moments, 107 MB)
-plus the sorted particle records (132 MB) exceed the 126 MB L2, so no extra
+plus the sorted particle records (115 MB) exceed the 126 MB L2, so no extra
 L2 flush is done between steps (config.l2 says so).
 
 value      : evaluations/s of the whole job (max-over-ranks device time),
@@ -21,7 +21,8 @@ e2e        : the same metric through the drop-in C-ABI call
 roofline   : the dominant kernel (P2P), nominal 229 flop per multipole pair
               x pairs / its CUDA-event duration, against the
              FP64 DFMA peak measured in-process (MEASURED_PEAKS.json has no
-             FP64 entry).
+             FP64 entry); roofline_m2l against the measured DMMA peak;
+             phase_rooflines: every phase against its own roofline.
 cpu_baseline / --impl reference : the reference itself (oracle/_ref, the
              unmodified reference sources built against oracle/shim), one full
              ankh::fmm_energy call per step on all host cores.
@@ -411,7 +412,7 @@ def main():
                                    f"L={L}, depth {plan.info()['depth']}, periodic p=15, xi=0.01",
                        "atoms": n, "order_cheb": L, "depth": plan.info()["depth"],
                        "parallelism": f"spatial Morton-range shards x{world}",
-                       "l2": "working set (inputs 107 MB + sorted records 132 MB + factors) exceeds the 126 MB L2; no extra flush",
+                       "l2": "working set (inputs 107 MB + sorted records 115 MB + factors 100 MB) exceeds the 126 MB L2; no extra flush",
                        "plan_cached": True, "plan_build_s": plan_s},
             "atoms_per_s": n * value,
             "e_total": e_total,
