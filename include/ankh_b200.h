@@ -108,6 +108,17 @@ int ankh_plan_energy_device_v1(ankh_plan_v1* plan, const double* d_positions,
                                const double* d_sources, void* stream, ankh_report_v1* out,
                                char* err, size_t errlen);
 
+/* Repeated evaluation with fixed positions (the config-4 pattern: moments
+ * change, positions and box do not).  set_positions copies the HOST positions,
+ * validates them and bins / sorts them once; energy_sources then copies only
+ * the HOST moments (n x 10), validates them and runs the evaluation -- no
+ * position copy, no re-binning.  Any other evaluation of the plan supersedes
+ * the bound positions (ANKH_RUNTIME_ERROR until set again). */
+int ankh_plan_set_positions_v1(ankh_plan_v1* plan, const double* positions, char* err,
+                               size_t errlen);
+int ankh_plan_energy_sources_v1(ankh_plan_v1* plan, const double* sources, ankh_report_v1* out,
+                                char* err, size_t errlen);
+
 /* Enqueue an evaluation without synchronising; results are fetched with
  * ankh_plan_result_v1.  Used for device-timed loops and CUDA-graph capture. */
 int ankh_plan_enqueue_v1(ankh_plan_v1* plan, const double* d_positions, const double* d_sources,

@@ -39,6 +39,8 @@ EXPORTS = [
     "ankh_radial_fit_v1",
     "ankh_probe_dmma_tflops_v1",
     "ankh_direct_energy_v1",
+    "ankh_plan_set_positions_v1",
+    "ankh_plan_energy_sources_v1",
 ]
 
 
@@ -96,6 +98,8 @@ def lib() -> ctypes.CDLL:
         L.ankh_plan_attach_nccl_v1.argtypes = [c_void_p, ctypes.c_char_p, cp, c_size_t]
         L.ankh_direct_energy_v1.argtypes = [c_size_t, D, D, c_double, c_double, c_int, c_int,
                                             c_double, D, D, cp, c_size_t]
+        L.ankh_plan_set_positions_v1.argtypes = [c_void_p, D, cp, c_size_t]
+        L.ankh_plan_energy_sources_v1.argtypes = [c_void_p, D, c_void_p, cp, c_size_t]
         L.ankh_probe_dmma_tflops_v1.argtypes = [c_int, c_int]
         L.ankh_probe_dmma_tflops_v1.restype = c_double
         L.ankh_radial_fit_v1.argtypes = [c_double, I, D, D, D, D]

@@ -333,6 +333,25 @@ class Plan:
         _check(lib().ankh_plan_energy_v1(self._h, _ptr(pos), _ptr(src), ctypes.byref(rep), err, 512), err)
         return EnergyReport._from_c(rep)
 
+    def set_positions(self, positions) -> None:
+        """Bind host positions (copied, validated, binned and sorted once) for
+        repeated ``energy_sources`` calls with new moments."""
+        pos = _as_host(positions, 3)
+        if pos.shape[0] != self.n:
+            raise InvalidArgument("fmm_energy: invalid system: positions and sources must have equal length")
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_set_positions_v1(self._h, _ptr(pos), err, 512), err)
+
+    def energy_sources(self, sources) -> EnergyReport:
+        """Evaluate new host moments (n x 10) at the bound positions."""
+        src = _as_host(sources, 10)
+        if src.shape[0] != self.n:
+            raise InvalidArgument("fmm_energy: invalid system: positions and sources must have equal length")
+        rep = _Report()
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_energy_sources_v1(self._h, _ptr(src), ctypes.byref(rep), err, 512), err)
+        return EnergyReport._from_c(rep)
+
     def energy_device(self, positions, sources, stream: int = 0) -> EnergyReport:
         """Device tensors (torch CUDA float64, contiguous N x 3 / N x 10)."""
         self._check_dev(positions, sources)

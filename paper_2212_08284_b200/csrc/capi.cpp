@@ -138,6 +138,25 @@ int ankh_plan_energy_v1(ankh_plan_v1* plan, const double* positions, const doubl
   });
 }
 
+int ankh_plan_set_positions_v1(ankh_plan_v1* plan, const double* positions, char* err,
+                               size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");
+    if (plan->plan->n > 0 && !positions) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+    plan->plan->set_positions(positions, nullptr);
+  });
+}
+
+int ankh_plan_energy_sources_v1(ankh_plan_v1* plan, const double* sources, ankh_report_v1* out,
+                                char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
+    if (plan->plan->n > 0 && !sources) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+    plan->plan->enqueue_sources(sources, nullptr);
+    plan->plan->result(out);
+  });
+}
+
 int ankh_plan_energy_device_v1(ankh_plan_v1* plan, const double* d_positions,
                                const double* d_sources, void* stream, ankh_report_v1* out,
                                char* err, size_t errlen) {

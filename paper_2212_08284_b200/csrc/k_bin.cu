@@ -37,12 +37,14 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
   bool mp = false;
   if (i < n) {
     const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
-    double s[10];
-#pragma unroll
-    for (int k = 0; k < 10; ++k) s[k] = src[10 * i + k];
+    double s[10] = {};
     bool finite = isfinite(x) && isfinite(y) && isfinite(z);
+    if (src) {  // src == nullptr: positions only (ankh_plan_set_positions_v1)
 #pragma unroll
-    for (int k = 0; k < 10; ++k) finite = finite && isfinite(s[k]);
+      for (int k = 0; k < 10; ++k) s[k] = src[10 * i + k];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) finite = finite && isfinite(s[k]);
+    }
     unsigned key = 0;
     if (!finite) {
       atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
@@ -163,8 +165,61 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     __syncthreads();
     order = sorted + base;
   }
+  if (!part) return;  // sort only (positions bound ahead of the moments)
   for (int p = threadIdx.x; p < c; p += kLeafThreads)
     write_record(pos, src, order[p], part + static_cast<std::size_t>(base + p) * kRec);
+}
+
+// Records in leaf order from an existing sorted index (the moments of a
+// plan whose positions were bound by ankh_plan_set_positions_v1).
+__global__ void __launch_bounds__(256) k_gather_sorted(const double* __restrict__ pos,
+                                                       const double* __restrict__ src,
+                                                       const unsigned* __restrict__ sorted,
+                                                       std::size_t n, double* __restrict__ part) {
+  const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (j >= n) return;
+  write_record(pos, src, sorted[j], part + j * kRec);
+}
+
+// The moment half of validate_system (types.cpp:16-63) and the self-energy
+// partials for the bound-positions path (same block layout as k_bin).
+__global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ src, std::size_t n,
+                                                   double c_mu, double c_th,
+                                                   double* __restrict__ self_partial,
+                                                   DevResult* res) {
+  __shared__ double red[8];
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  double acc = 0.0;
+  bool mp = false;
+  if (i < n) {
+    double s[10];
+    bool finite = true;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      s[k] = src[10 * i + k];
+      finite = finite && isfinite(s[k]);
+    }
+    if (!finite) {
+      atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
+    } else {
+      const double mu2 = s[1] * s[1] + s[2] * s[2] + s[3] * s[3];
+      const double th2 = s[4] * s[4] + s[7] * s[7] + s[9] * s[9] +
+                         2.0 * (s[5] * s[5] + s[6] * s[6] + s[8] * s[8]);
+      acc = s[0] * s[0] + c_mu * mu2 + c_th * th2;
+      mp = (s[1] != 0.0 || s[2] != 0.0 || s[3] != 0.0 || th2 != 0.0);
+    }
+  }
+  if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    self_partial[blockIdx.x] = t;
+  }
 }
 
 __global__ void k_init_result(DevResult* res) {
@@ -227,6 +282,16 @@ void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos,
                                                                     unsorted);
   k_leaf_gather<<<static_cast<unsigned>(n_leaves), kLeafThreads, 0, st>>>(
       pos, src, offsets, unsorted, scratch, sorted, need, part);
+}
+
+void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
+                       std::size_t n, double xi, double* self_partial, DevResult* res,
+                       double* part, cudaStream_t st) {
+  if (n == 0) return;
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  k_src_check<<<blocks, 256, 0, st>>>(src, n, 2.0 * xi * xi / 3.0, 8.0 * xi * xi * xi * xi / 5.0,
+                                      self_partial, res);
+  k_gather_sorted<<<blocks, 256, 0, st>>>(pos, src, sorted, n, part);
 }
 
 std::size_t sort_temp_bytes(std::size_t n, int n_leaves) {

@@ -121,11 +121,18 @@ void launch_finalize(const double* near_partial, int n_near, const unsigned long
                      int n_self, double self_scale, const double* periodic, int use_periodic,
                      int include_self, double* scratch, DevResult* res, cudaStream_t st);
 std::size_t finalize_scratch_bytes();
+/// Bound-positions path: moment validation + self-energy partials (k_bin's
+/// block layout) and the records gathered through an existing sorted index.
+void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
+                       std::size_t n, double xi, double* self_partial, DevResult* res,
+                       double* part, cudaStream_t st);
 void launch_init_result(DevResult* res, cudaStream_t st);
 /// Counting sort into leaves (after launch_bin with counts): scan -> offsets,
 /// scatter, per-leaf ascending order (sorted = the leaf CSR's index array) and
 /// the gather of 112-B records.  unsorted / scratch: N uints each; need
-/// (optional, per lex leaf): only those leaves are sorted and gathered.
+/// (optional, per lex leaf): only those leaves are sorted and gathered;
+/// part == nullptr: sort only.  launch_bin with src == nullptr bins and
+/// validates positions only.
 void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
                           const unsigned* keys, const unsigned* slots, const unsigned* counts,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,

@@ -117,6 +117,7 @@ Plan::~Plan() {
   if (stream_) cudaStreamSynchronize(stream_);
   if (last_stream_) cudaStreamSynchronize(last_stream_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_src_exec_) cudaGraphExecDestroy(graph_src_exec_);
   for (void* p : allocs_) cudaFree(p);
   if (h_res_) cudaFreeHost(h_res_);
   for (auto& e : ev_)
@@ -243,6 +244,7 @@ void Plan::allocate() {
       dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(unsigned long long)));
   d_per_ = static_cast<double*>(dalloc(sizeof(double)));
   d_res_ = static_cast<DevResult*>(dalloc(sizeof(DevResult)));
+  d_res_pos_ = static_cast<DevResult*>(dalloc(sizeof(DevResult)));
   ANKH_CUDA(cudaMallocHost(&h_res_, sizeof(DevResult)));
   // small operators (chebyshev.cpp:85-108, fmm.cpp:213-219, 421-424)
   const auto hd = diff_operator(L);
@@ -478,10 +480,16 @@ void Plan::validate_only(const double* d_pos, const double* d_src, cudaStream_t 
 }
 
 void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st, int mode) {
-  const bool timing = cfg.phase_timing != 0 && mode == 0;
+  const bool timing = cfg.phase_timing != 0 && (mode == 0 || mode == 3);
   std::uint32_t launches = 0;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[0], st));
-  if (mode != 2) {
+  if (mode == 3) {
+    // positions validated and sorted by set_positions: start from their flags,
+    // validate the moments, gather the records through the sorted index
+    ANKH_CUDA(cudaMemcpyAsync(d_res_, d_res_pos_, sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
+    launch_src_gather(d_pos, d_src, d_idx2_, n, cfg.xi, d_self_part_, d_res_, d_part_, st);
+    launches += 2;
+  } else if (mode != 2) {
     ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
     launch_init_result(d_res_, st);
     ++launches;
@@ -505,7 +513,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   // run concurrently on two streams (P2M/M2M are latency-bound and hide under
   // P2P).  With phase timing -- or when the caller drives the two halves
   // itself (mode 1/2, in-process shard exchange) -- they run back to back.
-  const bool serial = timing || mode != 0;
+  const bool serial = timing || mode == 1 || mode == 2;
   const bool do_periodic = periodic && include_self_;
   cudaStream_t far = st;
   if (!serial) {
@@ -525,7 +533,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     return;
   }
   // ... the leaf level completed by the shard exchange, then M2M (fmm.cpp:203-236)
-  if (mode == 0) exchange_leaves(far);
+  if (mode == 0 || mode == 3) exchange_leaves(far);
   for (int l = depth - 1; l >= 0; --l) {
     launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, far);
     ++launches;
@@ -586,6 +594,7 @@ void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
   if (!st) st = stream_;
   last_stream_ = st;
   evaluated_ = true;
+  bound_ = false;  // a full evaluation re-bins: bound positions are superseded
   if (n == 0) return;
   if (pending_code_ != 0) {
     validate_only(d_pos, d_src, st);
@@ -641,6 +650,69 @@ void Plan::enqueue_host(const double* h_pos, const double* h_src, cudaStream_t s
     ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
   }
   enqueue(d_pos_, d_src_, st);
+}
+
+void Plan::set_positions(const double* h_pos, cudaStream_t st) {
+  if (!st) st = stream_;
+  bound_ = false;
+  if (n == 0) {
+    bound_ = true;
+    return;
+  }
+  ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (pending_code_ == 0 && !csr_only_) {
+    ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
+    launch_init_result(d_res_pos_, st);
+    const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
+    launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_,
+               d_self_part_, d_res_pos_, st);
+    launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_,
+                         d_off_, d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
+  }
+  ANKH_CUDA(cudaGetLastError());
+  bound_ = true;
+}
+
+void Plan::enqueue_sources(const double* h_src, cudaStream_t st) {
+  if (!bound_) throw AnkhError(ANKH_RUNTIME_ERROR, "plan positions are not set (ankh_plan_set_positions_v1)");
+  if (!st) st = stream_;
+  last_stream_ = st;
+  evaluated_ = true;
+  if (n == 0) return;
+  ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (pending_code_ != 0) {
+    validate_only(d_pos_, d_src_, st);
+    return;
+  }
+  if (shard_upward_ && !coll_)
+    throw AnkhError(ANKH_RUNTIME_ERROR,
+                    "sharded plan (world > 1) needs ankh_plan_attach_nccl_v1");
+  if (cfg.phase_timing) {
+    launch_all(d_pos_, d_src_, st, 3);
+    return;
+  }
+  // same CUDA-graph policy as enqueue: plain launches once, then capture and replay
+  if (!graph_src_exec_ && graph_src_warm_ > 0) {
+    cudaGraph_t g = nullptr;
+    ANKH_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      launch_all(d_pos_, d_src_, st, 3);
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    ANKH_CUDA(cudaStreamEndCapture(st, &g));
+    const cudaError_t e = cudaGraphInstantiate(&graph_src_exec_, g, 0);
+    cudaGraphDestroy(g);
+    ANKH_CUDA(e);
+  }
+  if (graph_src_exec_) {
+    ANKH_CUDA(cudaGraphLaunch(graph_src_exec_, st));
+    return;
+  }
+  ++graph_src_warm_;
+  launch_all(d_pos_, d_src_, st, 3);
 }
 
 void Plan::result(ankh_report_v1* out) {
@@ -722,6 +794,7 @@ void Plan::expansions(double* out, std::size_t count) {
 void Plan::enqueue_phase(int phase, const double* d_pos, const double* d_src, cudaStream_t st) {
   if (!st) st = stream_;
   last_stream_ = st;
+  bound_ = false;
   if (phase == 1) evaluated_ = true;
   if (n == 0 || pending_code_ != 0) {
     if (phase == 1) enqueue(d_pos, d_src, st);
@@ -743,6 +816,11 @@ void Plan::attach_collective(Collective* c) {
     throw AnkhError(ANKH_INVALID_ARGUMENT, "collective rank/world does not match the plan's shard");
   }
   coll_.reset(c);
+  if (graph_src_exec_) {
+    cudaGraphExecDestroy(graph_src_exec_);
+    graph_src_exec_ = nullptr;
+    graph_src_warm_ = 0;
+  }
   if (graph_exec_) {  // recapture with the collectives in the graph
     cudaGraphExecDestroy(graph_exec_);
     graph_exec_ = nullptr;

@@ -52,6 +52,12 @@ class Plan {
   void enqueue(const double* d_pos, const double* d_src, cudaStream_t st);
   /// Enqueue including the host->device copy of host inputs.
   void enqueue_host(const double* h_pos, const double* h_src, cudaStream_t st);
+  /// Repeated evaluation with fixed positions:
+  /// copy, validate, bin and sort the positions once ...
+  void set_positions(const double* h_pos, cudaStream_t st);
+  /// ... then evaluate new moments (host n x 10) without re-copying or
+  /// re-binning the positions.
+  void enqueue_sources(const double* h_src, cudaStream_t st);
   /// Wait for the last evaluation and fill the report (throws on validation errors).
   void result(ankh_report_v1* out);
 
@@ -95,6 +101,8 @@ class Plan {
   void allocate();
   void* dalloc(std::size_t bytes);
   /// mode 0: whole evaluation; 1: up to this shard's P2M; 2: from M2M on.
+  // mode 0: full evaluation; 1 / 2: halves around a caller-driven shard
+  // exchange; 3: moments only (positions bound by set_positions)
   void launch_all(const double* d_pos, const double* d_src, cudaStream_t st, int mode = 0);
   void validate_only(const double* d_pos, const double* d_src, cudaStream_t st);
   void exchange_leaves(cudaStream_t st);
@@ -111,6 +119,11 @@ class Plan {
   cudaGraphExec_t graph_exec_ = nullptr;
   const double *graph_pos_ = nullptr, *graph_src_ = nullptr;
   const double *graph_warm_pos_ = nullptr, *graph_warm_src_ = nullptr;
+  // bound positions (set_positions): position flags + the moments-only graph
+  DevResult* d_res_pos_ = nullptr;
+  bool bound_ = false;
+  cudaGraphExec_t graph_src_exec_ = nullptr;
+  int graph_src_warm_ = 0;
   cudaStream_t last_stream_ = nullptr;
   std::vector<void*> allocs_;
   bool csr_only_ = false;

@@ -434,3 +434,47 @@ def test_fmm_converges_to_direct_lattice_sum(cuda):
         errs.append(abs(rep.e_total - exact) / abs(exact))
     assert errs[0] > errs[1] > errs[2], errs
     assert errs[2] < 1e-6, errs
+
+
+def test_bound_positions_series_equals_full_evaluations(cuda):
+    """ankh_plan_set_positions_v1 + ankh_plan_energy_sources_v1 (the config-4
+    pattern: dipoles rescaled, positions fixed) give the full evaluation's
+    energies bit for bit, including through the captured CUDA graph."""
+    pos, src, rb, cfg = inputs.make_config(1)
+    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    full = ankh.Plan(pos.shape[0], rb, ec)
+    bound = ankh.Plan(pos.shape[0], rb, ec, phase_timing=False)
+    bound.set_positions(pos)
+    for f in inputs.rescale_factors(cfg.seed, 4):
+        s = src.copy()
+        s[:, 1:4] *= f
+        want = full.energy(pos, s)
+        got = bound.energy_sources(s)
+        for k in ("e_total", "e_self", "e_near", "e_far", "e_periodic_far"):
+            assert getattr(got, k) == getattr(want, k), (k, getattr(got, k), getattr(want, k))
+        assert got.near_pairs == want.near_pairs
+
+
+def test_bound_positions_validation_and_misuse(cuda):
+    pos, src = inputs.random_system(300, 4.0, seed=41, multipoles=True)
+    ec = ankh.EwaldConfig(order_cheb=3, order_equi=3, depth=2)
+    plan = ankh.Plan(300, 4.0, ec)
+    with pytest.raises(ankh.AnkhRuntimeError, match="positions are not set"):
+        plan.energy_sources(src)
+    plan.set_positions(pos)
+    bad = src.copy()
+    bad[17, 5] = np.nan
+    with pytest.raises(ankh.InvalidArgument, match="non-finite coordinate or moment"):
+        plan.energy_sources(bad)
+    # a valid evaluation afterwards is unaffected by the failed one
+    want = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 4.0), ec)
+    assert plan.energy_sources(src).e_total == pytest.approx(want.e_total, rel=1e-13)
+    out = pos.copy()
+    out[3, 0] = 4.5
+    plan.set_positions(out)
+    with pytest.raises(ankh.InvalidArgument, match="outside box"):
+        plan.energy_sources(src)
+    # a full evaluation supersedes the bound positions
+    plan.energy(pos, src)
+    with pytest.raises(ankh.AnkhRuntimeError, match="positions are not set"):
+        plan.energy_sources(src)
