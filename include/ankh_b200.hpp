@@ -89,13 +89,8 @@ inline void rethrow(int code, const char* err) {
   }
 }
 
-template <class System, class Config, class Report = EnergyReport>
-Report fmm_energy(const System& system, const Config& config, int threads = 1) {
-  static_assert(sizeof(system.positions[0]) == 3 * sizeof(double), "Vec3 layout");
-  static_assert(sizeof(system.sources[0]) == 10 * sizeof(double), "MultipoleSource layout");
-  if (system.positions.size() != system.sources.size())
-    throw std::invalid_argument(
-        "fmm_energy: invalid system: positions and sources must have equal length");
+template <class Config>
+ankh_config_v1 to_c(const Config& config, int threads) {
   ankh_config_v1 c;
   ankh_config_default_v1(&c);
   c.xi = config.xi;
@@ -106,6 +101,20 @@ Report fmm_energy(const System& system, const Config& config, int threads = 1) {
   c.svd_tol = config.svd_tol;
   c.recip_cutoff = config.recip_cutoff;
   c.threads = threads;
+  return c;
+}
+
+template <class Report>
+Report from_c(const ankh_report_v1& r);
+
+template <class System, class Config, class Report = EnergyReport>
+Report fmm_energy(const System& system, const Config& config, int threads = 1) {
+  static_assert(sizeof(system.positions[0]) == 3 * sizeof(double), "Vec3 layout");
+  static_assert(sizeof(system.sources[0]) == 10 * sizeof(double), "MultipoleSource layout");
+  if (system.positions.size() != system.sources.size())
+    throw std::invalid_argument(
+        "fmm_energy: invalid system: positions and sources must have equal length");
+  const ankh_config_v1 c = to_c(config, threads);
   ankh_report_v1 r;
   char err[512];
   const int code = ankh_fmm_energy_v1(
@@ -113,6 +122,11 @@ Report fmm_energy(const System& system, const Config& config, int threads = 1) {
       reinterpret_cast<const double*>(system.sources.data()), system.box_radius, &c, &r, err,
       sizeof(err));
   rethrow(code, err);
+  return from_c<Report>(r);
+}
+
+template <class Report>
+Report from_c(const ankh_report_v1& r) {
   Report out;
   out.e_total = r.e_total;
   out.e_self = r.e_self;
@@ -129,6 +143,64 @@ Report fmm_energy(const System& system, const Config& config, int threads = 1) {
   out.wall_times["total"] = r.t_total;
   return out;
 }
+
+/// Repeated evaluation (the plan API of include/ankh_b200.h): geometry-only
+/// precompute once per (n, box radius, config); positions may be bound once
+/// when only the moments change (ankh_plan_set_positions_v1).
+template <class Config, class Report = EnergyReport>
+class Plan {
+ public:
+  Plan(std::size_t n, double box_radius, const Config& config, int threads = 0) : n_(n) {
+    const ankh_config_v1 c = to_c(config, threads);
+    char err[512];
+    rethrow(ankh_plan_create_v1(n, box_radius, &c, &plan_, err, sizeof(err)), err);
+  }
+  ~Plan() { ankh_plan_destroy_v1(plan_); }
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+
+  /// Full evaluation of host positions (n Vec3) and moments (n MultipoleSource).
+  template <class P, class S>
+  Report energy(const std::vector<P>& positions, const std::vector<S>& sources) {
+    check(positions.size(), sources.size());
+    ankh_report_v1 r;
+    char err[512];
+    rethrow(ankh_plan_energy_v1(plan_, reinterpret_cast<const double*>(positions.data()),
+                                reinterpret_cast<const double*>(sources.data()), &r, err,
+                                sizeof(err)),
+            err);
+    return from_c<Report>(r);
+  }
+  /// Bind positions once (copied, validated, binned) ...
+  template <class P>
+  void set_positions(const std::vector<P>& positions) {
+    check(positions.size(), n_);
+    char err[512];
+    rethrow(ankh_plan_set_positions_v1(plan_, reinterpret_cast<const double*>(positions.data()),
+                                       err, sizeof(err)),
+            err);
+  }
+  /// ... then evaluate new moments at the bound positions.
+  template <class S>
+  Report energy_sources(const std::vector<S>& sources) {
+    check(n_, sources.size());
+    ankh_report_v1 r;
+    char err[512];
+    rethrow(ankh_plan_energy_sources_v1(plan_, reinterpret_cast<const double*>(sources.data()),
+                                        &r, err, sizeof(err)),
+            err);
+    return from_c<Report>(r);
+  }
+
+ private:
+  void check(std::size_t a, std::size_t b) const {
+    if (a != b || a != n_)
+      throw std::invalid_argument(
+          "fmm_energy: invalid system: positions and sources must have equal length");
+  }
+  std::size_t n_;
+  ankh_plan_v1* plan_ = nullptr;
+};
 
 }  // namespace b200
 

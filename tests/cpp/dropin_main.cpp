@@ -8,6 +8,7 @@
 #include <fstream>
 #include <sstream>
 #include <string>
+#include <vector>
 
 #ifdef ANKH_B200_USE_REFERENCE_TYPES
 #include "ankh/types.hpp"  // the reference's own value types (types.hpp:13-135)
@@ -56,6 +57,24 @@ int main(int argc, char** argv) {
   const ankh::EnergyReport r = call(sys, cfg);
   std::printf("%.17g %.17g %.17g %.17g %.17g\n", r.e_total, r.e_self, r.e_near, r.e_far,
               r.e_periodic_far);
+  {
+    // repeated evaluation with bound positions (ankh::b200::Plan), moments halved:
+    // the energy is quadratic in the moments, so e_total scales by exactly 1/4
+    // up to the self-energy and rounding -- printed for the Python side to check
+    ankh::b200::Plan<ankh::EwaldConfig, ankh::EnergyReport> plan(n, sys.box_radius, cfg);
+    plan.set_positions(sys.positions);
+    const ankh::EnergyReport a = plan.energy_sources(sys.sources);
+    std::vector<ankh::MultipoleSource> half = sys.sources;
+    for (auto& s : half) {
+      s.q *= 0.5;
+      s.mu.x *= 0.5;
+      s.mu.y *= 0.5;
+      s.mu.z *= 0.5;
+      for (double& t : s.theta.m) t *= 0.5;
+    }
+    const ankh::EnergyReport b = plan.energy_sources(half);
+    std::printf("plan %.17g %.17g\n", a.e_total, b.e_total);
+  }
   try {
     ankh::EwaldConfig bad = cfg;
     bad.xi = -1.0;

@@ -48,3 +48,9 @@ def test_dropin_runs_and_matches_python(cuda, tmp_path):
     r = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 5.0),
                         ankh.EwaldConfig(order_cheb=4, order_equi=4, depth=2, p=15))
     assert vals == [r.e_total, r.e_self, r.e_near, r.e_far, r.e_periodic_far]
+    # the RAII plan with bound positions: same energy, and a quarter of it for
+    # moments halved (the energy is a quadratic form in the moments)
+    line = [l for l in out.splitlines() if l.startswith("plan ")][0].split()
+    full, quarter = float(line[1]), float(line[2])
+    assert full == r.e_total
+    assert abs(quarter - 0.25 * r.e_total) <= 1e-12 * abs(r.e_total)
