@@ -103,10 +103,31 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--high", action="store_true", help="orders 8-10 only -> golden_high.json")
+    ap.add_argument("--series", action="store_true",
+                    help="with --config 4: all evaluations of the rescale series -> golden_c4_series.json")
     ap.add_argument("--config", type=int, default=None,
                     help="only BASELINE config 3 or 4 (config 4: evaluation 0 of the rescale series)")
     args = ap.parse_args()
     threads = os.cpu_count() or 1
+    if args.config == 4 and args.series:
+        pos, src0, rb, c = inputs.make_config(4)
+        L = c.orders[0]
+        facs = inputs.rescale_factors(c.seed, c.evaluations)
+        out = {"generator": "tests/golden/make_golden.py --config 4 --series",
+               "reference": "oracle/_ref/libankh_ref.so", "n": pos.shape[0], "box_radius": rb,
+               "seed": c.seed, "config": dict(order_cheb=L, order_equi=L),
+               "sha256_positions": sha(pos), "sha256_sources": sha(src0), "evaluations": []}
+        path = os.path.join(HERE, "golden_c4_series.json")
+        for k, f in enumerate(facs):
+            src = src0.copy()
+            src[:, 1:4] *= float(f)
+            rep = R.fmm_energy(pos, src, rb, order_cheb=L, order_equi=L, threads=threads)
+            out["evaluations"].append({"index": k, "dipole_scale": float(f), "energies": energies(rep),
+                                       "ref_wall_total": rep["wall_times"]["total"]})
+            with open(path, "w") as fh:  # written as it goes (long run)
+                json.dump(out, fh, indent=1)
+            print(k, float(f), out["evaluations"][-1]["energies"]["e_total"], flush=True)
+        return
     if args.config is not None:
         pos, src, rb, c = inputs.make_config(args.config)
         L = c.orders[0]

@@ -478,3 +478,22 @@ def test_bound_positions_validation_and_misuse(cuda):
     plan.energy(pos, src)
     with pytest.raises(ankh.AnkhRuntimeError, match="positions are not set"):
         plan.energy_sources(src)
+
+
+def test_config4_series_all_evaluations_vs_reference(cuda):
+    """BASELINE config 4 (8,232,000 atoms, L = 5, depth 6): all 20 evaluations
+    of the dipole-rescaling series through the bound-positions plan API,
+    against the reference's energies for each evaluation."""
+    path = os.path.join(HERE, "golden", "golden_c4_series.json")
+    if not os.path.exists(path):
+        pytest.skip("golden_c4_series.json not generated")
+    want = _load("golden_c4_series.json")
+    pos, src0, rb, cfg = inputs.make_config(4)
+    assert hashlib.sha256(np.ascontiguousarray(pos).tobytes()).hexdigest() == want["sha256_positions"]
+    plan = ankh.Plan(pos.shape[0], rb, ankh.EwaldConfig(**want["config"]), phase_timing=False)
+    plan.set_positions(pos)
+    for ev in want["evaluations"]:
+        src = src0.copy()
+        src[:, 1:4] *= ev["dipole_scale"]
+        rep = plan.energy_sources(src)
+        check_energies(rep, ev["energies"])
