@@ -1,0 +1,227 @@
+// M2L operator compression on the GPU: the exact-SVD
+// path of compress_m2l (fmm.cpp:98-133 with K <= 150, thin BDCSVD there) as a
+// batched one-sided Jacobi SVD, one CTA per symmetry class, then the factor
+// rows and their per-offset signed node permutations written straight into the
+// plan's padded operator blocks.
+//
+//   k_jacobi_svd : W = C V by Jacobi rotations of column pairs (C's columns,
+//                  K x K in shared memory, column-major); sigma_j = |w_j|.
+//                  Round-robin ordering: every step rotates K/2 disjoint pairs
+//                  (one half-warp per pair), K - 1 (or K) steps per sweep, until a
+//                  sweep rotates nothing.  Same rotation formula as the host
+//                  Jacobi (host_numerics.cpp jacobi_colmajor); convergence at
+//                  |w_p.w_q| <= sqrt(K) eps |w_p||w_q| (the rounding level of
+//                  the dot product); pairs with a column below skip_rel of the
+//                  largest are not rotated (see the loop).
+//   k_svd_factors: row r of lmat = w_{o(r)} (= U_k Sigma_k), row r of rmat =
+//                  C^T w_{o(r)} / sigma^2 (= V_k^T; the projection of C onto
+//                  the kept columns, accurate to eps |C| at any kept sigma),
+//                  with o the host's stable descending order of sigma.
+//   k_m2l_pack   : operator row blocks, columns scattered by the offset's node
+//                  permutation (symmetry_of / node_permutation).
+//
+// The rank rule (1 + #{sigma_i > sigma_0 tol}) runs on the host from the
+// downloaded sigmas, exactly as finish() does.
+#include "kernels.cuh"
+
+namespace ankh_b200 {
+
+namespace {
+
+constexpr int kSvdWarps = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double half_sum(double v, unsigned mask) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kSvdWarps * 32) k_jacobi_svd(const double* __restrict__ c_all,
+                                                              int K, double skip_rel,
+                                                              double* __restrict__ w_all,
+                                                              double* __restrict__ sig_all,
+                                                              int* __restrict__ sweeps) {
+  extern __shared__ __align__(16) double smem[];
+  double* w = smem;                 // K x K, column j at w + j K
+  double* nrm = smem + K * K;       // squared column norms
+  __shared__ int rotated;
+  __shared__ double skip2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* c = c_all + static_cast<std::size_t>(blockIdx.x) * K * K;  // row-major C
+  for (int e = tid; e < K * K; e += blockDim.x) {
+    const int i = e / K, j = e - i * K;
+    w[j * K + i] = c[e];
+  }
+  __syncthreads();
+  for (int j = warp; j < K; j += kSvdWarps) {
+    double a = 0.0;
+    for (int i = lane; i < K; i += 32) a = fma(w[j * K + i], w[j * K + i], a);
+    a = warp_sum(a);
+    if (lane == 0) nrm[j] = a;
+  }
+  // rotation threshold sqrt(K) eps |w_p||w_q|: the rounding level of a K-term
+  // dot product summed in lane partials
+  const double eps2 = 2.220446049250313e-16 * 2.220446049250313e-16 * K;
+  const int np = K + (K & 1);  // players (one dummy when K is odd)
+  int sweep = 0;
+  for (; sweep < 100; ++sweep) {
+    __syncthreads();
+    if (warp == 0) {
+      double mx = 0.0;
+      for (int j = lane; j < K; j += 32) mx = fmax(mx, nrm[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) {
+        skip2 = skip_rel > 0.0 ? mx * skip_rel * skip_rel : 0.0;
+        rotated = 0;
+      }
+    }
+    __syncthreads();
+    const double sk2 = skip2;
+    // one pair per half-warp (16 lanes): K/2 <= 64 pairs per step for K <= 128
+    const int hl = lane & 15, grp = tid >> 4, ngrp = blockDim.x >> 4;
+    const unsigned hmask = 0xffffu << (lane & 16);
+    for (int step = 0; step < np - 1; ++step) {
+      for (int pi = grp; pi < np / 2; pi += ngrp) {
+        int p, q;
+        if (pi == 0) {
+          p = step;
+          q = np - 1;
+        } else {
+          p = (step + pi) % (np - 1);
+          q = (step - pi + np - 1) % (np - 1);
+        }
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        if (q >= K) continue;  // the dummy player
+        const double alpha = nrm[p], beta = nrm[q];
+        // skip a pair when either column is below the skip level (the host
+        // skips only when both are): rotations against columns that small
+        // are rounding noise that keeps the sweeps from terminating (with the
+        // host rule many classes hit the sweep cap; with this one every class
+        // at config 3 converges in 17..29 sweeps, scripts/svd_emulate.cpp).
+        // An unrotated column u leaves its component along the kept columns
+        // behind -- first order in |u| -- so the plan passes a skip level far
+        // below the truncation (svd_tol 1e-6: 1e-13 sigma_0; kept subspace
+        // then within 4e-10 of LAPACK's, scripts/svd_accuracy.py).
+        if (fmin(alpha, beta) < sk2) continue;
+        double* wp = w + p * K;
+        double* wq = w + q * K;
+        double g = 0.0;
+        for (int i = hl; i < K; i += 16) g = fma(wp[i], wq[i], g);
+        g = half_sum(g, hmask);
+        if (g == 0.0 || g * g <= eps2 * alpha * beta) continue;
+        const double zeta = (beta - alpha) / (2.0 * g);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double cs = rsqrt(fma(t, t, 1.0));
+        const double sn = cs * t;
+        double a2 = 0.0, b2 = 0.0;
+        for (int i = hl; i < K; i += 16) {
+          const double x = wp[i], y = wq[i];
+          const double a = cs * x - sn * y, b = sn * x + cs * y;
+          wp[i] = a;
+          wq[i] = b;
+          a2 = fma(a, a, a2);
+          b2 = fma(b, b, b2);
+        }
+        a2 = half_sum(a2, hmask);
+        b2 = half_sum(b2, hmask);
+        if (hl == 0) {
+          nrm[p] = a2;
+          nrm[q] = b2;
+          rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+  }
+  double* wo = w_all + static_cast<std::size_t>(blockIdx.x) * K * K;
+  for (int e = tid; e < K * K; e += blockDim.x) wo[e] = w[e];
+  for (int j = warp; j < K; j += kSvdWarps) {
+    double a = 0.0;
+    for (int i = lane; i < K; i += 32) a = fma(w[j * K + i], w[j * K + i], a);
+    a = warp_sum(a);
+    if (lane == 0) sig_all[static_cast<std::size_t>(blockIdx.x) * K + j] = sqrt(a);
+  }
+  if (tid == 0 && sweeps) sweeps[blockIdx.x] = sweep;
+}
+
+// grid (classes, K): block r < rank[cls] writes lmat / rmat row r
+__global__ void k_svd_factors(const double* __restrict__ c_all, const double* __restrict__ w_all,
+                              const double* __restrict__ sig_all, const int* __restrict__ order,
+                              const int* __restrict__ rank, int K, double* __restrict__ lf,
+                              double* __restrict__ rf) {
+  const int cls = blockIdx.x, r = blockIdx.y;
+  if (r >= rank[cls]) return;
+  const std::size_t kk = static_cast<std::size_t>(K) * K;
+  const int j = order[static_cast<std::size_t>(cls) * K + r];
+  const double* wj = w_all + cls * kk + static_cast<std::size_t>(j) * K;
+  const double* c = c_all + cls * kk;
+  const double s = sig_all[static_cast<std::size_t>(cls) * K + j];
+  const double inv = 1.0 / (s * s);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double a = 0.0;
+    for (int i = 0; i < K; ++i) a = fma(c[static_cast<std::size_t>(i) * K + k], wj[i], a);
+    lf[cls * kk + static_cast<std::size_t>(r) * K + k] = wj[k];
+    rf[cls * kk + static_cast<std::size_t>(r) * K + k] = a * inv;
+  }
+}
+
+// grid (operator blocks, rows): dst rows of the L and R halves of one block
+__global__ void k_m2l_pack(const M2LPack* __restrict__ ops, const int* __restrict__ perms,
+                           const double* __restrict__ lf, const double* __restrict__ rf, int K,
+                           int Kp, double* __restrict__ factors) {
+  const M2LPack op = ops[blockIdx.x];
+  const int r = blockIdx.y;
+  if (r >= op.rows) return;
+  const std::size_t kk = static_cast<std::size_t>(K) * K;
+  const int* perm = perms + op.perm_off;
+  const double* ls = lf + op.cls * kk + static_cast<std::size_t>(op.r0 + r) * K;
+  const double* rs = rf + op.cls * kk + static_cast<std::size_t>(op.r0 + r) * K;
+  double* dl = factors + op.factor_off + static_cast<std::size_t>(r) * Kp;
+  double* dr = factors + op.factor_off + static_cast<std::size_t>(op.kp) * Kp +
+               static_cast<std::size_t>(r) * Kp;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    dl[perm[k]] = ls[k];
+    dr[perm[k]] = rs[k];
+  }
+}
+
+}  // namespace
+
+std::size_t jacobi_svd_smem(int K) { return (static_cast<std::size_t>(K) * K + K) * sizeof(double); }
+
+void launch_jacobi_svd(const double* c_all, int n_classes, int K, double skip_rel, double* w_all,
+                       double* sig_all, int* sweeps, cudaStream_t st) {
+  if (n_classes == 0) return;
+  const std::size_t smem = jacobi_svd_smem(K);
+  cudaFuncSetAttribute(k_jacobi_svd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  k_jacobi_svd<<<n_classes, kSvdWarps * 32, smem, st>>>(c_all, K, skip_rel, w_all, sig_all, sweeps);
+}
+
+void launch_svd_factors(const double* c_all, const double* w_all, const double* sig_all,
+                        const int* order, const int* rank, int n_classes, int K, double* lf,
+                        double* rf, cudaStream_t st) {
+  if (n_classes == 0) return;
+  k_svd_factors<<<dim3(n_classes, K), 128, 0, st>>>(c_all, w_all, sig_all, order, rank, K, lf, rf);
+}
+
+void launch_m2l_pack(const M2LPack* ops, int n_ops, int max_rows, const int* perms,
+                     const double* lf, const double* rf, int K, int Kp, double* factors,
+                     cudaStream_t st) {
+  if (n_ops == 0) return;
+  k_m2l_pack<<<dim3(n_ops, max_rows), 128, 0, st>>>(ops, perms, lf, rf, K, Kp, factors);
+}
+
+}  // namespace ankh_b200

@@ -145,6 +145,23 @@ int direct_partials(int n, int p);
 void launch_direct(const double* pos, const double* src, int n, double box_radius, double xi,
                    int p, const P2PRadial& rad, double* rec, double* partial, cudaStream_t st);
 double probe_dmma_tflops(int shape, int iters);
+
+// M2L operator compression on the GPU (k_svd.cu)
+struct M2LPack {
+  long long factor_off;  // operator block (as M2LOp)
+  int cls;               // symmetry class (row of the class factor arrays)
+  int r0, rows, kp;      // rank rows [r0, r0 + rows) of the class factors
+  int perm_off;          // node permutation (K ints) in the perm array
+};
+std::size_t jacobi_svd_smem(int K);
+void launch_jacobi_svd(const double* c_all, int n_classes, int K, double skip_rel, double* w_all,
+                       double* sig_all, int* sweeps, cudaStream_t st);
+void launch_svd_factors(const double* c_all, const double* w_all, const double* sig_all,
+                        const int* order, const int* rank, int n_classes, int K, double* lf,
+                        double* rf, cudaStream_t st);
+void launch_m2l_pack(const M2LPack* ops, int n_ops, int max_rows, const int* perms,
+                     const double* lf, const double* rf, int K, int Kp, double* factors,
+                     cudaStream_t st);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);
 

@@ -316,7 +316,85 @@ void Plan::build_m2l() {
   // factors: exact SVD path uses the signed-permutation symmetry of the block
   // (one SVD per class, SURVEY.md Decision 3); K > 150 replicates the
   // reference's seeded randomized path per offset.
-  if (K <= 150) {
+  // GPU path (default for the exact SVD): dense class blocks on the host (the
+  // reference's erfc formula), batched Jacobi SVD + factor rows on the device
+  // (k_svd.cu); only the sigmas come back for the rank rule.
+  std::vector<int> work_cls;
+  DeviceScratch svd_tmp(stream_);
+  double *d_lf = nullptr, *d_rf = nullptr;
+  const bool gpu_fac = K <= 150 && std::getenv("ANKH_HOST_SVD") == nullptr;
+  if (gpu_fac) {
+    std::map<std::pair<int, std::array<int, 3>>, int> cls_of;
+    for (const auto& w : work) cls_of[{w.level, symmetry_of(w.o).rep}] = 0;
+    std::vector<std::pair<int, std::array<int, 3>>> keys;
+    for (auto& kv : cls_of) {
+      kv.second = static_cast<int>(keys.size());
+      keys.push_back(kv.first);
+    }
+    const int nc = static_cast<int>(keys.size());
+    const std::size_t kk = static_cast<std::size_t>(K) * K;
+    std::vector<double> hc(nc * kk);
+    parallel_for(nc, threads, [&](int i) {
+      const std::vector<double> c = m2l_dense(L, rb / (1 << keys[i].first), keys[i].second, cfg.xi);
+      std::copy(c.begin(), c.end(), hc.begin() + i * kk);
+    });
+    stamp("dense");
+    double* d_c = svd_tmp.alloc<double>(nc * kk);
+    double* d_w = svd_tmp.alloc<double>(nc * kk);
+    double* d_sig = svd_tmp.alloc<double>(static_cast<std::size_t>(nc) * K);
+    d_lf = svd_tmp.alloc<double>(nc * kk);
+    d_rf = svd_tmp.alloc<double>(nc * kk);
+    int* d_order = svd_tmp.alloc<int>(static_cast<std::size_t>(nc) * K);
+    int* d_rank = svd_tmp.alloc<int>(nc);
+    ANKH_CUDA(cudaMemcpyAsync(d_c, hc.data(), hc.size() * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    int* d_sweeps = verbose ? svd_tmp.alloc<int>(nc) : nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (verbose) {
+      ANKH_CUDA(cudaEventCreate(&e0));
+      ANKH_CUDA(cudaEventCreate(&e1));
+      ANKH_CUDA(cudaEventRecord(e0, stream_));
+    }
+    launch_jacobi_svd(d_c, nc, K, cfg.svd_tol * 1e-6, d_w, d_sig, d_sweeps, stream_);
+    ANKH_CUDA(cudaGetLastError());
+    if (verbose) {
+      ANKH_CUDA(cudaEventRecord(e1, stream_));
+      ANKH_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      ANKH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      std::vector<int> sw(nc);
+      ANKH_CUDA(cudaMemcpy(sw.data(), d_sweeps, nc * sizeof(int), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[ankh plan]   m2l jacobi kernel %.3f ms, %d classes, sweeps max %d\n", ms, nc,
+                   nc ? *std::max_element(sw.begin(), sw.end()) : 0);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    std::vector<double> sig(static_cast<std::size_t>(nc) * K);
+    ANKH_CUDA(cudaMemcpyAsync(sig.data(), d_sig, sig.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    ANKH_CUDA(cudaStreamSynchronize(stream_));
+    // finish() (host_numerics.cpp): stable descending order, rank rule
+    std::vector<int> order(static_cast<std::size_t>(nc) * K), rank(nc);
+    for (int i = 0; i < nc; ++i) {
+      int* o = order.data() + static_cast<std::size_t>(i) * K;
+      const double* sv = sig.data() + static_cast<std::size_t>(i) * K;
+      std::iota(o, o + K, 0);
+      std::stable_sort(o, o + K, [&](int x, int y) { return sv[x] > sv[y]; });
+      int r = 1;
+      while (r < K && sv[o[r]] > sv[o[0]] * cfg.svd_tol) ++r;
+      rank[i] = r;
+    }
+    ANKH_CUDA(cudaMemcpyAsync(d_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    ANKH_CUDA(cudaMemcpyAsync(d_rank, rank.data(), rank.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    launch_svd_factors(d_c, d_w, d_sig, d_order, d_rank, nc, K, d_lf, d_rf, stream_);
+    ANKH_CUDA(cudaGetLastError());
+    work_cls.resize(work.size());
+    for (std::size_t wi = 0; wi < work.size(); ++wi) {
+      const int c = cls_of.at({work[wi].level, symmetry_of(work[wi].o).rep});
+      work_cls[wi] = c;
+      work[wi].f.rank = rank[c];
+      work[wi].f.k_full = K;
+    }
+    ANKH_CUDA(cudaStreamSynchronize(stream_));  // the host vectors above go out of scope
+  } else if (K <= 150) {
     std::map<std::pair<int, std::array<int, 3>>, Factors> reps;
     for (const auto& w : work) reps[{w.level, symmetry_of(w.o).rep}] = Factors{};
     std::vector<std::pair<int, std::array<int, 3>>> keys;
@@ -392,22 +470,47 @@ void Plan::build_m2l() {
     far_flops += static_cast<double>(w.inst.size()) * (4.0 * rank * K + 2.0 * rank);
   }
   m2l_instances = n_inst;
-  h_factors_.assign(n_fac, 0.0);
   std::vector<uint2> inst(n_inst);
   parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
     std::copy(work[wi].inst.begin(), work[wi].inst.end(), inst.begin() + inst_begin[wi]);
   });
-  parallel_for(static_cast<int>(blocks.size()), threads, [&](int bi) {
-    const Block& b = blocks[bi];
-    const Factors& f = work[b.work].f;
-    double* dl = h_factors_.data() + h_ops_[bi].factor_off;
-    double* dr = dl + static_cast<std::size_t>(h_ops_[bi].kp) * Kp;
-    for (int r = 0; r < b.rows; ++r)
-      for (int k = 0; k < K; ++k) {
-        dl[static_cast<std::size_t>(r) * Kp + k] = f.lmat[static_cast<std::size_t>(b.r0 + r) * K + k];
-        dr[static_cast<std::size_t>(r) * Kp + k] = f.rmat[static_cast<std::size_t>(b.r0 + r) * K + k];
+  std::vector<double> h_factors;  // host-built operator blocks (host SVD paths)
+  std::vector<M2LPack> packs;     // GPU path: block descriptors for k_m2l_pack
+  std::vector<int> perms;
+  int max_rows = 0;
+  if (gpu_fac) {
+    std::map<std::array<int, 3>, int> perm_off;  // one permutation per distinct offset
+    std::vector<int> work_perm(work.size());
+    for (std::size_t wi = 0; wi < work.size(); ++wi) {
+      auto it = perm_off.find(work[wi].o);
+      if (it == perm_off.end()) {
+        it = perm_off.emplace(work[wi].o, static_cast<int>(perms.size())).first;
+        const std::vector<int> p = node_permutation(symmetry_of(work[wi].o), L);
+        perms.insert(perms.end(), p.begin(), p.end());
       }
-  });
+      work_perm[wi] = it->second;
+    }
+    packs.resize(blocks.size());
+    for (std::size_t bi = 0; bi < blocks.size(); ++bi) {
+      const Block& b = blocks[bi];
+      packs[bi] = {h_ops_[bi].factor_off, work_cls[b.work], b.r0, b.rows, h_ops_[bi].kp,
+                   work_perm[b.work]};
+      max_rows = std::max(max_rows, b.rows);
+    }
+  } else {
+    h_factors.assign(n_fac, 0.0);
+    parallel_for(static_cast<int>(blocks.size()), threads, [&](int bi) {
+      const Block& b = blocks[bi];
+      const Factors& f = work[b.work].f;
+      double* dl = h_factors.data() + h_ops_[bi].factor_off;
+      double* dr = dl + static_cast<std::size_t>(h_ops_[bi].kp) * Kp;
+      for (int r = 0; r < b.rows; ++r)
+        for (int k = 0; k < K; ++k) {
+          dl[static_cast<std::size_t>(r) * Kp + k] = f.lmat[static_cast<std::size_t>(b.r0 + r) * K + k];
+          dr[static_cast<std::size_t>(r) * Kp + k] = f.rmat[static_cast<std::size_t>(b.r0 + r) * K + k];
+        }
+    });
+  }
   m2l_operators = work.size();
   m2l_rank_mean = work.empty() ? 0.0 : rank_sum / work.size();
   n_tiles_ = static_cast<int>(tiles.size());
@@ -423,14 +526,28 @@ void Plan::build_m2l() {
     class_range_[c] = {begin, static_cast<int>(ids.size()) - begin};
   }
   stamp("pack");
-  d_factors_ = static_cast<double*>(dalloc(h_factors_.size() * sizeof(double)));
+  n_factors_ = n_fac;
+  d_factors_ = static_cast<double*>(dalloc(std::max<std::size_t>(n_fac, 1) * sizeof(double)));
   d_ops_ = static_cast<M2LOp*>(dalloc(h_ops_.size() * sizeof(M2LOp)));
   d_tiles_ = static_cast<M2LTile*>(dalloc(tiles.size() * sizeof(M2LTile)));
   d_inst_ = static_cast<uint2*>(dalloc(inst.size() * sizeof(uint2)));
   d_tile_ids_ = static_cast<int*>(dalloc(std::max<std::size_t>(ids.size(), 1) * sizeof(int)));
   d_far_part_ = static_cast<double*>(dalloc(std::max<std::size_t>(tiles.size(), 1) * sizeof(double)));
-  ANKH_CUDA(cudaMemcpyAsync(d_factors_, h_factors_.data(), h_factors_.size() * sizeof(double),
-                            cudaMemcpyHostToDevice, stream_));
+  if (gpu_fac) {
+    M2LPack* d_packs = svd_tmp.alloc<M2LPack>(std::max<std::size_t>(packs.size(), 1));
+    int* d_perms = svd_tmp.alloc<int>(std::max<std::size_t>(perms.size(), 1));
+    ANKH_CUDA(cudaMemsetAsync(d_factors_, 0, n_fac * sizeof(double), stream_));
+    ANKH_CUDA(cudaMemcpyAsync(d_packs, packs.data(), packs.size() * sizeof(M2LPack),
+                              cudaMemcpyHostToDevice, stream_));
+    ANKH_CUDA(cudaMemcpyAsync(d_perms, perms.data(), perms.size() * sizeof(int),
+                              cudaMemcpyHostToDevice, stream_));
+    launch_m2l_pack(d_packs, static_cast<int>(packs.size()), max_rows, d_perms, d_lf, d_rf, K, Kp,
+                    d_factors_, stream_);
+    ANKH_CUDA(cudaGetLastError());
+  } else {
+    ANKH_CUDA(cudaMemcpyAsync(d_factors_, h_factors.data(), h_factors.size() * sizeof(double),
+                              cudaMemcpyHostToDevice, stream_));
+  }
   ANKH_CUDA(cudaMemcpyAsync(d_ops_, h_ops_.data(), h_ops_.size() * sizeof(M2LOp),
                             cudaMemcpyHostToDevice, stream_));
   ANKH_CUDA(cudaMemcpyAsync(d_tiles_, tiles.data(), tiles.size() * sizeof(M2LTile),
@@ -842,7 +959,10 @@ void Plan::m2l_factors(int level, const int* offset, double* lmat, double* rmat,
   int row = 0;
   for (int b = 0; b < info.n_blocks; ++b) {
     const M2LOp& op = h_ops_[info.first_op + b];
-    const double* Lb = h_factors_.data() + op.factor_off;
+    std::vector<double> blk(2 * static_cast<std::size_t>(op.kp) * Kp);
+    ANKH_CUDA(cudaMemcpy(blk.data(), d_factors_ + op.factor_off, blk.size() * sizeof(double),
+                         cudaMemcpyDeviceToHost));
+    const double* Lb = blk.data();
     const double* Rb = Lb + static_cast<std::size_t>(op.kp) * Kp;
     for (int r = 0; r < op.rank; ++r, ++row)
       for (int k = 0; k < K; ++k) {

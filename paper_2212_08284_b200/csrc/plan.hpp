@@ -28,6 +28,26 @@ struct AnkhError : std::runtime_error {
                                                         cudaGetErrorString(e_));        \
   } while (0)
 
+/// Temporary device buffers from the stream-ordered pool (cudaMallocAsync),
+/// released on the same stream at scope exit.
+struct DeviceScratch {
+  explicit DeviceScratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* alloc(std::size_t count) {
+    void* q = nullptr;
+    ANKH_CUDA(cudaMallocAsync(&q, (count ? count : 1) * sizeof(T), st));
+    ptrs.push_back(q);
+    return static_cast<T*>(q);
+  }
+  DeviceScratch(const DeviceScratch&) = delete;
+  DeviceScratch& operator=(const DeviceScratch&) = delete;
+  ~DeviceScratch() {
+    for (void* q : ptrs) cudaFreeAsync(q, st);
+  }
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+};
+
 /// types.cpp:9-14
 int default_depth(std::size_t n);
 /// types.cpp:65-79 (throws AnkhError(ANKH_INVALID_ARGUMENT, same message))
@@ -157,7 +177,7 @@ class Plan {
   std::vector<std::pair<int, int>> class_range_;  // per kp8: (begin, count) in d_tile_ids_
   int n_tiles_ = 0;
   std::map<std::pair<int, std::int64_t>, OpInfo> op_info_;
-  std::vector<double> h_factors_;  // kept for introspection
+  std::size_t n_factors_ = 0;  // doubles in d_factors_ (m2l_factors reads them back)
   std::vector<M2LOp> h_ops_;
   // partials
   double *d_near_part_ = nullptr, *d_far_part_ = nullptr, *d_self_part_ = nullptr,

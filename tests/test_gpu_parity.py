@@ -204,6 +204,30 @@ def test_m2l_factors(cuda, ref, L, level, offset):
     assert np.abs(lm.T @ rm - l2.T @ r2).max() <= 1e-12 * np.abs(c).max()
 
 
+@pytest.mark.parametrize("L", [3, 4, 5])
+def test_gpu_svd_matches_host_svd(cuda, ref, L, monkeypatch):
+    """The plan's M2L factors from the batched GPU Jacobi SVD (k_svd.cu, the
+    default for K <= 150) and from the host Jacobi (ANKH_HOST_SVD=1) give the
+    same ranks, the same truncated operators L^T R and the same energies."""
+    rb = 10.0
+    pos, src = inputs.random_system(1500, rb, seed=31 + L, multipoles=True)
+    cfg = ankh.EwaldConfig(order_cheb=L, order_equi=L, depth=3)
+    gpu = ankh.Plan(1500, rb, cfg)
+    monkeypatch.setenv("ANKH_HOST_SVD", "1")
+    host = ankh.Plan(1500, rb, cfg)
+    monkeypatch.delenv("ANKH_HOST_SVD")
+    for level, off in [(1, (2, 0, 0)), (2, (-3, 1, 2)), (2, (0, -2, 3)), (3, (3, 3, -2)), (3, (2, 2, 2))]:
+        lg, rg = gpu.m2l_factors(level, off)
+        lh, rh = host.m2l_factors(level, off)
+        assert lg.shape == lh.shape, (level, off)
+        c = ref.m2l_dense(L, rb / (1 << level), off)
+        assert np.abs(lg.T @ rg - lh.T @ rh).max() <= 1e-12 * np.abs(c).max(), (level, off)
+    a, b = gpu.energy(pos, src), host.energy(pos, src)
+    assert a.e_near == b.e_near
+    assert abs(a.e_far - b.e_far) <= 1e-13 * abs(a.e_total)
+    assert abs(a.e_total - b.e_total) <= 1e-13 * abs(a.e_total)
+
+
 def test_deterministic_and_device_path(cuda):
     torch = cuda
     pos, src, rb, cfg = inputs.make_config(1)
