@@ -146,6 +146,15 @@ void launch_direct(const double* pos, const double* src, int n, double box_radiu
                    int p, const P2PRadial& rad, double* rec, double* partial, cudaStream_t st);
 double probe_dmma_tflops(int shape, int iters);
 
+// M2L instance lists on the GPU (k_inst.cu)
+std::size_t m2l_instances_device(int depth, int periodic, int rank, int world, const int4* d_offs,
+                                 int n_offs, unsigned* d_counts, unsigned* d_offsets,
+                                 std::size_t n_blocks_total, void* d_temp, std::size_t temp_bytes,
+                                 uint2* inst, cudaStream_t st);
+std::size_t m2l_instances_temp_bytes(std::size_t n_blocks_total);
+std::size_t m2l_instance_blocks(int depth, int n_offs);
+int m2l_instance_block_size();
+
 // M2L operator compression on the GPU (k_svd.cu)
 struct M2LPack {
   long long factor_off;  // operator block (as M2LOp)

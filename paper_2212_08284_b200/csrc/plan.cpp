@@ -280,7 +280,8 @@ void Plan::build_m2l() {
   struct OffsetWork {
     int level;
     std::array<int, 3> o;
-    std::vector<uint2> inst;
+    std::vector<uint2> inst;  // host enumeration only
+    std::size_t count = 0;    // instances of this operator
     Factors f;
   };
   const int threads = cfg.threads;
@@ -293,10 +294,60 @@ void Plan::build_m2l() {
                  std::chrono::duration<double, std::milli>(now - t_last).count());
     t_last = now;
   };
-  // canonical instances owned by this shard (shard.cpp, fmm.cpp:244-253)
-  std::vector<OffsetInstances> groups =
-      enumerate_m2l(depth, periodic, cfg.world > 1 ? cfg.rank : -1, cfg.world, threads);
-  std::vector<OffsetWork> work(groups.size());
+  // canonical instances owned by this shard (shard.cpp, fmm.cpp:244-253):
+  // generated on the device straight into d_inst_ (k_inst.cu; same operator
+  // order and per-operator target-Morton order as the host enumeration,
+  // which ANKH_HOST_INST=1 selects)
+  const bool gpu_inst = std::getenv("ANKH_HOST_INST") == nullptr;
+  std::vector<OffsetWork> work;
+  std::vector<OffsetInstances> groups;
+  DeviceScratch inst_tmp(stream_);
+  if (gpu_inst) {
+    std::vector<int4> offs;
+    for (int ox = -3; ox <= 3; ++ox)
+      for (int oy = -3; oy <= 3; ++oy)
+        for (int oz = -3; oz <= 3; ++oz)
+          if (std::max({std::abs(ox), std::abs(oy), std::abs(oz)}) >= 2) offs.push_back(make_int4(ox, oy, oz, 0));
+    const int n_offs = static_cast<int>(offs.size());
+    const std::size_t nb = m2l_instance_blocks(depth, n_offs);
+    int4* d_offs = inst_tmp.alloc<int4>(offs.size());
+    unsigned* d_counts = inst_tmp.alloc<unsigned>(nb + 1);
+    unsigned* d_offsets = inst_tmp.alloc<unsigned>(nb + 1);
+    const std::size_t tb = m2l_instances_temp_bytes(nb);
+    void* d_temp = inst_tmp.alloc<unsigned char>(tb);
+    ANKH_CUDA(cudaMemcpyAsync(d_offs, offs.data(), offs.size() * sizeof(int4), cudaMemcpyHostToDevice, stream_));
+    ANKH_CUDA(cudaMemsetAsync(d_counts, 0, (nb + 1) * sizeof(unsigned), stream_));
+    const int shard = cfg.world > 1 ? cfg.rank : -1;
+    m2l_instances_device(depth, periodic, shard, cfg.world, d_offs, n_offs, d_counts, d_offsets, nb, d_temp,
+                         tb, nullptr, stream_);
+    ANKH_CUDA(cudaGetLastError());
+    std::vector<unsigned> off(nb + 1);
+    ANKH_CUDA(cudaMemcpyAsync(off.data(), d_offsets, off.size() * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                              stream_));
+    ANKH_CUDA(cudaStreamSynchronize(stream_));
+    const std::size_t total = off[nb];
+    d_inst_ = static_cast<uint2*>(dalloc(std::max<std::size_t>(total, 1) * sizeof(uint2)));
+    m2l_instances_device(depth, periodic, shard, cfg.world, d_offs, n_offs, d_counts, d_offsets, nb, d_temp,
+                         tb, d_inst_, stream_);
+    ANKH_CUDA(cudaGetLastError());
+    const int bs = m2l_instance_block_size();
+    std::size_t blk = 0;
+    for (int level = 1; level <= depth; ++level) {
+      const std::size_t per_op = ((std::size_t(1) << (3 * level)) + bs - 1) / bs;
+      for (int j = 0; j < n_offs; ++j, blk += per_op) {
+        const std::size_t c = off[blk + per_op] - off[blk];
+        if (c == 0) continue;
+        OffsetWork w;
+        w.level = level;
+        w.o = {offs[j].x, offs[j].y, offs[j].z};
+        w.count = c;
+        work.push_back(std::move(w));
+      }
+    }
+  } else {
+    groups = enumerate_m2l(depth, periodic, cfg.world > 1 ? cfg.rank : -1, cfg.world, threads);
+    work.resize(groups.size());
+  }
   parallel_for(static_cast<int>(groups.size()), threads, [&](int i) {
     work[i].level = groups[i].level;
     work[i].o = groups[i].offset;
@@ -309,6 +360,7 @@ void Plan::build_m2l() {
       work[i].inst[k] = make_uint2(to_morton(groups[i].t[k]), to_morton(groups[i].s[k]));
     std::sort(work[i].inst.begin(), work[i].inst.end(),
               [](const uint2& a, const uint2& b) { return a.x < b.x; });
+    work[i].count = work[i].inst.size();
     groups[i] = OffsetInstances{};  // release as we go
   });
   groups.clear();
@@ -460,20 +512,21 @@ void Plan::build_m2l() {
       h_ops_.push_back(op);
       blocks.push_back({static_cast<int>(wi), r0, rows});
       ++info.n_blocks;
-      for (int b = 0; b < static_cast<int>(w.inst.size()); b += kM2LTile)
+      for (int b = 0; b < static_cast<int>(w.count); b += kM2LTile)
         tiles.push_back({op_index, w.level, static_cast<int>(n_inst) + b,
-                         std::min(kM2LTile, static_cast<int>(w.inst.size()) - b)});
+                         std::min(kM2LTile, static_cast<int>(w.count) - b)});
     }
     op_info_[{w.level, info.key}] = info;
     rank_sum += rank;
-    n_inst += w.inst.size();
-    far_flops += static_cast<double>(w.inst.size()) * (4.0 * rank * K + 2.0 * rank);
+    n_inst += w.count;
+    far_flops += static_cast<double>(w.count) * (4.0 * rank * K + 2.0 * rank);
   }
   m2l_instances = n_inst;
-  std::vector<uint2> inst(n_inst);
-  parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
-    std::copy(work[wi].inst.begin(), work[wi].inst.end(), inst.begin() + inst_begin[wi]);
-  });
+  std::vector<uint2> inst(gpu_inst ? 0 : n_inst);  // host enumeration: gathered for the upload
+  if (!gpu_inst)
+    parallel_for(static_cast<int>(work.size()), threads, [&](int wi) {
+      std::copy(work[wi].inst.begin(), work[wi].inst.end(), inst.begin() + inst_begin[wi]);
+    });
   std::vector<double> h_factors;  // host-built operator blocks (host SVD paths)
   std::vector<M2LPack> packs;     // GPU path: block descriptors for k_m2l_pack
   std::vector<int> perms;
@@ -530,7 +583,7 @@ void Plan::build_m2l() {
   d_factors_ = static_cast<double*>(dalloc(std::max<std::size_t>(n_fac, 1) * sizeof(double)));
   d_ops_ = static_cast<M2LOp*>(dalloc(h_ops_.size() * sizeof(M2LOp)));
   d_tiles_ = static_cast<M2LTile*>(dalloc(tiles.size() * sizeof(M2LTile)));
-  d_inst_ = static_cast<uint2*>(dalloc(inst.size() * sizeof(uint2)));
+  if (!gpu_inst) d_inst_ = static_cast<uint2*>(dalloc(std::max<std::size_t>(inst.size(), 1) * sizeof(uint2)));
   d_tile_ids_ = static_cast<int*>(dalloc(std::max<std::size_t>(ids.size(), 1) * sizeof(int)));
   d_far_part_ = static_cast<double*>(dalloc(std::max<std::size_t>(tiles.size(), 1) * sizeof(double)));
   if (gpu_fac) {
@@ -552,8 +605,9 @@ void Plan::build_m2l() {
                             cudaMemcpyHostToDevice, stream_));
   ANKH_CUDA(cudaMemcpyAsync(d_tiles_, tiles.data(), tiles.size() * sizeof(M2LTile),
                             cudaMemcpyHostToDevice, stream_));
-  ANKH_CUDA(cudaMemcpyAsync(d_inst_, inst.data(), inst.size() * sizeof(uint2),
-                            cudaMemcpyHostToDevice, stream_));
+  if (!gpu_inst)
+    ANKH_CUDA(cudaMemcpyAsync(d_inst_, inst.data(), inst.size() * sizeof(uint2),
+                              cudaMemcpyHostToDevice, stream_));
   if (!ids.empty())
     ANKH_CUDA(cudaMemcpyAsync(d_tile_ids_, ids.data(), ids.size() * sizeof(int),
                               cudaMemcpyHostToDevice, stream_));

@@ -228,6 +228,26 @@ def test_gpu_svd_matches_host_svd(cuda, ref, L, monkeypatch):
     assert abs(a.e_total - b.e_total) <= 1e-13 * abs(a.e_total)
 
 
+@pytest.mark.parametrize("p,world", [(15, 1), (0, 1), (15, 3), (0, 4)])
+def test_gpu_instances_match_host_enumeration(cuda, p, world, monkeypatch):
+    """M2L instance lists generated on the device (k_inst.cu, the default) equal
+    the host enumeration (ANKH_HOST_INST=1): same per-shard counts and, in
+    the same order, bit-identical single-GPU energies."""
+    rb, n = 9.0, 3000
+    pos, src = inputs.random_system(n, rb, seed=77 + p, multipoles=True)
+    cfg = ankh.EwaldConfig(order_cheb=4, order_equi=4, depth=3, p=p)
+    for r in range(world):
+        kw = dict(rank=r, world=world) if world > 1 else {}
+        gpu = ankh.Plan(n, rb, cfg, **kw)
+        monkeypatch.setenv("ANKH_HOST_INST", "1")
+        host = ankh.Plan(n, rb, cfg, **kw)
+        monkeypatch.delenv("ANKH_HOST_INST")
+        assert gpu.info()["m2l_instances"] == host.info()["m2l_instances"] > 0
+        if world == 1:
+            a, b = gpu.energy(pos, src), host.energy(pos, src)
+            assert (a.e_far, a.e_total) == (b.e_far, b.e_total)
+
+
 def test_deterministic_and_device_path(cuda):
     torch = cuda
     pos, src, rb, cfg = inputs.make_config(1)
