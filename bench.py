@@ -18,6 +18,10 @@ value      : evaluations/s of the whole job (max-over-ranks device time),
 e2e        : the same metric through the drop-in C-ABI call
              ankh_fmm_energy_v1 with pinned HOST buffers, H2D of all inputs
              and D2H of the result inside every timed step.
+e2e_fixed_positions : positions bound once (ankh_plan_set_positions_v1), each
+             step copies and evaluates new moments (the config-4 pattern).
+e2e_including_precompute : one-shot calls that rebuild the plan every step
+             (as the reference rebuilds its precompute on every call).
 roofline   : the dominant kernel (P2P), nominal 229 flop per multipole pair
               x pairs / its CUDA-event duration, against the
              FP64 DFMA peak measured in-process (MEASURED_PEAKS.json has no
@@ -367,7 +371,7 @@ def main():
     plan_t.close()
 
     # ---- e2e through the drop-in C-ABI with pinned host buffers ----
-    e2e = e2e_fixed = None
+    e2e = e2e_fixed = e2e_cold = None
     if not args.no_e2e:
         hp = torch.from_numpy(pos).pin_memory()
         hs = torch.from_numpy(src).pin_memory()
@@ -415,6 +419,28 @@ def main():
                      "d2h_bytes_per_step": 72, "steps": k2,
                      "api": "ankh_plan_set_positions_v1 once + ankh_plan_energy_sources_v1 per step"}
 
+        # one-shot with the precompute included (the reference rebuilds it per
+        # call, fmm.cpp:397-409): a fresh plan per step, host buffers in,
+        # energies out; SURVEY.md §8d asks for evals/s both ways
+        if world == 1:
+            def cold_step():
+                p_ = ankh.Plan(n, rb, ecfg, threads=0, device=local, phase_timing=False)
+                e = p_.energy(hpos, hsrc).e_total
+                p_.close()
+                return e
+
+            cold_step()
+            torch.cuda.synchronize()
+            k3 = 3
+            t0 = time.perf_counter()
+            for _ in range(k3):
+                cold_step()
+            t_cold = time.perf_counter() - t0
+            e2e_cold = {"value": k3 / t_cold, "unit": "evals/s", "h2d_bytes_per_step": int(pos.nbytes + src.nbytes),
+                        "d2h_bytes_per_step": 72, "steps": k3,
+                        "api": "Plan(...) + energy(host buffers) + close per step: geometry, M2L factors "
+                               "(GPU Jacobi SVD), instance lists and periodic spectrum rebuilt every step"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(args, pos, src, rb, L)
@@ -450,6 +476,7 @@ def main():
                              "algorithmic": "sum over instances 4kK+2k flop"},
             "e2e": e2e,
             "e2e_fixed_positions": e2e_fixed,
+            "e2e_including_precompute": e2e_cold,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
