@@ -183,12 +183,19 @@ __global__ void __launch_bounds__(256) k_gather_sorted(const double* __restrict_
 
 // The moment half of validate_system (types.cpp:16-63) and the self-energy
 // partials for the bound-positions path (same block layout as k_bin).
+// Streamed host path: particles [block0 256, n) of one arrived chunk, and each
+// particle's record scattered to its sorted slot inv[i].
 __global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ src, std::size_t n,
                                                    double c_mu, double c_th,
                                                    double* __restrict__ self_partial,
-                                                   DevResult* res) {
+                                                   DevResult* res, unsigned block0,
+                                                   const double* __restrict__ pos,
+                                                   const unsigned* __restrict__ inv,
+                                                   double* __restrict__ part) {
   __shared__ double red[8];
-  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  const unsigned blk = block0 + blockIdx.x;
+  const std::size_t i = static_cast<std::size_t>(blk) * 256 + threadIdx.x;
+  if (inv && i < n) write_record(pos, src, static_cast<unsigned>(i), part + static_cast<std::size_t>(inv[i]) * kRec);
   double acc = 0.0;
   bool mp = false;
   if (i < n) {
@@ -218,8 +225,78 @@ __global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ sr
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) t += red[w];
-    self_partial[blockIdx.x] = t;
+    self_partial[blk] = t;
   }
+}
+
+// inv[sorted[j]] = j: the sorted slot of every particle
+__global__ void k_inverse(const unsigned* __restrict__ sorted, std::size_t n, unsigned* __restrict__ inv) {
+  const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (j < n) inv[sorted[j]] = static_cast<unsigned>(j);
+}
+
+// Streamed host path, per Morton leaf m: the chunk after which its records
+// are complete (its largest particle index -- leaves hold ascending indices)
+// and the chunk after which its 13 half-shell neighbours are too (P2P's
+// source set, k_p2p); counts per chunk in cnt[0..C) (P2M) / cnt[C..2C) (P2P).
+__global__ void k_stream_ready(const unsigned* __restrict__ offsets, const unsigned* __restrict__ sorted,
+                               int depth, int periodic, unsigned chunk, int n_chunks,
+                               unsigned char* __restrict__ ready, unsigned* __restrict__ cnt) {
+  const unsigned m = blockIdx.x * 256 + threadIdx.x;
+  const int n = 1 << depth;
+  if (m >= static_cast<unsigned>(n) * n * n) return;
+  const int ax = static_cast<int>(morton_compact3(m >> 2)), ay = static_cast<int>(morton_compact3(m >> 1)),
+            az = static_cast<int>(morton_compact3(m));
+  auto leaf_ready = [&](int x, int y, int z) -> int {
+    const unsigned b = static_cast<unsigned>((x * n + y) * n + z);
+    const unsigned e = offsets[b + 1];
+    return e > offsets[b] ? static_cast<int>(sorted[e - 1] / chunk) : 0;
+  };
+  const int r = leaf_ready(ax, ay, az);
+  int p = r;
+  for (int d = 0; d < 13; ++d) {  // the 13 lex-positive directions, as k_p2p
+    const int dx = d < 4 ? 0 : 1;
+    const int dy = d == 0 ? 0 : (d < 4 ? 1 : (d - 4) / 3 - 1);
+    const int dz = d == 0 ? 1 : (d < 4 ? d - 2 : (d - 4) % 3 - 1);
+    int e[3] = {ax + dx, ay + dy, az + dz};
+    bool ok = true;
+    for (int k = 0; k < 3; ++k) {
+      if (e[k] < 0 || e[k] >= n) {
+        if (!periodic) ok = false;
+        e[k] = ((e[k] % n) + n) % n;
+      }
+    }
+    if (ok) p = max(p, leaf_ready(e[0], e[1], e[2]));
+  }
+  ready[2 * m] = static_cast<unsigned char>(r);
+  ready[2 * m + 1] = static_cast<unsigned char>(p);
+  atomicAdd(&cnt[r], 1u);
+  atomicAdd(&cnt[n_chunks + p], 1u);
+}
+
+// bounds[0..C] / bounds[C+1..2C+1]: exclusive scans of the two count sets;
+// cursors reset to the bucket starts
+__global__ void k_stream_scan(const unsigned* __restrict__ cnt, int n_chunks, unsigned* __restrict__ bounds,
+                              unsigned* __restrict__ cursor) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int s = 0; s < 2; ++s) {
+    unsigned acc = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      bounds[s * (n_chunks + 1) + c] = acc;
+      cursor[s * n_chunks + c] = acc;
+      acc += cnt[s * n_chunks + c];
+    }
+    bounds[s * (n_chunks + 1) + n_chunks] = acc;
+  }
+}
+
+__global__ void k_stream_lists(const unsigned char* __restrict__ ready, unsigned n_leaves, int n_chunks,
+                               unsigned* __restrict__ cursor, unsigned* __restrict__ list_p2m,
+                               unsigned* __restrict__ list_p2p) {
+  const unsigned m = blockIdx.x * 256 + threadIdx.x;
+  if (m >= n_leaves) return;
+  list_p2m[atomicAdd(&cursor[ready[2 * m]], 1u)] = m;
+  list_p2p[atomicAdd(&cursor[n_chunks + ready[2 * m + 1]], 1u)] = m;
 }
 
 __global__ void k_init_result(DevResult* res) {
@@ -290,8 +367,32 @@ void launch_src_gather(const double* pos, const double* src, const unsigned* sor
   if (n == 0) return;
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
   k_src_check<<<blocks, 256, 0, st>>>(src, n, 2.0 * xi * xi / 3.0, 8.0 * xi * xi * xi * xi / 5.0,
-                                      self_partial, res);
+                                      self_partial, res, 0u, nullptr, nullptr, nullptr);
   k_gather_sorted<<<blocks, 256, 0, st>>>(pos, src, sorted, n, part);
+}
+
+void launch_src_chunk(const double* pos, const double* src, const unsigned* inv, std::size_t i0,
+                      std::size_t i1, double xi, double* self_partial, DevResult* res, double* part,
+                      cudaStream_t st) {
+  if (i1 <= i0) return;  // i0 is a multiple of 256 (k_bin's self-partial blocks)
+  const unsigned blocks = static_cast<unsigned>((i1 - i0 + 255) / 256);
+  k_src_check<<<blocks, 256, 0, st>>>(src, i1, 2.0 * xi * xi / 3.0, 8.0 * xi * xi * xi * xi / 5.0,
+                                      self_partial, res, static_cast<unsigned>(i0 / 256), pos, inv,
+                                      part);
+}
+
+void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,
+                           int periodic, unsigned chunk, int n_chunks, unsigned* inv,
+                           unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
+                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st) {
+  const unsigned n_leaves = 1u << (3 * depth);
+  if (n > 0) k_inverse<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(sorted, n, inv);
+  cudaMemsetAsync(cnt, 0, 2 * n_chunks * sizeof(unsigned), st);
+  k_stream_ready<<<(n_leaves + 255) / 256, 256, 0, st>>>(offsets, sorted, depth, periodic, chunk,
+                                                        n_chunks, ready, cnt);
+  k_stream_scan<<<1, 32, 0, st>>>(cnt, n_chunks, bounds, cursor);
+  k_stream_lists<<<(n_leaves + 255) / 256, 256, 0, st>>>(ready, n_leaves, n_chunks, cursor, list_p2m,
+                                                        list_p2p);
 }
 
 std::size_t sort_temp_bytes(std::size_t n, int n_leaves) {

@@ -54,7 +54,9 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
                                                        int depth, double rb,
                                                        const double* __restrict__ hd_g,
                                                        double* __restrict__ exp_leaf,
-                                                       unsigned m_begin, unsigned m_end) {
+                                                       unsigned m_begin, unsigned m_end,
+                                                       const unsigned* __restrict__ list,
+                                                       const unsigned* __restrict__ bounds) {
   using Sh = P2MWShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER, KS = exp_stride(K);
   extern __shared__ double sm[];
@@ -65,8 +67,16 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
   (void)hd_g;
   const int n = 1 << depth;
   // leaves are visited (and their expansions stored) in Morton order
-  const unsigned m = m_begin + blockIdx.x * kP2MWarps + warp;
-  if (m >= m_end) return;
+  // list mode (streamed host path): the leaves list[bounds[0] .. bounds[1])
+  const unsigned item = blockIdx.x * kP2MWarps + warp;
+  unsigned m;
+  if (list) {
+    if (item >= bounds[1] - bounds[0]) return;
+    m = list[bounds[0] + item];
+  } else {
+    m = m_begin + item;
+    if (m >= m_end) return;
+  }
   const int ci0 = static_cast<int>(morton_compact3(m >> 2)),
             ci1 = static_cast<int>(morton_compact3(m >> 1)), ci2 = static_cast<int>(morton_compact3(m));
   const unsigned leaf = (static_cast<unsigned>(ci0) * n + ci1) * n + ci2;
@@ -389,10 +399,12 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
 template <int L>
 void p2m_order(const double* part, const unsigned* leaf_off, int depth, double rb,
                const double* hd, double* exp_leaf, const DevResult* res, unsigned m_begin,
-               unsigned m_end, cudaStream_t st) {
-  if (m_end <= m_begin) return;
-  const unsigned leaves = m_end - m_begin;
+               unsigned m_end, const unsigned* list, const unsigned* bounds, unsigned list_count,
+               cudaStream_t st) {
+  const unsigned leaves = list ? list_count : (m_end > m_begin ? m_end - m_begin : 0u);
+  if (leaves == 0) return;
   if (L > 6) {  // register budget of the warp-per-leaf variant: block-per-leaf instead
+    if (list) return;  // (no list mode: the plan streams only for L <= 6)
     const std::size_t smem = sizeof(double) * P2MShape<L>::smem_doubles;
     static bool attr_b = false;
     if (!attr_b) {
@@ -413,7 +425,7 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
     attr = true;
   }
   k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(
-      part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end);
+      part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end, list, bounds);
 }
 
 }  // namespace
@@ -460,9 +472,11 @@ void m2m_order(const double* child, double* parent, int parent_level, const doub
 
 void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
                 double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
-                unsigned m_begin, unsigned m_end, cudaStream_t st) {
+                unsigned m_begin, unsigned m_end, cudaStream_t st, const unsigned* list,
+                const unsigned* bounds, unsigned list_count) {
 #define ANKH_P2M(N) \
-  p2m_order<N>(part, leaf_off, depth, box_radius, hd, exp_leaf, res, m_begin, m_end, st)
+  p2m_order<N>(part, leaf_off, depth, box_radius, hd, exp_leaf, res, m_begin, m_end, list, bounds, \
+               list_count, st)
   ANKH_ORDER_SWITCH(order, ANKH_P2M)
 #undef ANKH_P2M
 }

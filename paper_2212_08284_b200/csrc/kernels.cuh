@@ -84,9 +84,24 @@ void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, un
                  const unsigned* counts, unsigned* offsets, int n_leaves, cudaStream_t st);
 /// hd[n] = H D^n, n = 0..2 (3 x L x L, host order) into the P2M constant bank.
 void upload_p2m_basis(int order, const double* hd, cudaStream_t st);
+// list != nullptr (L <= 6 only): the leaves list[bounds[0] .. bounds[1]),
+// list_count of them (streamed host path)
 void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
                 double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
-                unsigned m_begin, unsigned m_end, cudaStream_t st);
+                unsigned m_begin, unsigned m_end, cudaStream_t st, const unsigned* list = nullptr,
+                const unsigned* bounds = nullptr, unsigned list_count = 0);
+// streamed host path (k_bin.cu): one arrived chunk [i0, i1) of the moments --
+// validation, self-energy partials, records scattered to their sorted slots
+void launch_src_chunk(const double* pos, const double* src, const unsigned* inv, std::size_t i0,
+                      std::size_t i1, double xi, double* self_partial, DevResult* res, double* part,
+                      cudaStream_t st);
+// inverse permutation, per-leaf readiness chunk (P2M: own records; P2P: + the
+// 13 half-shell neighbours), per-chunk leaf lists and their bounds
+// (bounds[0..C] P2M, bounds[C+1..2C+1] P2P)
+void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,
+                           int periodic, unsigned chunk, int n_chunks, unsigned* inv,
+                           unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
+                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st);
 void launch_m2m(const double* child, double* parent, int parent_level, int order,
                 const double* m2m, cudaStream_t st);
 void launch_m2l(const double* exp, const long long* level_off, const double* factors,
@@ -105,10 +120,14 @@ struct P2PRadial {
 /// pipe = 1: persistent CTAs fed by a bulk-copy ring, dynamic leaf
 /// scheduling, near_partial[leaf * p2p_pipe_warps(256) + warp].  Returns the
 /// number of near partials written.
+// list != nullptr: the target leaves are list[bounds[0] .. bounds[1]) (Morton
+// indices, list_grid of them -- the host knows the count), partials still
+// indexed by leaf - leaf_begin (streamed host path)
 int launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
                double period, double xi, const P2PRadial& rad, int cap, int pipe, int leaf_begin,
                int leaf_end, double* near_partial, unsigned long long* pair_count, DevResult* res,
-               cudaStream_t st);
+               cudaStream_t st, const unsigned* list = nullptr, const unsigned* bounds = nullptr,
+               int list_grid = 0);
 int p2p_pipe_warps(int tpb);
 int p2p_pipe_max_cap();
 int p2p_max_cap();

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstddef>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <set>
 
@@ -114,16 +115,31 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
 }
 
 Plan::~Plan() {
-  if (stream_) cudaStreamSynchronize(stream_);
-  if (last_stream_) cudaStreamSynchronize(last_stream_);
+  for (cudaStream_t s : {stream_, last_stream_, side_stream_, copy_stream_, gather_stream_})
+    if (s) cudaStreamSynchronize(s);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_src_exec_) cudaGraphExecDestroy(graph_src_exec_);
-  for (void* p : allocs_) cudaFree(p);
+  for (void* p : allocs_) cudaFreeAsync(p, stream_);  // back to the pool (kept for the next plan)
+  if (stream_) cudaStreamSynchronize(stream_);
   if (h_res_) cudaFreeHost(h_res_);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  for (cudaStream_t s : {copy_stream_, gather_stream_})
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  for (cudaEvent_t e : {ev_s_start_, ev_s_pos_, ev_s_sorted_})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_t_)
+    if (e) cudaEventDestroy(e);
+  for (int c = 0; c < kMaxStreamChunks; ++c) {
+    if (ev_s_chunk_[c]) cudaEventDestroy(ev_s_chunk_[c]);
+    if (ev_s_gath_[c]) cudaEventDestroy(ev_s_gath_[c]);
+  }
+  if (h_sbounds_) cudaFreeHost(h_sbounds_);
   if (side_stream_) {
     cudaStreamSynchronize(side_stream_);
     cudaStreamDestroy(side_stream_);
@@ -131,10 +147,28 @@ Plan::~Plan() {
   if (stream_) cudaStreamDestroy(stream_);
 }
 
+// Plan buffers come from the device's stream-ordered pool, kept by the pool
+// when a plan is destroyed (release threshold raised once per device): the
+// next plan -- e.g. a one-shot call for another system size -- reuses that
+// memory instead of mapping gigabytes anew (cudaMalloc / cudaFree of the
+// plan's buffers took 0.03-0.9 s per build / close, erratically).
 void* Plan::dalloc(std::size_t bytes) {
+  static std::mutex mu;
+  static std::vector<int> pooled;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(pooled.begin(), pooled.end(), device_) == pooled.end()) {
+      cudaMemPool_t pool = nullptr;
+      if (cudaDeviceGetDefaultMemPool(&pool, device_) == cudaSuccess) {
+        unsigned long long keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pooled.push_back(device_);
+    }
+  }
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
-  ANKH_CUDA(cudaMalloc(&p, bytes));
+  ANKH_CUDA(cudaMallocAsync(&p, bytes, stream_));
   allocs_.push_back(p);
   device_bytes += bytes;
   return p;
@@ -765,7 +799,8 @@ void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
   if (!st) st = stream_;
   last_stream_ = st;
   evaluated_ = true;
-  bound_ = false;  // a full evaluation re-bins: bound positions are superseded
+  streamed_last_ = false;
+  bound_ = stream_bound_ = false;  // a full evaluation re-bins: bound positions are superseded
   if (n == 0) return;
   if (pending_code_ != 0) {
     validate_only(d_pos, d_src, st);
@@ -814,8 +849,200 @@ void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
   launch_all(d_pos, d_src, st);
 }
 
+bool Plan::stream_eligible() const {
+  const char* e = std::getenv("ANKH_STREAM_INPUT");  // "0": never, "1": any size
+  if (e && e[0] == '0') return false;
+  const std::size_t min_n = (e && e[0] == '1') ? 1 : 65536;
+  return n >= min_n && cfg.world <= 1 && !shard_upward_ && !coll_ && !csr_only_ &&
+         pending_code_ == 0 && L <= 6 && p2p_pipe_ == 0;
+}
+
+void Plan::stream_setup() {
+  if (stream_init_) return;
+  {
+    if (const char* c = std::getenv("ANKH_STREAM_CHUNKS")) stream_chunks_ = std::atoi(c);
+    stream_chunks_ = std::max(1, std::min(stream_chunks_, kMaxStreamChunks));
+    d_inv_ = static_cast<unsigned*>(dalloc(n * sizeof(unsigned)));
+    d_ready_ = static_cast<unsigned char*>(dalloc(2 * static_cast<std::size_t>(n_leaves)));
+    d_scnt_ = static_cast<unsigned*>(dalloc(2 * kMaxStreamChunks * sizeof(unsigned)));
+    d_scursor_ = static_cast<unsigned*>(dalloc(2 * kMaxStreamChunks * sizeof(unsigned)));
+    d_sbounds_ = static_cast<unsigned*>(dalloc(2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
+    d_list_p2m_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
+    d_list_p2p_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
+    ANKH_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_sbounds_), 2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
+    ANKH_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    ANKH_CUDA(cudaStreamCreateWithFlags(&gather_stream_, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ev_s_start_, &ev_s_pos_, &ev_s_sorted_})
+      ANKH_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (int c = 0; c < kMaxStreamChunks; ++c) {
+      ANKH_CUDA(cudaEventCreateWithFlags(&ev_s_chunk_[c], cudaEventDisableTiming));
+      ANKH_CUDA(cudaEventCreateWithFlags(&ev_s_gath_[c], cudaEventDisableTiming));
+    }
+    for (auto& e : ev_t_) ANKH_CUDA(cudaEventCreate(&e));
+    ANKH_CUDA(cudaStreamSynchronize(stream_));  // pool allocations complete before other streams use them
+    stream_init_ = true;
+  }
+}
+
+// positions half of the streamed path: validation, binning, per-leaf sort
+// (build_tree, as set_positions) and the per-chunk leaf lists; their bounds
+// land in h_sbounds_ (pinned) once `ev_s_sorted_` completes
+void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C) {
+  ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
+  launch_init_result(res, st);
+  const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
+  launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_, d_self_part_, res, st);
+  launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_, d_off_, d_keys2_,
+                       d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
+  launch_stream_prepare(d_off_, d_idx2_, n, depth, periodic ? 1 : 0, static_cast<unsigned>(chunk), C, d_inv_,
+                        d_ready_, d_scnt_, d_sbounds_, d_scursor_, d_list_p2m_, d_list_p2p_, st);
+  ANKH_CUDA(cudaMemcpyAsync(h_sbounds_, d_sbounds_, 2 * (C + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+}
+
+std::size_t Plan::stream_chunk_size() const {
+  // chunks of whole 256-particle blocks (k_bin's self-energy partial layout)
+  return ((n + stream_chunks_ - 1) / stream_chunks_ + 255) / 256 * 256;
+}
+
+void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream_t st) {
+  // ANKH_STREAM_TRACE=1: stage timestamps (ms after the call) on stderr
+  const bool trace = std::getenv("ANKH_STREAM_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  auto mark = [&](const std::string& what, cudaStream_t s) {
+    if (!trace) return;
+    cudaEvent_t e = nullptr;
+    ANKH_CUDA(cudaEventCreate(&e));
+    ANKH_CUDA(cudaEventRecord(e, s));
+    marks.emplace_back(what, e);
+  };
+  // h_pos == nullptr: positions bound by set_positions (flags in d_res_pos_,
+  // sorted order and per-chunk lists already built) -- stream the moments only
+  const bool bound_pos = h_pos == nullptr;
+  last_stream_ = st;
+  evaluated_ = true;
+  if (!bound_pos) bound_ = stream_bound_ = false;
+  streamed_last_ = true;
+  const bool timing = cfg.phase_timing != 0;
+  stream_setup();
+  const std::size_t chunk = stream_chunk_size();
+  const int C = static_cast<int>((n + chunk - 1) / chunk);
+  // copies: positions, then the moment chunks (after the previous evaluation)
+  ANKH_CUDA(cudaEventRecord(ev_s_start_, st));
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[0], st));
+  mark("start", st);
+  ANKH_CUDA(cudaStreamWaitEvent(copy_stream_, ev_s_start_, 0));
+  if (!bound_pos) {
+    ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, copy_stream_));
+    ANKH_CUDA(cudaEventRecord(ev_s_pos_, copy_stream_));
+    mark("copy positions done", copy_stream_);
+  }
+  for (int c = 0; c < C; ++c) {
+    const std::size_t i0 = c * chunk, i1 = std::min(n, i0 + chunk);
+    ANKH_CUDA(cudaMemcpyAsync(d_src_ + 10 * i0, h_src + 10 * i0, (i1 - i0) * 10 * sizeof(double),
+                              cudaMemcpyHostToDevice, copy_stream_));
+    ANKH_CUDA(cudaEventRecord(ev_s_chunk_[c], copy_stream_));
+    mark("copy chunk " + std::to_string(c), copy_stream_);
+  }
+  if (!bound_pos) {
+    ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_pos_, 0));
+    stream_positions(st, d_res_, chunk, C);
+  } else {
+    ANKH_CUDA(cudaMemcpyAsync(d_res_, d_res_pos_, sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
+  }
+  ANKH_CUDA(cudaEventRecord(ev_s_sorted_, st));
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[1], st));
+  mark("sorted + lists", st);
+  ANKH_CUDA(cudaGetLastError());
+  if (!bound_pos) ANKH_CUDA(cudaEventSynchronize(ev_s_sorted_));  // per-chunk leaf counts -> exact grids
+  std::uint32_t launches = 9;
+  // per chunk: records (gather stream), P2M (far stream), P2P (this stream)
+  ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_sorted_, 0));
+  ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_sorted_, 0));
+  const bool do_periodic = periodic && include_self_;
+  int n_near_parts = leaf_end_ - leaf_begin_;
+  bool near_started = false;
+  for (int c = 0; c < C; ++c) {
+    const std::size_t i0 = c * chunk, i1 = std::min(n, i0 + chunk);
+    ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_chunk_[c], 0));
+    launch_src_chunk(d_pos_, d_src_, d_inv_, i0, i1, cfg.xi, d_self_part_, d_res_, d_part_, gather_stream_);
+    ANKH_CUDA(cudaEventRecord(ev_s_gath_[c], gather_stream_));
+    mark("gather " + std::to_string(c), gather_stream_);
+    const unsigned n_m = h_sbounds_[c + 1] - h_sbounds_[c];
+    const unsigned n_p = h_sbounds_[C + 1 + c + 1] - h_sbounds_[C + 1 + c];
+    if (n_m) {
+      ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[c], 0));
+      launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, 0u, 0u, side_stream_,
+                 d_list_p2m_, d_sbounds_ + c, n_m);
+      ++launches;
+      mark("p2m " + std::to_string(c) + " (" + std::to_string(n_m) + " leaves)", side_stream_);
+    }
+    if (n_p) {
+      ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[c], 0));
+      if (timing && !near_started) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
+      near_started = true;
+      n_near_parts = launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, p2p_cap_, 0,
+                                leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, st, d_list_p2p_,
+                                d_sbounds_ + (C + 1) + c, static_cast<int>(n_p));
+      ++launches;
+      mark("p2p " + std::to_string(c) + " (" + std::to_string(n_p) + " leaves)", st);
+    }
+    launches += 1;
+  }
+  // the last chunk's records are in before the tail (far stream waits below)
+  ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[C - 1], 0));
+  ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[C - 1], 0));
+  if (timing) {
+    if (!near_started) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
+    ANKH_CUDA(cudaEventRecord(ev_t_[3], st));
+  }
+  for (int l = depth - 1; l >= 0; --l) {
+    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, side_stream_);
+    ++launches;
+  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[4], side_stream_));
+  for (int c = 1; c <= kMaxKp8; ++c) {
+    const auto r = class_range_[c];
+    if (r.second == 0) continue;
+    launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c, d_tile_ids_ + r.first, d_inst_, K,
+               Kp, d_far_part_, side_stream_);
+    ++launches;
+  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[5], side_stream_));
+  if (do_periodic) {
+    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, side_stream_);
+    ++launches;
+  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[6], side_stream_));
+  mark("far chain (m2m, m2l, periodic)", side_stream_);
+  ANKH_CUDA(cudaEventRecord(ev_join_, side_stream_));
+  ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[7], st));
+  launch_finalize(d_near_part_, n_near_parts, d_pair_count_, leaf_end_ - leaf_begin_, d_far_part_, n_tiles_,
+                  d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
+                  include_self_ ? 1 : 0, d_fin_scratch_, d_res_, st);
+  launches += 2;
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[8], st));
+  ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+  mark("finalize + result copy", st);
+  ANKH_CUDA(cudaGetLastError());
+  launches_ = launches;
+  if (trace) {
+    ANKH_CUDA(cudaStreamSynchronize(st));
+    for (auto& m : marks) {
+      float ms = 0.f;
+      ANKH_CUDA(cudaEventElapsedTime(&ms, marks[0].second, m.second));
+      std::fprintf(stderr, "[ankh stream] %8.3f ms  %s\n", ms, m.first.c_str());
+    }
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+}
+
 void Plan::enqueue_host(const double* h_pos, const double* h_src, cudaStream_t st) {
   if (!st) st = stream_;
+  if (stream_eligible()) {
+    enqueue_streamed(h_pos, h_src, st);
+    return;
+  }
   if (n > 0) {
     ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
     ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -825,9 +1052,18 @@ void Plan::enqueue_host(const double* h_pos, const double* h_src, cudaStream_t s
 
 void Plan::set_positions(const double* h_pos, cudaStream_t st) {
   if (!st) st = stream_;
-  bound_ = false;
+  bound_ = stream_bound_ = false;
   if (n == 0) {
     bound_ = true;
+    return;
+  }
+  if (stream_eligible()) {  // energy_sources will stream the moments chunk by chunk
+    stream_setup();
+    const std::size_t chunk = stream_chunk_size();
+    ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    stream_positions(st, d_res_pos_, chunk, static_cast<int>((n + chunk - 1) / chunk));
+    ANKH_CUDA(cudaStreamSynchronize(st));
+    bound_ = stream_bound_ = true;
     return;
   }
   ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -847,8 +1083,13 @@ void Plan::set_positions(const double* h_pos, cudaStream_t st) {
 void Plan::enqueue_sources(const double* h_src, cudaStream_t st) {
   if (!bound_) throw AnkhError(ANKH_RUNTIME_ERROR, "plan positions are not set (ankh_plan_set_positions_v1)");
   if (!st) st = stream_;
+  if (stream_bound_ && stream_eligible()) {
+    enqueue_streamed(nullptr, h_src, st);
+    return;
+  }
   last_stream_ = st;
   evaluated_ = true;
+  streamed_last_ = false;
   if (n == 0) return;
   ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
   if (pending_code_ != 0) {
@@ -923,7 +1164,23 @@ void Plan::result(ankh_report_v1* out) {
     out->far_instances = m2l_instances;
     out->far_flops = far_flops;
   }
-  if (cfg.phase_timing) {
+  if (cfg.phase_timing && streamed_last_) {
+    // overlapped phases: wall-clock span of each (they may sum to more than
+    // the total); interpolation = chunk gathers + P2M + M2M, precompute =
+    // the positions copy, binning and sort
+    auto span = [&](int a, int b) {
+      float ms = 0.f;
+      ANKH_CUDA(cudaEventElapsedTime(&ms, ev_t_[a], ev_t_[b]));
+      return ms * 1e-3;
+    };
+    out->t_precompute = span(0, 1);
+    out->t_interpolation = span(1, 4);
+    out->t_far_field = span(4, 5);
+    out->t_near_field = span(2, 3);
+    out->t_periodic_far = span(5, 6);
+    out->t_self = span(7, 8);
+    out->t_total = span(0, 8);
+  } else if (cfg.phase_timing) {
     float ms[6];
     for (int i = 0; i < 6; ++i) ANKH_CUDA(cudaEventElapsedTime(&ms[i], ev_[i], ev_[i + 1]));
     out->t_precompute = ms[0] * 1e-3;
@@ -963,6 +1220,7 @@ void Plan::expansions(double* out, std::size_t count) {
 }
 
 void Plan::enqueue_phase(int phase, const double* d_pos, const double* d_src, cudaStream_t st) {
+  streamed_last_ = false;
   if (!st) st = stream_;
   last_stream_ = st;
   bound_ = false;

@@ -124,6 +124,29 @@ class Plan {
   // mode 0: full evaluation; 1 / 2: halves around a caller-driven shard
   // exchange; 3: moments only (positions bound by set_positions)
   void launch_all(const double* d_pos, const double* d_src, cudaStream_t st, int mode = 0);
+  // Streamed host path (enqueue_host, one GPU, L <= 6): positions first, then
+  // the moments in chunks on a copy stream; each chunk's records are scattered
+  // to their sorted slots as it lands, and P2M / P2P run on the leaves whose
+  // records (P2P: and those of their 13 half-shell neighbours) are complete,
+  // so the PCIe copy overlaps the evaluation.  Bit-identical to enqueue().
+  bool stream_eligible() const;
+  void stream_setup();
+  std::size_t stream_chunk_size() const;
+  void stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C);
+  void enqueue_streamed(const double* h_pos, const double* h_src, cudaStream_t st);
+  bool stream_bound_ = false;  // set_positions built the streamed path's lists
+  static constexpr int kMaxStreamChunks = 32;
+  int stream_chunks_ = 8;
+  bool stream_init_ = false;
+  unsigned *d_inv_ = nullptr, *d_scnt_ = nullptr, *d_sbounds_ = nullptr, *d_scursor_ = nullptr;
+  unsigned *d_list_p2m_ = nullptr, *d_list_p2p_ = nullptr, *h_sbounds_ = nullptr;
+  unsigned char* d_ready_ = nullptr;
+  cudaStream_t copy_stream_ = nullptr, gather_stream_ = nullptr;
+  cudaEvent_t ev_s_start_ = nullptr, ev_s_pos_ = nullptr, ev_s_sorted_ = nullptr;
+  cudaEvent_t ev_s_chunk_[kMaxStreamChunks] = {}, ev_s_gath_[kMaxStreamChunks] = {};
+  // phase spans of a streamed evaluation (phases overlap: start/end per phase)
+  cudaEvent_t ev_t_[9] = {};
+  bool streamed_last_ = false;
   void validate_only(const double* d_pos, const double* d_src, cudaStream_t st);
   void exchange_leaves(cudaStream_t st);
 

@@ -248,6 +248,75 @@ def test_gpu_instances_match_host_enumeration(cuda, p, world, monkeypatch):
             assert (a.e_far, a.e_total) == (b.e_far, b.e_total)
 
 
+def _stream_systems():
+    pos, src, rb, _ = inputs.make_config(1)  # 24,000 atoms in lattice (spatially coherent) order
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(pos.shape[0])
+    charges = src.copy()
+    charges[:, 1:] = 0.0
+    mixed = src.copy()
+    mixed[::3, 1:] = 0.0
+    opos, osrc = inputs.random_system(6000, 7.0, seed=8, multipoles=True)
+    return {"coherent": (pos, src, rb, 15), "shuffled": (pos[perm], src[perm], rb, 15),
+            "charges": (pos, charges, rb, 15), "mixed": (pos, mixed, rb, 15), "open": (opos, osrc, 7.0, 0)}
+
+
+@pytest.mark.parametrize("case", ["coherent", "shuffled", "charges", "mixed", "open"])
+def test_streamed_host_path_bitwise(cuda, case, monkeypatch):
+    """Host inputs through the streamed path (moments copied in chunks, each
+    chunk's leaves evaluated as their records complete) give bit-identical
+    reports to the copy-then-evaluate path, for any chunk count and input
+    order, on repeated calls with new moments, and with bound positions
+    (set_positions once, energy_sources streams the moments)."""
+    pos, src, rb, p = _stream_systems()[case]
+    n = pos.shape[0]
+    cfg = ankh.EwaldConfig(order_cheb=4, order_equi=4, p=p)
+    src2 = src * 1.07
+    monkeypatch.setenv("ANKH_STREAM_INPUT", "0")
+    plain = ankh.Plan(n, rb, cfg)
+    want = [plain.energy(pos, src), plain.energy(pos, src2)]
+    monkeypatch.setenv("ANKH_STREAM_INPUT", "1")
+    for chunks in (1, 3, 8, 32):
+        monkeypatch.setenv("ANKH_STREAM_CHUNKS", str(chunks))
+        sp = ankh.Plan(n, rb, cfg)
+        key = lambda r: (r.e_total, r.e_self, r.e_near, r.e_far, r.e_periodic_far, r.near_pairs)
+        for w, s_ in zip(want, (src, src2)):
+            assert key(sp.energy(pos, s_)) == key(w), (case, chunks)
+        # bound positions: only the moments stream on each call
+        sp.set_positions(pos)
+        for w, s_ in zip(want, (src, src2, src)):
+            assert key(sp.energy_sources(s_)) == key(w), (case, chunks, "bound")
+        sp.close()
+
+
+def test_streamed_host_path_errors(cuda, monkeypatch):
+    """Invalid inputs report the same first violation through the streamed
+    path (moments validated chunk by chunk) as through the plain path."""
+    pos, src, rb, _ = inputs.make_config(1)
+    n = pos.shape[0]
+    cfg = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    cases = []
+    s1 = src.copy(); s1[n - 1, 7] = np.nan; cases.append((pos, s1))              # moment, last chunk
+    p2 = pos.copy(); p2[n - 2, 0] = 2.0 * rb; s2 = src.copy(); s2[n - 1, 0] = np.inf
+    cases.append((p2, s2))                                                       # outside box before a bad moment
+    p3 = pos.copy(); p3[17] = p3[16]; cases.append((p3, src))                      # exact duplicate
+    s4 = src.copy(); s4[40, 3] = np.nan; p4 = pos.copy(); p4[40, 1] = 2.0 * rb
+    cases.append((p4, s4))                                                       # same particle: non-finite wins
+    msgs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ANKH_STREAM_INPUT", mode)
+        plan = ankh.Plan(n, rb, cfg)
+        out = []
+        for pp, ss in cases:
+            with pytest.raises(Exception) as ei:
+                plan.energy(pp, ss)
+            out.append((type(ei.value).__name__, str(ei.value)))
+        ok = plan.energy(pos, src)  # the plan stays usable
+        assert np.isfinite(ok.e_total)
+        msgs[mode] = out
+    assert msgs["0"] == msgs["1"], msgs
+
+
 def test_deterministic_and_device_path(cuda):
     torch = cuda
     pos, src, rb, cfg = inputs.make_config(1)
