@@ -173,6 +173,12 @@ int ankh_plan_leaf_level_v1(ankh_plan_v1* plan, double** d_leaf_level, int64_t* 
                             int64_t* row_end, int* row_stride);
 int ankh_device_copy_v1(void* dst, const void* src, size_t bytes, void* stream, char* err,
                         size_t errlen);
+/* (c) Diagnostics on a one-GPU box: a loopback "collective" that lands the
+ *     leaf-level all-gather's bytes with device copies and makes the
+ *     all-reduce the identity, so one shard's complete evaluation (with the
+ *     exchange in its CUDA graph and P2P concurrent with the far chain) can be
+ *     timed.  Energies are this shard's partials. */
+int ankh_plan_attach_loopback_v1(ankh_plan_v1* plan, char* err, size_t errlen);
 
 /* ---- spatial sharding (host only; no device needed) ----
  * Shards own contiguous Morton ranges of leaves; a level-l cell belongs to the

@@ -386,6 +386,13 @@ class Plan:
         err = ctypes.create_string_buffer(512)
         _check(lib().ankh_plan_attach_nccl_v1(self._h, unique_id, err, 512), err)
 
+    def attach_loopback(self) -> None:
+        """Diagnostics on one GPU: stand-in exchange (device copies for the
+        leaf all-gather, identity all-reduce) so one shard's whole evaluation
+        can be timed; reports then carry this shard's partial sums."""
+        err = ctypes.create_string_buffer(512)
+        _check(lib().ankh_plan_attach_loopback_v1(self._h, err, 512), err)
+
     def enqueue_phase(self, phase: int, positions, sources, stream: int = 0) -> None:
         """Caller-driven shard exchange: phase 1 = binning..this shard's P2M,
         phase 2 = M2M..final reduction (after the leaf level is completed)."""

@@ -285,6 +285,15 @@ int ankh_plan_attach_nccl_v1(ankh_plan_v1* plan, const unsigned char* id128, cha
   });
 }
 
+int ankh_plan_attach_loopback_v1(ankh_plan_v1* plan, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    const ankh_config_v1& c = plan->plan->cfg;
+    plan->plan->attach_collective(ankh_b200::make_loopback_collective(c.rank, c.world));
+  });
+}
+
 int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* begin, int64_t* end) {
   if (depth < 1 || depth > 8 || world < 1 || rank < 0 || rank >= world || !begin || !end)
     return ANKH_INVALID_ARGUMENT;

@@ -99,4 +99,30 @@ Collective* make_nccl_collective(const unsigned char id[128], int rank, int worl
   return new NcclCollective(id, rank, world);
 }
 
+namespace {
+
+class LoopbackCollective final : public Collective {
+ public:
+  LoopbackCollective(int rank, int world) : rank_(rank), world_(world) {}
+  void allgather_inplace(double* recv, std::size_t count, cudaStream_t st) override {
+    const double* own = recv + static_cast<std::size_t>(rank_) * count;
+    for (int r = 0; r < world_; ++r)
+      if (r != rank_)
+        ANKH_CUDA(cudaMemcpyAsync(recv + static_cast<std::size_t>(r) * count, own,
+                                  count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  void allreduce_sum(double*, std::size_t, cudaStream_t) override {}
+  int rank() const override { return rank_; }
+  int world() const override { return world_; }
+
+ private:
+  int rank_, world_;
+};
+
+}  // namespace
+
+Collective* make_loopback_collective(int rank, int world) {
+  return new LoopbackCollective(rank, world);
+}
+
 }  // namespace ankh_b200

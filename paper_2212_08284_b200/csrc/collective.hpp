@@ -26,5 +26,10 @@ class Collective {
 void nccl_unique_id(unsigned char out[128]);
 /// Communicator over `world` ranks (one GPU each, current device).
 Collective* make_nccl_collective(const unsigned char id[128], int rank, int world);
+/// Timing stand-in for a one-GPU box (diagnostics only): the all-gather fills
+/// the other shards' rows with device copies of this shard's slab (the bytes
+/// land in HBM as they would over NVLink, at HBM rather than NVLink speed),
+/// the all-reduce is the identity.  Reports then hold this shard's partial sums.
+Collective* make_loopback_collective(int rank, int world);
 
 }  // namespace ankh_b200

@@ -53,7 +53,8 @@ def to_unit(v, unit, want):
 
 # launched by bench.py outside the evaluation step: the FP64 peak probe and
 # the plan's geometry-only precompute
-NOT_STEP = ("k_dfma", "k_dmma", "k_periodic_gen")
+NOT_STEP = ("k_dfma", "k_dmma", "k_periodic_gen", "k_jacobi_svd", "k_svd_factors", "k_m2l_pack",
+            "k_inst_count", "k_inst_write")
 
 
 def launch_share(path):
