@@ -334,19 +334,32 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
                                                      double* __restrict__ parent, int level,
                                                      const double* __restrict__ m2m_g) {
   constexpr int L2 = L * L, K = L2 * L, KS = exp_stride(K);
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   double* M = sm;               // 2 x L x L: M[c][i][a] = T_c(i, a)
-  double* V = M + 2 * L2;       // 8 x K children
-  double* S1 = V + 8 * K;       // 4 x K  (cx, cy) after z
+  double* V = M + 2 * L2;       // 8 x KS children (rows as stored, zero tails)
+  double* S1 = V + 8 * KS;      // 4 x K  (cx, cy) after z
   double* S2 = S1 + 4 * K;      // 2 x K  (cx) after y
   (void)level;
-  // Morton order: the children of parent p are rows 8p + (cx<<2 | cy<<1 | cz)
+  // Morton order: the children of parent p are rows 8p + (cx<<2 | cy<<1 | cz),
+  // one contiguous 8 KS-double block: loaded as 16-B pieces, a batch of
+  // loads in flight per thread before any shared-memory store
   const unsigned pcell = blockIdx.x;
-  const double* ch0 = child + static_cast<std::size_t>(pcell) * 8 * KS;
+  const double2* ch0 = reinterpret_cast<const double2*>(child + static_cast<std::size_t>(pcell) * 8 * KS);
+  double2* V2 = reinterpret_cast<double2*>(V);
+  constexpr int NV = 8 * KS / 2, kBatch = 8;
   for (int w = threadIdx.x; w < 2 * L2; w += kM2MThreads) M[w] = m2m_g[w];
-  for (int w = threadIdx.x; w < 8 * K; w += kM2MThreads) {
-    const int c = w / K, e = w - K * (w / K);
-    V[w] = __ldg(ch0 + c * KS + e);
+  for (int w0 = 0; w0 < NV; w0 += kBatch * kM2MThreads) {
+    double2 t[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int w = w0 + u * kM2MThreads + threadIdx.x;
+      if (w < NV) t[u] = __ldg(ch0 + w);
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int w = w0 + u * kM2MThreads + threadIdx.x;
+      if (w < NV) V2[w] = t[u];
+    }
   }
   __syncthreads();
   // z: S1[(cx,cy)][a,b,k] = sum_cz sum_c' Mz[cz](k,c') V[(cx,cy,cz)][a,b,c']
@@ -356,7 +369,7 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
     double acc = 0.0;
 #pragma unroll
     for (int cz = 0; cz < 2; ++cz) {
-      const double* v = V + (2 * q + cz) * K + ab * L;
+      const double* v = V + (2 * q + cz) * KS + ab * L;
       const double* m = M + cz * L2 + k * L;
 #pragma unroll
       for (int c = 0; c < L; ++c) acc += m[c] * v[c];
@@ -443,7 +456,7 @@ template <int L>
 void m2m_order(const double* child, double* parent, int parent_level, const double* m2m,
                cudaStream_t st) {
   constexpr int K = L * L * L;
-  const std::size_t smem = sizeof(double) * (2 * L * L + 14 * K);
+  const std::size_t smem = sizeof(double) * (2 * L * L + 8 * exp_stride(K) + 6 * K);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_m2m<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -204,14 +204,21 @@ __device__ T slice_sum(const T* __restrict__ a, int n) {
   return acc;
 }
 
-// Level 1: block b sums slice b of every partial array (fixed order per slice).
-__global__ void __launch_bounds__(kFinThreads) k_finalize_slices(
+// Level 1: block b sums slice b of every partial array (fixed order per
+// slice).  Level 2 runs in the block that finishes last (completion counter
+// after a release fence): one pass over the kFinBlocks slices in slice order,
+// so the result is bitwise independent of which block that is.  The counter
+// is left at zero for the next evaluation (and CUDA-graph replays).
+__global__ void __launch_bounds__(kFinThreads) k_finalize(
     const double* __restrict__ near_partial, int n_near,
     const unsigned long long* __restrict__ pair_count, int n_count,
     const double* __restrict__ far_partial, int n_far, const double* __restrict__ self_partial,
-    int n_self, double* __restrict__ slices, unsigned long long* __restrict__ slice_pairs) {
+    int n_self, double* slices, unsigned long long* slice_pairs, unsigned* done,
+    double self_scale, const double* __restrict__ periodic, int use_periodic, int include_self,
+    DevResult* res) {
   __shared__ double red[kFinThreads];
   __shared__ unsigned long long redu[kFinThreads];
+  __shared__ bool last;
   const double a = block_sum(slice_sum(near_partial, n_near), red);
   const double b = block_sum(slice_sum(far_partial, n_far), red);
   const double c = block_sum(slice_sum(self_partial, n_self), red);
@@ -221,28 +228,28 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_slices(
     slices[3 * blockIdx.x + 1] = b;
     slices[3 * blockIdx.x + 2] = c;
     slice_pairs[blockIdx.x] = p;
+    __threadfence();
+    last = atomicAdd(done, 1u) == kFinBlocks - 1;
   }
-}
-
-// Level 2: one warp-sized pass over the kFinBlocks slices, in slice order.
-__global__ void k_finalize(const double* __restrict__ slices,
-                           const unsigned long long* __restrict__ slice_pairs, double self_scale,
-                           const double* __restrict__ periodic, int use_periodic,
-                           int include_self, DevResult* res) {
-  if (threadIdx.x != 0) return;
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  const volatile double* vs = slices;
+  const volatile unsigned long long* vp = slice_pairs;
   double e_near = 0.0, e_far = 0.0, self_acc = 0.0;
   unsigned long long pairs = 0;
-  for (int b = 0; b < kFinBlocks; ++b) {
-    e_near += slices[3 * b];
-    e_far += slices[3 * b + 1];
-    self_acc += slices[3 * b + 2];
-    pairs += slice_pairs[b];
+  for (int k = 0; k < kFinBlocks; ++k) {
+    e_near += vs[3 * k];
+    e_far += vs[3 * k + 1];
+    self_acc += vs[3 * k + 2];
+    pairs += vp[k];
   }
   res->red[kENear] = e_near;
   res->red[kEFar] = e_far;
   res->red[kESelf] = include_self ? self_scale * self_acc : 0.0;  // -xi/sqrt(pi) acc (kernel.cpp:212)
   res->red[kEPeriodic] = use_periodic ? periodic[0] : 0.0;
   res->red[kNearPairs] = static_cast<double>(pairs);
+  *done = 0u;
 }
 
 }  // namespace
@@ -270,16 +277,18 @@ void launch_finalize(const double* near_partial, int n_near, const unsigned long
                      int n_count, const double* far_partial, int n_far, const double* self_partial,
                      int n_self, double self_scale, const double* periodic, int use_periodic,
                      int include_self, double* scratch, DevResult* res, cudaStream_t st) {
-  // scratch: kFinBlocks x 3 doubles + kFinBlocks uint64 (finalize_scratch_bytes)
+  // scratch: kFinBlocks x 3 doubles, kFinBlocks uint64, the completion
+  // counter (finalize_scratch_bytes; zeroed once at allocation)
   unsigned long long* slice_pairs = reinterpret_cast<unsigned long long*>(scratch + 3 * kFinBlocks);
-  k_finalize_slices<<<kFinBlocks, kFinThreads, 0, st>>>(near_partial, n_near, pair_count, n_count,
-                                                        far_partial, n_far,
-                                                        include_self ? self_partial : nullptr,
-                                                        n_self, scratch, slice_pairs);
-  k_finalize<<<1, 32, 0, st>>>(scratch, slice_pairs, self_scale, periodic, use_periodic,
-                               include_self, res);
+  unsigned* done = reinterpret_cast<unsigned*>(slice_pairs + kFinBlocks);
+  k_finalize<<<kFinBlocks, kFinThreads, 0, st>>>(near_partial, n_near, pair_count, n_count, far_partial, n_far,
+                                                 include_self ? self_partial : nullptr, n_self, scratch,
+                                                 slice_pairs, done, self_scale, periodic, use_periodic,
+                                                 include_self, res);
 }
 
-std::size_t finalize_scratch_bytes() { return kFinBlocks * (3 * sizeof(double) + sizeof(unsigned long long)); }
+std::size_t finalize_scratch_bytes() {
+  return kFinBlocks * (3 * sizeof(double) + sizeof(unsigned long long)) + 16;
+}
 
 }  // namespace ankh_b200

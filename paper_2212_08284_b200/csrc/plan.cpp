@@ -78,6 +78,11 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
   ANKH_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
   ANKH_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   ANKH_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  ANKH_CUDA(cudaEventCreateWithFlags(&ev_m2l_fork_, cudaEventDisableTiming));
+  for (int k = 0; k < kM2LStreams; ++k) {
+    ANKH_CUDA(cudaStreamCreateWithFlags(&m2l_streams_[k], cudaStreamNonBlocking));
+    ANKH_CUDA(cudaEventCreateWithFlags(&ev_m2l_join_[k], cudaEventDisableTiming));
+  }
   for (auto& e : ev_) ANKH_CUDA(cudaEventCreate(&e));
   if (pending_code_ != 0) {
     depth = 1;  // validation-only plan
@@ -126,6 +131,14 @@ Plan::~Plan() {
     if (e) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  if (ev_m2l_fork_) cudaEventDestroy(ev_m2l_fork_);
+  for (int k = 0; k < kM2LStreams; ++k) {
+    if (m2l_streams_[k]) {
+      cudaStreamSynchronize(m2l_streams_[k]);
+      cudaStreamDestroy(m2l_streams_[k]);
+    }
+    if (ev_m2l_join_[k]) cudaEventDestroy(ev_m2l_join_[k]);
+  }
   for (cudaStream_t s : {copy_stream_, gather_stream_})
     if (s) {
       cudaStreamSynchronize(s);
@@ -225,6 +238,7 @@ void Plan::allocate() {
   d_counts_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
   d_off_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
   d_fin_scratch_ = static_cast<double*>(dalloc(finalize_scratch_bytes()));
+  ANKH_CUDA(cudaMemsetAsync(d_fin_scratch_, 0, finalize_scratch_bytes(), stream_));  // completion counter
   // A shard gathers particle records only for the leaves it reads: its P2P
   // targets, their 13 half-shell neighbours (k_p2p's stencil, periodic wrap)
   // and its P2M rows.  (One shard: every leaf, no mask.)
@@ -745,19 +759,10 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[2], st));
   // far field: M2L (fmm.cpp:238-276)
-  for (int c = 1; c <= kMaxKp8; ++c) {
-    const auto r = class_range_[c];
-    if (r.second == 0) continue;
-    launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c,
-               d_tile_ids_ + r.first, d_inst_, K, Kp, d_far_part_, far);
-    ++launches;
-  }
+  // + periodic far images (fmm.cpp:421-427), counted once (rank 0), off the
+  // timed path here (serial mode runs it after P2P)
+  launches += launch_m2l_classes(far, !serial, !serial && do_periodic);
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
-  // periodic far images (fmm.cpp:421-427), counted once (rank 0)
-  if (!serial && do_periodic) {
-    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, far);
-    ++launches;
-  }
   if (!serial) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
   const int n_near_parts =
@@ -776,7 +781,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
                   n_tiles_,
                   d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
                   include_self_ ? 1 : 0, d_fin_scratch_, d_res_, st);
-  launches += 2;
+  ++launches;
   // shards: one all-reduce of the energy / counter / flag vector (the path's
   // only exchange besides the leaf all-gather)
   if (coll_) coll_->allreduce_sum(d_res_->red, kRedShared, st);
@@ -784,6 +789,49 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
   ANKH_CUDA(cudaGetLastError());
   launches_ = launches;
+}
+
+// The rank classes of M2L (one kernel instantiation per padded rank) in
+// parallel branches: greedy longest-first over `far` and the kM2LStreams extra
+// streams by estimated work (tiles x padded rank), joined back into `far`.
+// With `with_periodic` the far-image term (independent of M2L) follows on the
+// least-loaded branch.
+std::uint32_t Plan::launch_m2l_classes(cudaStream_t far, bool fork, bool with_periodic) {
+  std::vector<int> cls;
+  for (int c = 1; c <= kMaxKp8; ++c)
+    if (class_range_[c].second > 0) cls.push_back(c);
+  std::sort(cls.begin(), cls.end(), [&](int a, int b) {
+    return static_cast<long long>(class_range_[a].second) * a > static_cast<long long>(class_range_[b].second) * b;
+  });
+  const int lanes = fork ? std::max(1, std::min<int>(1 + kM2LStreams, static_cast<int>(cls.size()))) : 1;
+  if (lanes > 1) ANKH_CUDA(cudaEventRecord(ev_m2l_fork_, far));
+  std::vector<long long> load(lanes, 0);
+  std::vector<bool> used(lanes, false);
+  for (int c : cls) {
+    const int k = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+    load[k] += static_cast<long long>(class_range_[c].second) * c;
+    cudaStream_t s = k == 0 ? far : m2l_streams_[k - 1];
+    if (k > 0 && !used[k]) ANKH_CUDA(cudaStreamWaitEvent(s, ev_m2l_fork_, 0));
+    used[k] = true;
+    const auto r = class_range_[c];
+    launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c, d_tile_ids_ + r.first, d_inst_, K,
+               Kp, d_far_part_, s);
+  }
+  std::uint32_t extra = 0;
+  if (with_periodic) {
+    const int k = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+    cudaStream_t s = k == 0 ? far : m2l_streams_[k - 1];
+    if (k > 0 && !used[k]) ANKH_CUDA(cudaStreamWaitEvent(s, ev_m2l_fork_, 0));
+    used[k] = true;
+    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, s);
+    extra = 1;
+  }
+  for (int k = 1; k < lanes; ++k)
+    if (used[k]) {
+      ANKH_CUDA(cudaEventRecord(ev_m2l_join_[k - 1], m2l_streams_[k - 1]));
+      ANKH_CUDA(cudaStreamWaitEvent(far, ev_m2l_join_[k - 1], 0));
+    }
+  return static_cast<std::uint32_t>(cls.size()) + extra;
 }
 
 void Plan::exchange_leaves(cudaStream_t st) {
@@ -1000,13 +1048,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
     ++launches;
   }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[4], side_stream_));
-  for (int c = 1; c <= kMaxKp8; ++c) {
-    const auto r = class_range_[c];
-    if (r.second == 0) continue;
-    launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c, d_tile_ids_ + r.first, d_inst_, K,
-               Kp, d_far_part_, side_stream_);
-    ++launches;
-  }
+  launches += launch_m2l_classes(side_stream_, !timing, false);
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[5], side_stream_));
   if (do_periodic) {
     launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, side_stream_);
@@ -1020,7 +1062,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   launch_finalize(d_near_part_, n_near_parts, d_pair_count_, leaf_end_ - leaf_begin_, d_far_part_, n_tiles_,
                   d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
                   include_self_ ? 1 : 0, d_fin_scratch_, d_res_, st);
-  launches += 2;
+  ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[8], st));
   ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
   mark("finalize + result copy", st);

@@ -158,6 +158,12 @@ class Plan {
   cudaStream_t stream_ = nullptr;
   cudaStream_t side_stream_ = nullptr;  // far-field chain, concurrent with P2P
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  // M2L rank classes run as parallel branches (their tails overlap; the
+  // small latency-bound classes hide under the large ones)
+  static constexpr int kM2LStreams = 3;
+  cudaStream_t m2l_streams_[kM2LStreams] = {};
+  cudaEvent_t ev_m2l_fork_ = nullptr, ev_m2l_join_[kM2LStreams] = {};
+  std::uint32_t launch_m2l_classes(cudaStream_t far, bool fork, bool with_periodic);
   // CUDA-graph replay of launch_all for repeated inputs
   cudaGraphExec_t graph_exec_ = nullptr;
   const double *graph_pos_ = nullptr, *graph_src_ = nullptr;
