@@ -17,7 +17,7 @@ using ncclComm_t = void*;
 struct NcclUniqueId {
   char internal[128];
 };
-enum { kNcclSuccess = 0, kNcclFloat64 = 8, kNcclSum = 0 };
+enum { kNcclSuccess = 0, kNcclUint64 = 5, kNcclFloat64 = 8, kNcclSum = 0, kNcclMin = 3 };
 
 struct NcclApi {
   int (*GetUniqueId)(NcclUniqueId*) = nullptr;
@@ -25,6 +25,8 @@ struct NcclApi {
   int (*CommDestroy)(ncclComm_t) = nullptr;
   int (*AllGather)(const void*, void*, std::size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*AllReduce)(const void*, void*, std::size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
 };
 
@@ -50,6 +52,8 @@ const NcclApi& nccl() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
   });
   if (!failure.empty()) throw AnkhError(ANKH_CUDA_ERROR, failure);
@@ -78,6 +82,16 @@ class NcclCollective final : public Collective {
   }
   void allreduce_sum(double* buf, std::size_t count, cudaStream_t st) override {
     check(nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, comm_, st), "ncclAllReduce");
+  }
+  void allreduce_sum_min(double* sum, std::size_t n_sum, unsigned long long* mins, std::size_t n_min,
+                         cudaStream_t st) override {
+    // one grouped launch for both reductions
+    check(nccl().GroupStart(), "ncclGroupStart");
+    const int a = nccl().AllReduce(sum, sum, n_sum, kNcclFloat64, kNcclSum, comm_, st);
+    const int b = nccl().AllReduce(mins, mins, n_min, kNcclUint64, kNcclMin, comm_, st);
+    check(nccl().GroupEnd(), "ncclGroupEnd");
+    check(a, "ncclAllReduce(sum)");
+    check(b, "ncclAllReduce(min)");
   }
   int rank() const override { return rank_; }
   int world() const override { return world_; }
@@ -112,6 +126,7 @@ class LoopbackCollective final : public Collective {
                                   count * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
   void allreduce_sum(double*, std::size_t, cudaStream_t) override {}
+  void allreduce_sum_min(double*, std::size_t, unsigned long long*, std::size_t, cudaStream_t) override {}
   int rank() const override { return rank_; }
   int world() const override { return world_; }
 

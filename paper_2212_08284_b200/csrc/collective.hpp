@@ -18,6 +18,9 @@ class Collective {
   /// recv + rank * count (in-place all-gather).
   virtual void allgather_inplace(double* recv, std::size_t count, cudaStream_t st) = 0;
   virtual void allreduce_sum(double* buf, std::size_t count, cudaStream_t st) = 0;
+  /// sum over `sum[0, n_sum)` and minimum over `mins[0, n_min)`, together
+  virtual void allreduce_sum_min(double* sum, std::size_t n_sum, unsigned long long* mins,
+                                 std::size_t n_min, cudaStream_t st) = 0;
   virtual int rank() const = 0;
   virtual int world() const = 0;
 };

@@ -299,11 +299,11 @@ __global__ void k_stream_lists(const unsigned char* __restrict__ ready, unsigned
   list_p2p[atomicAdd(&cursor[n_chunks + ready[2 * m + 1]], 1u)] = m;
 }
 
-__global__ void k_init_result(DevResult* res) {
+__global__ void k_init_result(DevResult* res, int any_multipole) {
   for (int k = 0; k < kRedCount; ++k) res->red[k] = 0.0;
   res->min_nonfinite = ~0ull;
   res->min_outside = ~0ull;
-  res->any_multipole = 0;
+  res->any_multipole = any_multipole;
   res->p2p_next = 0;
 }
 
@@ -327,7 +327,9 @@ __global__ void k_dup_check(const unsigned* __restrict__ keys, const unsigned* _
 
 }  // namespace
 
-void launch_init_result(DevResult* res, cudaStream_t st) { k_init_result<<<1, 1, 0, st>>>(res); }
+void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole) {
+  k_init_result<<<1, 1, 0, st>>>(res, any_multipole);
+}
 
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st) {

@@ -56,7 +56,8 @@ enum RedSlot {
 struct DevResult {
   double red[kRedCount];
   unsigned long long min_nonfinite;  // lowest index with a non-finite value (same on every shard)
-  unsigned long long min_outside;    // lowest finite index outside the box
+  unsigned long long min_outside;    // lowest finite index outside the box (follows min_nonfinite:
+                                     // the two are MIN-reduced together across shards)
   int any_multipole;                 // some particle has mu or Theta != 0
   unsigned p2p_next;                 // dynamic leaf counter of the pipelined P2P kernel
 };
@@ -145,7 +146,7 @@ std::size_t finalize_scratch_bytes();
 void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
                        std::size_t n, double xi, double* self_partial, DevResult* res,
                        double* part, cudaStream_t st);
-void launch_init_result(DevResult* res, cudaStream_t st);
+void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole = 0);
 /// Counting sort into leaves (after launch_bin with counts): scan -> offsets,
 /// scatter, per-leaf ascending order (sorted = the leaf CSR's index array) and
 /// the gather of 112-B records.  unsorted / scratch: N uints each; need

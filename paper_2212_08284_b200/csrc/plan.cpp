@@ -200,6 +200,12 @@ void Plan::build_geometry() {
   shard_upward_ = cfg.world > 1 && (static_cast<long long>(n_leaves) % cfg.world) == 0;
   p2m_begin_ = shard_upward_ ? lb : 0;
   p2m_end_ = shard_upward_ ? le : n_leaves;
+  slice_src_ = shard_upward_ && std::getenv("ANKH_SHARD_FULL_SRC") == nullptr;
+  if (slice_src_) {
+    const std::size_t blocks = (n + 255) / 256;
+    src_i0_ = std::min(n, blocks * cfg.rank / cfg.world * 256);
+    src_i1_ = std::min(n, blocks * (cfg.rank + 1) / cfg.world * 256);
+  }
   // P2P polynomial length from the largest possible near distance
   // (2 leaf sides per axis): s_max = xi^2 (2 sqrt(3) * 2 r_B / n)^2
   const double side = 2.0 * rb / nax;
@@ -710,13 +716,19 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     launches += 2;
   } else if (mode != 2) {
     ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
-    launch_init_result(d_res_, st);
+    // sliced moments: other slices' multipoles are unseen, so the kernels
+    // that branch on the global flag take the multipole path (same energies)
+    launch_init_result(d_res_, st, slice_src_ ? 1 : 0);
     ++launches;
     // binning + sort + gather (build_tree, octree.cpp:27-45)
     const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
-    launch_bin(d_pos, d_src, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_,
-               d_self_part_, d_res_, st);
+    launch_bin(d_pos, slice_src_ ? nullptr : d_src, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_,
+               d_counts_, d_self_part_, d_res_, st);
     ++launches;
+    if (slice_src_ && src_i1_ > src_i0_) {  // this shard's moment slice (self partials, flags)
+      launch_src_chunk(d_pos, d_src, nullptr, src_i0_, src_i1_, cfg.xi, d_self_part_, d_res_, nullptr, st);
+      ++launches;
+    }
     // counting sort by leaf: d_idx_ holds the arrival slots, d_keys2_ the
     // scattered indices, d_idx2_ the leaf CSR's ascending indices
     launch_bucket_gather(d_temp_, temp_bytes_, d_pos, d_src, d_keys_, d_idx_, d_counts_, d_off_,
@@ -777,14 +789,24 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   }
   if (!serial) ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[5], st));
+  // self energy: rank 0 sums all N (or, sliced, every shard its slice)
+  const bool count_self = include_self_ || (slice_src_ && mode != 3);
   launch_finalize(d_near_part_, n_near_parts, d_pair_count_, leaf_end_ - leaf_begin_, d_far_part_,
                   n_tiles_,
                   d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
-                  include_self_ ? 1 : 0, d_fin_scratch_, d_res_, st);
+                  count_self ? 1 : 0, d_fin_scratch_, d_res_, st);
   ++launches;
   // shards: one all-reduce of the energy / counter / flag vector (the path's
-  // only exchange besides the leaf all-gather)
-  if (coll_) coll_->allreduce_sum(d_res_->red, kRedShared, st);
+  // only exchange besides the leaf all-gather), grouped with the MIN of the
+  // first-violation indices when the moment pass is sliced
+  static_assert(offsetof(DevResult, min_outside) == offsetof(DevResult, min_nonfinite) + 8,
+                "min_nonfinite / min_outside are MIN-reduced as one pair");
+  if (coll_) {
+    if (slice_src_)
+      coll_->allreduce_sum_min(d_res_->red, kRedShared, &d_res_->min_nonfinite, 2, st);
+    else
+      coll_->allreduce_sum(d_res_->red, kRedShared, st);
+  }
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[6], st));
   ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
   ANKH_CUDA(cudaGetLastError());
@@ -1087,6 +1109,18 @@ void Plan::enqueue_host(const double* h_pos, const double* h_src, cudaStream_t s
   }
   if (n > 0) {
     ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    // a shard with a sliced moment pass reads moments only for the leaves it
+    // touches and for its index slice: from page-locked host memory it reads
+    // them in place (mapped, over PCIe) instead of copying all N
+    if (slice_src_ && pending_code_ == 0 && std::getenv("ANKH_SHARD_COPY_SRC") == nullptr) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, h_src) == cudaSuccess && a.type == cudaMemoryTypeHost &&
+          a.devicePointer != nullptr) {
+        enqueue(d_pos_, static_cast<const double*>(a.devicePointer), st);
+        return;
+      }
+      cudaGetLastError();
+    }
     ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
   }
   enqueue(d_pos_, d_src_, st);

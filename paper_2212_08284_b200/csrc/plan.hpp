@@ -182,6 +182,13 @@ class Plan {
   // partition
   int leaf_begin_ = 0, leaf_end_ = 0;
   bool include_self_ = true;
+  // Shards (world | 8^E) split the moment pass (validation of q/mu/Theta and
+  // the self-energy sum) by particle-index slice [src_i0_, src_i1_) -- whole
+  // 256-particle blocks -- instead of every shard reading all N moments;
+  // with NCCL attached the per-slice first violations are MIN-reduced (phase
+  // API: each shard reports its slice, positions are checked by all)
+  bool slice_src_ = false;
+  std::size_t src_i0_ = 0, src_i1_ = 0;
 
   // inputs / sort
   double *d_pos_ = nullptr, *d_src_ = nullptr;

@@ -17,7 +17,8 @@ rank = int(os.environ.get("RANK_", "0"))
 steps = int(os.environ.get("STEPS", "4"))
 pos, src, rb, cfg = inputs.make_config(ci)
 L = cfg.orders[0] if ci != 2 else 5
-plan = ankh.Plan(pos.shape[0], rb, ankh.EwaldConfig(order_cheb=L, order_equi=L), rank=rank, world=world)
+plan = ankh.Plan(pos.shape[0], rb, ankh.EwaldConfig(order_cheb=L, order_equi=L), rank=rank, world=world,
+                 phase_timing=False)
 if world > 1:
     plan.attach_loopback()
 dp, ds = torch.from_numpy(pos).cuda(), torch.from_numpy(src).cuda()

@@ -484,6 +484,76 @@ def test_inprocess_shards_sum_to_single_gpu(cuda, world, p):
         assert abs(got - getattr(whole, k)) <= 1e-12 * abs(getattr(whole, k)) + 1e-15, k
     assert abs(sum(r.e_total for r in parts) - whole.e_total) <= 1e-12 * abs(whole.e_total)
     assert sum(r.near_pairs for r in parts) == whole.near_pairs
+    if world > 1 and 512 % world == 0:  # sliced moment pass: every shard sums its own slice
+        assert all(r.e_self != 0.0 for r in parts)
+
+
+def _loopback_shards(n, rb, ec, world):
+    plans = [ankh.Plan(n, rb, ec, rank=r, world=world, phase_timing=False) for r in range(world)]
+    for p in plans:
+        p.attach_loopback()
+    return plans
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_loopback_shards_sliced_moments(cuda, world):
+    """The NCCL-attached schedule (one CUDA graph per shard with the exchange
+    inside, P2P concurrent with the far chain) driven by the loopback
+    collective: the near field and the sliced self energy do not depend on
+    the leaf all-gather, so their per-shard values sum to the single-GPU
+    result exactly as the real all-reduce would; plain launch, graph capture
+    and replay agree bitwise."""
+    torch = cuda
+    pos, src, rb, cfg = inputs.make_config(1)
+    n = pos.shape[0]
+    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    dp, ds = torch.from_numpy(pos).cuda(), torch.from_numpy(src).cuda()
+    whole = ankh.Plan(n, rb, ec).energy_device(dp, ds)
+    plans = _loopback_shards(n, rb, ec, world)
+    reps = [[p.energy_device(dp, ds) for _ in range(3)] for p in plans]
+    for rr in reps:
+        assert rr[0].e_near == rr[1].e_near == rr[2].e_near
+        assert rr[0].e_self == rr[1].e_self == rr[2].e_self
+    for k in ("e_near", "e_self"):
+        got = sum(getattr(rr[0], k) for rr in reps)
+        assert abs(got - getattr(whole, k)) <= 1e-12 * abs(getattr(whole, k)), k
+    assert sum(rr[0].near_pairs for rr in reps) == whole.near_pairs
+    # host buffers: a shard copies the positions and reads its moments in
+    # place from page-locked memory (mapped), with the same results
+    hp = torch.from_numpy(pos).pin_memory()
+    hs = torch.from_numpy(src).pin_memory()
+    for p, rr in zip(plans, reps):
+        for _ in range(3):
+            h = p.energy(hp.numpy(), hs.numpy())
+            assert h.e_near == rr[0].e_near and h.e_self == rr[0].e_self
+        pageable = p.energy(pos, src)  # not page-locked: full copy
+        assert pageable.e_near == rr[0].e_near and pageable.e_self == rr[0].e_self
+    for p in plans:
+        p.close()
+
+
+def test_sliced_moment_validation(cuda):
+    """Sliced moment pass: positions are validated by every shard, moments
+    by the shard whose index slice holds them (the NCCL MIN all-reduce makes
+    that a job-wide error; the loopback collective reduces nothing)."""
+    torch = cuda
+    pos, src, rb, cfg = inputs.make_config(1)
+    n = pos.shape[0]
+    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    bad = src.copy()
+    bad[n - 5, 2] = np.nan  # last slice
+    plans = _loopback_shards(n, rb, ec, 2)
+    dp = torch.from_numpy(pos).cuda()
+    assert np.isfinite(plans[0].energy_device(dp, torch.from_numpy(bad).cuda()).e_total)
+    with pytest.raises(ankh.InvalidArgument, match="non-finite coordinate or moment"):
+        plans[1].energy_device(dp, torch.from_numpy(bad).cuda())
+    out = pos.copy()
+    out[n - 5, 0] = 2.0 * rb
+    for p in plans:
+        with pytest.raises(ankh.InvalidArgument, match="outside box"):
+            p.energy_device(torch.from_numpy(out).cuda(), torch.from_numpy(src).cuda())
+    for p in plans:
+        p.close()
 
 
 def test_nccl_collective_single_rank(cuda):
