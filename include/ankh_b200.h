@@ -225,6 +225,9 @@ double ankh_probe_fp64_tflops_v1(int iters);
  * 0 = m8n8k4 (the M2L kernel's), 1 = m16n8k8, 2 = m16n8k16: the roofline
  * denominator for k_m2l (no reference counterpart). */
 double ankh_probe_dmma_tflops_v1(int shape, int iters);
+/* Pipe-sharing probe: ms of a kernel whose warps run DFMA chains (mode 0),
+ * m8n8k4 DMMAs (mode 1), or half and half (mode 2). */
+double ankh_probe_fp64_mix_ms_v1(int mode, int iters_dfma, int iters_dmma);
 
 /* Library version string. */
 const char* ankh_version_v1(void);

@@ -37,6 +37,7 @@ EXPORTS = [
     "ankh_nccl_unique_id_v1",
     "ankh_plan_attach_nccl_v1",
     "ankh_plan_attach_loopback_v1",
+    "ankh_probe_fp64_mix_ms_v1",
     "ankh_radial_fit_v1",
     "ankh_probe_dmma_tflops_v1",
     "ankh_direct_energy_v1",
@@ -104,6 +105,8 @@ def lib() -> ctypes.CDLL:
         L.ankh_plan_energy_sources_v1.argtypes = [c_void_p, D, c_void_p, cp, c_size_t]
         L.ankh_probe_dmma_tflops_v1.argtypes = [c_int, c_int]
         L.ankh_probe_dmma_tflops_v1.restype = c_double
+        L.ankh_probe_fp64_mix_ms_v1.argtypes = [c_int, c_int, c_int]
+        L.ankh_probe_fp64_mix_ms_v1.restype = c_double
         L.ankh_radial_fit_v1.argtypes = [c_double, I, D, D, D, D]
         L.ankh_version_v1.argtypes = []
         L.ankh_version_v1.restype = ctypes.c_char_p

@@ -428,6 +428,14 @@ double ankh_probe_dmma_tflops_v1(int shape, int iters) {
   }
 }
 
+double ankh_probe_fp64_mix_ms_v1(int mode, int iters_dfma, int iters_dmma) {
+  try {
+    return ankh_b200::probe_fp64_mix_ms(mode, iters_dfma, iters_dmma);
+  } catch (...) {
+    return 0.0;
+  }
+}
+
 double ankh_probe_fp64_tflops_v1(int iters) {
   try {
     return ankh_b200::probe_fp64_tflops(iters > 0 ? iters : 4096);

@@ -24,26 +24,38 @@ __device__ __forceinline__ int bin_axis(double x, double rb, double inv_side, in
   return static_cast<int>(f);
 }
 
+// The moment half of validate_system (types.cpp:16-63) for particle i:
+// first non-finite index, and whether moment_order (kernel.cpp:40-44) > 0.
+// Returns the multipole flag (false for a non-finite particle).
+__device__ __forceinline__ bool check_moments(const double* __restrict__ s, std::size_t i, DevResult* res) {
+  bool finite = true, mp = false;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    finite = finite && isfinite(s[k]);
+    mp = mp || (k > 0 && s[k] != 0.0);
+  }
+  if (!finite) atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
+  return finite && mp;
+}
+
 __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
                                              const double* __restrict__ src, std::size_t n,
-                                             double rb, double inv_side, int nax, double c_mu,
-                                             double c_th, unsigned* __restrict__ keys,
+                                             double rb, double inv_side, int nax,
+                                             unsigned* __restrict__ keys,
                                              unsigned* __restrict__ idx,
-                                             unsigned* __restrict__ counts,
-                                             double* __restrict__ self_partial, DevResult* res) {
-  __shared__ double red[8];
+                                             unsigned* __restrict__ counts, DevResult* res) {
   const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
-  double acc = 0.0;
   bool mp = false;
   if (i < n) {
     const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
-    double s[10] = {};
     bool finite = isfinite(x) && isfinite(y) && isfinite(z);
-    if (src) {  // src == nullptr: positions only (ankh_plan_set_positions_v1)
+    if (src) {  // src == nullptr: positions only (the moments are checked elsewhere)
+      double s[10];
 #pragma unroll
       for (int k = 0; k < 10; ++k) s[k] = src[10 * i + k];
 #pragma unroll
       for (int k = 0; k < 10; ++k) finite = finite && isfinite(s[k]);
+      mp = finite && check_moments(s, i, res);
     }
     unsigned key = 0;
     if (!finite) {
@@ -55,13 +67,6 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
       const int iy = bin_axis(y, rb, inv_side, nax);
       const int iz = bin_axis(z, rb, inv_side, nax);
       key = static_cast<unsigned>((ix * nax + iy) * nax + iz);
-      // self_energy summand (kernel.cpp:208-209)
-      const double mu2 = s[1] * s[1] + s[2] * s[2] + s[3] * s[3];
-      const double th2 = s[4] * s[4] + s[7] * s[7] + s[9] * s[9] +
-                         2.0 * (s[5] * s[5] + s[6] * s[6] + s[8] * s[8]);
-      acc = s[0] * s[0] + c_mu * mu2 + c_th * th2;
-      // moment_order (kernel.cpp:40-44) > 0 for this particle?
-      mp = (s[1] != 0.0 || s[2] != 0.0 || s[3] != 0.0 || th2 != 0.0);
     }
     keys[i] = key;
     // counting sort: idx receives the particle's arrival slot in its leaf
@@ -70,17 +75,6 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
     idx[i] = counts ? atomicAdd(&counts[key], 1u) : static_cast<unsigned>(i);
   }
   if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
-  // deterministic block reduction
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w];
-    self_partial[blockIdx.x] = t;
-  }
 }
 
 // Counting-sort scatter: particle i goes to offsets[key] + slot (leaf order is
@@ -117,11 +111,15 @@ __device__ __forceinline__ void write_record(const double* __restrict__ pos,
 // a position) and gather its records.  Small leaves: rank sort in shared
 // memory; large ones: bottom-up merge passes in global memory (ping-pong
 // between the leaf's slices of `unsorted` and `scratch`).
+// With `check_src` the leaf's moments are also validated here (the moment
+// half of validate_system) -- k_bin then reads positions only, and the
+// moments are read once, by this gather, instead of twice.
 __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     const double* __restrict__ pos, const double* __restrict__ src,
     const unsigned* __restrict__ offsets, unsigned* __restrict__ unsorted,
     unsigned* __restrict__ scratch, unsigned* __restrict__ sorted,
-    const unsigned char* __restrict__ need, double* __restrict__ part) {
+    const unsigned char* __restrict__ need, double* __restrict__ part, bool check_src,
+    DevResult* res) {
   __shared__ unsigned a[kLeafSmem], b[kLeafSmem];
   const unsigned leaf = blockIdx.x;
   if (need && !need[leaf]) return;  // another shard's leaf
@@ -166,8 +164,13 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     order = sorted + base;
   }
   if (!part) return;  // sort only (positions bound ahead of the moments)
-  for (int p = threadIdx.x; p < c; p += kLeafThreads)
-    write_record(pos, src, order[p], part + static_cast<std::size_t>(base + p) * kRec);
+  bool mp = false;
+  for (int p = threadIdx.x; p < c; p += kLeafThreads) {
+    const unsigned i = order[p];
+    write_record(pos, src, i, part + static_cast<std::size_t>(base + p) * kRec);
+    if (check_src) mp = check_moments(src + 10 * static_cast<std::size_t>(i), i, res) || mp;
+  }
+  if (check_src && __syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
 }
 
 // Records in leaf order from an existing sorted index (the moments of a
@@ -181,52 +184,22 @@ __global__ void __launch_bounds__(256) k_gather_sorted(const double* __restrict_
   write_record(pos, src, sorted[j], part + j * kRec);
 }
 
-// The moment half of validate_system (types.cpp:16-63) and the self-energy
-// partials for the bound-positions path (same block layout as k_bin).
-// Streamed host path: particles [block0 256, n) of one arrived chunk, and each
-// particle's record scattered to its sorted slot inv[i].
+// The moment half of validate_system (types.cpp:16-63) for particles
+// [block0 256, n): the bound-positions path (all particles), a shard's index
+// slice, or -- streamed host path -- one arrived chunk, each particle's
+// record then also scattered to its sorted slot inv[i].
 __global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ src, std::size_t n,
-                                                   double c_mu, double c_th,
-                                                   double* __restrict__ self_partial,
                                                    DevResult* res, unsigned block0,
                                                    const double* __restrict__ pos,
                                                    const unsigned* __restrict__ inv,
                                                    double* __restrict__ part) {
-  __shared__ double red[8];
-  const unsigned blk = block0 + blockIdx.x;
-  const std::size_t i = static_cast<std::size_t>(blk) * 256 + threadIdx.x;
-  if (inv && i < n) write_record(pos, src, static_cast<unsigned>(i), part + static_cast<std::size_t>(inv[i]) * kRec);
-  double acc = 0.0;
+  const std::size_t i = (static_cast<std::size_t>(block0) + blockIdx.x) * 256 + threadIdx.x;
   bool mp = false;
   if (i < n) {
-    double s[10];
-    bool finite = true;
-#pragma unroll
-    for (int k = 0; k < 10; ++k) {
-      s[k] = src[10 * i + k];
-      finite = finite && isfinite(s[k]);
-    }
-    if (!finite) {
-      atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
-    } else {
-      const double mu2 = s[1] * s[1] + s[2] * s[2] + s[3] * s[3];
-      const double th2 = s[4] * s[4] + s[7] * s[7] + s[9] * s[9] +
-                         2.0 * (s[5] * s[5] + s[6] * s[6] + s[8] * s[8]);
-      acc = s[0] * s[0] + c_mu * mu2 + c_th * th2;
-      mp = (s[1] != 0.0 || s[2] != 0.0 || s[3] != 0.0 || th2 != 0.0);
-    }
+    if (inv) write_record(pos, src, static_cast<unsigned>(i), part + static_cast<std::size_t>(inv[i]) * kRec);
+    mp = check_moments(src + 10 * i, i, res);
   }
   if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w];
-    self_partial[blk] = t;
-  }
 }
 
 // inv[sorted[j]] = j: the sorted slot of every particle
@@ -239,12 +212,11 @@ __global__ void k_inverse(const unsigned* __restrict__ sorted, std::size_t n, un
 // are complete (its largest particle index -- leaves hold ascending indices)
 // and the chunk after which its 13 half-shell neighbours are too (P2P's
 // source set, k_p2p); counts per chunk in cnt[0..C) (P2M) / cnt[C..2C) (P2P).
-__global__ void k_stream_ready(const unsigned* __restrict__ offsets, const unsigned* __restrict__ sorted,
-                               int depth, int periodic, unsigned chunk, int n_chunks,
-                               unsigned char* __restrict__ ready, unsigned* __restrict__ cnt) {
-  const unsigned m = blockIdx.x * 256 + threadIdx.x;
+__device__ __forceinline__ void stream_ready_leaf(unsigned m, const unsigned* __restrict__ offsets,
+                                                  const unsigned* __restrict__ sorted, int depth, int periodic,
+                                                  unsigned chunk, int n_chunks, unsigned char* __restrict__ ready,
+                                                  unsigned* key_p2m, unsigned* key_p2p) {
   const int n = 1 << depth;
-  if (m >= static_cast<unsigned>(n) * n * n) return;
   const int ax = static_cast<int>(morton_compact3(m >> 2)), ay = static_cast<int>(morton_compact3(m >> 1)),
             az = static_cast<int>(morton_compact3(m));
   auto leaf_ready = [&](int x, int y, int z) -> int {
@@ -270,8 +242,38 @@ __global__ void k_stream_ready(const unsigned* __restrict__ offsets, const unsig
   }
   ready[2 * m] = static_cast<unsigned char>(r);
   ready[2 * m + 1] = static_cast<unsigned char>(p);
-  atomicAdd(&cnt[r], 1u);
-  atomicAdd(&cnt[n_chunks + p], 1u);
+  *key_p2m = static_cast<unsigned>(r);
+  *key_p2p = static_cast<unsigned>(n_chunks + p);
+}
+
+// Warp-aggregated slot in a shared-memory counter per key: the lanes with
+// equal keys take consecutive slots with one shared atomic per distinct key
+// (leaves of one warp mostly share a chunk, so per-lane atomics on a handful
+// of counters serialise).  key == ~0u: lane inactive.
+__device__ __forceinline__ unsigned warp_slot(unsigned key, unsigned* s_cnt) {
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  unsigned base = 0;
+  if (lane == leader && key != ~0u) base = atomicAdd(&s_cnt[key], static_cast<unsigned>(__popc(peers)));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + static_cast<unsigned>(__popc(peers & ((1u << lane) - 1u)));
+}
+
+__global__ void __launch_bounds__(256) k_stream_ready(const unsigned* __restrict__ offsets,
+                                                      const unsigned* __restrict__ sorted, int depth,
+                                                      int periodic, unsigned chunk, int n_chunks,
+                                                      unsigned char* __restrict__ ready,
+                                                      unsigned* __restrict__ cnt) {
+  __shared__ unsigned s_cnt[2 * kMaxStreamChunks];
+  if (threadIdx.x < 2 * kMaxStreamChunks) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned m = blockIdx.x * 256 + threadIdx.x;
+  unsigned k0 = ~0u, k1 = ~0u;
+  if (m < (1u << (3 * depth))) stream_ready_leaf(m, offsets, sorted, depth, periodic, chunk, n_chunks, ready, &k0, &k1);
+  warp_slot(k0, s_cnt);
+  warp_slot(k1, s_cnt);
+  __syncthreads();
+  if (threadIdx.x < 2 * n_chunks && s_cnt[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], s_cnt[threadIdx.x]);
 }
 
 // bounds[0..C] / bounds[C+1..2C+1]: exclusive scans of the two count sets;
@@ -290,13 +292,28 @@ __global__ void k_stream_scan(const unsigned* __restrict__ cnt, int n_chunks, un
   }
 }
 
-__global__ void k_stream_lists(const unsigned char* __restrict__ ready, unsigned n_leaves, int n_chunks,
-                               unsigned* __restrict__ cursor, unsigned* __restrict__ list_p2m,
-                               unsigned* __restrict__ list_p2p) {
+// Per-chunk leaf lists: each block reserves one contiguous range per key in
+// the global buckets, its leaves take warp-aggregated slots inside it.
+__global__ void __launch_bounds__(256) k_stream_lists(const unsigned char* __restrict__ ready, unsigned n_leaves,
+                                                      int n_chunks, unsigned* __restrict__ cursor,
+                                                      unsigned* __restrict__ list_p2m,
+                                                      unsigned* __restrict__ list_p2p) {
+  __shared__ unsigned s_cnt[2 * kMaxStreamChunks], s_base[2 * kMaxStreamChunks];
+  if (threadIdx.x < 2 * kMaxStreamChunks) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
   const unsigned m = blockIdx.x * 256 + threadIdx.x;
-  if (m >= n_leaves) return;
-  list_p2m[atomicAdd(&cursor[ready[2 * m]], 1u)] = m;
-  list_p2p[atomicAdd(&cursor[n_chunks + ready[2 * m + 1]], 1u)] = m;
+  const bool ok = m < n_leaves;
+  const unsigned k0 = ok ? ready[2 * m] : ~0u;
+  const unsigned k1 = ok ? n_chunks + ready[2 * m + 1] : ~0u;
+  const unsigned s0 = warp_slot(k0, s_cnt);
+  const unsigned s1 = warp_slot(k1, s_cnt);
+  __syncthreads();
+  if (threadIdx.x < 2 * n_chunks)
+    s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]) : 0u;
+  __syncthreads();
+  if (!ok) return;
+  list_p2m[s_base[k0] + s0] = m;
+  list_p2p[s_base[k1] + s1] = m;
 }
 
 __global__ void k_init_result(DevResult* res, int any_multipole) {
@@ -339,48 +356,41 @@ void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, c
 }
 
 void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
-                double inv_side, int n_axis, double xi, unsigned* keys, unsigned* idx,
-                unsigned* counts, double* self_partial, DevResult* res, cudaStream_t st) {
+                double inv_side, int n_axis, unsigned* keys, unsigned* idx, unsigned* counts,
+                DevResult* res, cudaStream_t st) {
   if (n == 0) return;
-  const double c_mu = 2.0 * xi * xi / 3.0;
-  const double c_th = 8.0 * xi * xi * xi * xi / 5.0;
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  k_bin<<<blocks, 256, 0, st>>>(pos, src, n, box_radius, inv_side, n_axis, c_mu, c_th, keys, idx,
-                                counts, self_partial, res);
+  k_bin<<<blocks, 256, 0, st>>>(pos, src, n, box_radius, inv_side, n_axis, keys, idx, counts, res);
 }
 
 void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
                           const unsigned* keys, const unsigned* slots, const unsigned* counts,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
                           unsigned* sorted, std::size_t n, int n_leaves,
-                          const unsigned char* need, double* part, cudaStream_t st) {
+                          const unsigned char* need, double* part, cudaStream_t st,
+                          bool check_src, DevResult* res) {
   std::size_t bytes = temp_bytes;
   cub::DeviceScan::ExclusiveSum(temp, bytes, counts, offsets, n_leaves + 1, st);
   if (n == 0) return;
   k_scatter<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, slots, offsets, n,
                                                                     unsorted);
   k_leaf_gather<<<static_cast<unsigned>(n_leaves), kLeafThreads, 0, st>>>(
-      pos, src, offsets, unsorted, scratch, sorted, need, part);
+      pos, src, offsets, unsorted, scratch, sorted, need, part, check_src && part != nullptr, res);
 }
 
 void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
-                       std::size_t n, double xi, double* self_partial, DevResult* res,
-                       double* part, cudaStream_t st) {
+                       std::size_t n, DevResult* res, double* part, cudaStream_t st) {
   if (n == 0) return;
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  k_src_check<<<blocks, 256, 0, st>>>(src, n, 2.0 * xi * xi / 3.0, 8.0 * xi * xi * xi * xi / 5.0,
-                                      self_partial, res, 0u, nullptr, nullptr, nullptr);
+  k_src_check<<<blocks, 256, 0, st>>>(src, n, res, 0u, nullptr, nullptr, nullptr);
   k_gather_sorted<<<blocks, 256, 0, st>>>(pos, src, sorted, n, part);
 }
 
 void launch_src_chunk(const double* pos, const double* src, const unsigned* inv, std::size_t i0,
-                      std::size_t i1, double xi, double* self_partial, DevResult* res, double* part,
-                      cudaStream_t st) {
-  if (i1 <= i0) return;  // i0 is a multiple of 256 (k_bin's self-partial blocks)
+                      std::size_t i1, DevResult* res, double* part, cudaStream_t st) {
+  if (i1 <= i0) return;  // i0 is a multiple of 256
   const unsigned blocks = static_cast<unsigned>((i1 - i0 + 255) / 256);
-  k_src_check<<<blocks, 256, 0, st>>>(src, i1, 2.0 * xi * xi / 3.0, 8.0 * xi * xi * xi * xi / 5.0,
-                                      self_partial, res, static_cast<unsigned>(i0 / 256), pos, inv,
-                                      part);
+  k_src_check<<<blocks, 256, 0, st>>>(src, i1, res, static_cast<unsigned>(i0 / 256), pos, inv, part);
 }
 
 void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,

@@ -21,6 +21,16 @@ namespace {
 
 constexpr int kP2MThreads = 128;
 
+// self_energy summand of one particle record (kernel.cpp:208-209): q^2 +
+// c_mu |mu|^2 + c_th Theta:Theta (off-diagonals twice, SymMat3::contract)
+__device__ __forceinline__ double self_term(double q, double mx, double my, double mz, double txx,
+                                            double txy, double txz, double tyy, double tyz, double tzz,
+                                            double c_mu, double c_th) {
+  const double mu2 = fma(mx, mx, fma(my, my, mz * mz));
+  const double th2 = fma(txx, txx, fma(tyy, tyy, tzz * tzz)) + 2.0 * fma(txy, txy, fma(txz, txz, tyz * tyz));
+  return fma(c_th, th2, fma(c_mu, mu2, q * q));
+}
+
 // hd[n] = H D^n (chebyshev.cpp:85-115) for n = 0..2 depends only on the
 // order L, so it lives in the constant bank (one slot per L = 2..10) and the
 // basis DFMAs read it as an immediate operand instead of loading it per
@@ -56,7 +66,9 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
                                                        double* __restrict__ exp_leaf,
                                                        unsigned m_begin, unsigned m_end,
                                                        const unsigned* __restrict__ list,
-                                                       const unsigned* __restrict__ bounds) {
+                                                       const unsigned* __restrict__ bounds,
+                                                       double* __restrict__ self_leaf, double c_mu,
+                                                       double c_th) {
   using Sh = P2MWShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER, KS = exp_stride(K);
   extern __shared__ double sm[];
@@ -100,6 +112,7 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
     for (int i = 0; i < L; ++i) acc[q][i] = 0.0;
   }
 
+  double self_acc = 0.0;
   for (int p0 = 0; p0 < cnt; p0 += 32) {
     const int pc = min(32, cnt - p0);
     __syncwarp();
@@ -109,6 +122,7 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
                     v4 = __ldg(r + 4), v5 = __ldg(r + 5), v6 = __ldg(r + 6);
       const double q = v1.y, mx = v2.x, my = v2.y, mz = v3.x, txx = v3.y, txy = v4.x,
                    txz = v4.y, tyy = v5.x, tyz = v5.y, tzz = v6.x;
+      self_acc += self_term(q, mx, my, mz, txx, txy, txz, tyy, tyz, tzz, c_mu, c_th);
       const double lx = (v0.x - c0) * inv_rad, ly = (v0.y - c1) * inv_rad,
                    lz = (v1.x - c2) * inv_rad;
       double* dst = st + lane * PER;
@@ -189,6 +203,10 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
       for (int i = 0; i < L; ++i) out[i * L2 + jk] = acc[q][i];
     }
   }
+  // the leaf's self-energy sum, fixed lane order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) self_acc += __shfl_down_sync(0xffffffffu, self_acc, o);
+  if (lane == 0) self_leaf[m] = self_acc;
 }
 
 template <int L>
@@ -207,7 +225,8 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
                                                      const double* __restrict__ hd_g,
                                                      double* __restrict__ exp_leaf,
                                                      const DevResult* __restrict__ res,
-                                                     unsigned m_begin) {
+                                                     unsigned m_begin, double* __restrict__ self_leaf,
+                                                     double c_mu, double c_th) {
   using Sh = P2MShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PB = Sh::PB, RS = Sh::RS, KS = exp_stride(K);
   extern __shared__ double sm[];
@@ -224,8 +243,10 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
   double* out = exp_leaf + static_cast<std::size_t>(m) * KS;
   if (cnt == 0) {
     for (int o = tid; o < K; o += kP2MThreads) out[o] = 0.0;
+    if (tid == 0) self_leaf[m] = 0.0;
     return;
   }
+  double self_acc = 0.0;  // particle tid of each batch (PB <= kP2MThreads)
   const bool charges_only = res->any_multipole == 0;
   // cell_geometry (octree.cpp:18-25)
   const double rad = rb / n;
@@ -255,6 +276,10 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
       rec[p * RS + 2 * c + 1] = v.y;
     }
     __syncthreads();
+    if (tid < pb) {
+      const double* r = rec + tid * RS;
+      self_acc += self_term(r[3], r[4], r[5], r[6], r[7], r[8], r[9], r[10], r[11], r[12], c_mu, c_th);
+    }
     // phase A: 1-D basis derivatives per (particle, axis)
     for (int w = tid; w < pb * 3; w += kP2MThreads) {
       const int p = w / 3, ax = w - 3 * (w / 3);
@@ -325,6 +350,15 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
 #pragma unroll
   for (int q = 0; q < Sh::QN; ++q)
     if (tid + q * kP2MThreads < K) out[tid + q * kP2MThreads] = acc[q];
+  // the leaf's self-energy sum: PB threads, fixed order
+  __shared__ double s_self[PB];
+  if (tid < PB) s_self[tid] = self_acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int k = 0; k < PB; ++k) t += s_self[k];
+    self_leaf[m] = t;
+  }
 }
 
 constexpr int kM2MThreads = 128;
@@ -411,9 +445,10 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
 
 template <int L>
 void p2m_order(const double* part, const unsigned* leaf_off, int depth, double rb,
-               const double* hd, double* exp_leaf, const DevResult* res, unsigned m_begin,
-               unsigned m_end, const unsigned* list, const unsigned* bounds, unsigned list_count,
-               cudaStream_t st) {
+               const double* hd, double* exp_leaf, const DevResult* res, double* self_leaf, double xi,
+               unsigned m_begin, unsigned m_end, const unsigned* list, const unsigned* bounds,
+               unsigned list_count, cudaStream_t st) {
+  const double c_mu = 2.0 * xi * xi / 3.0, c_th = 8.0 * xi * xi * xi * xi / 5.0;  // kernel.cpp:209
   const unsigned leaves = list ? list_count : (m_end > m_begin ? m_end - m_begin : 0u);
   if (leaves == 0) return;
   if (L > 6) {  // register budget of the warp-per-leaf variant: block-per-leaf instead
@@ -426,7 +461,7 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
       attr_b = true;
     }
     k_p2m<L><<<leaves, kP2MThreads, smem, st>>>(part, leaf_off, depth, rb, hd, exp_leaf, res,
-                                                m_begin);
+                                                m_begin, self_leaf, c_mu, c_th);
     return;
   }
   constexpr int LW = L > 6 ? 6 : L;  // (never launched with L > 6)
@@ -438,7 +473,7 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
     attr = true;
   }
   k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(
-      part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end, list, bounds);
+      part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end, list, bounds, self_leaf, c_mu, c_th);
 }
 
 }  // namespace
@@ -485,11 +520,11 @@ void m2m_order(const double* child, double* parent, int parent_level, const doub
 
 void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
                 double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
-                unsigned m_begin, unsigned m_end, cudaStream_t st, const unsigned* list,
-                const unsigned* bounds, unsigned list_count) {
+                double* self_leaf, double xi, unsigned m_begin, unsigned m_end, cudaStream_t st,
+                const unsigned* list, const unsigned* bounds, unsigned list_count) {
 #define ANKH_P2M(N) \
-  p2m_order<N>(part, leaf_off, depth, box_radius, hd, exp_leaf, res, m_begin, m_end, list, bounds, \
-               list_count, st)
+  p2m_order<N>(part, leaf_off, depth, box_radius, hd, exp_leaf, res, self_leaf, xi, m_begin, m_end, list, \
+               bounds, list_count, st)
   ANKH_ORDER_SWITCH(order, ANKH_P2M)
 #undef ANKH_P2M
 }

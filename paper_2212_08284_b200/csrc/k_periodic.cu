@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kPerThreads) k_periodic_eval(const double* __r
 
 constexpr int kFinThreads = 256;
 constexpr int kFinBlocks = 64;  // first level: contiguous slices, fixed order
+static_assert(3 * kFinBlocks <= kFinThreads, "k_finalize stages the slices in red[]");
 
 __device__ double block_sum(double v, double* red) {
   red[threadIdx.x] = v;
@@ -232,17 +233,24 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(
     last = atomicAdd(done, 1u) == kFinBlocks - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
-  const volatile double* vs = slices;
-  const volatile unsigned long long* vp = slice_pairs;
+  // the other blocks' slices: one L2 load per thread, then the fixed-order sum
+  if (threadIdx.x < kFinBlocks) {
+    red[threadIdx.x] = __ldcg(slices + 3 * threadIdx.x);
+    red[kFinBlocks + threadIdx.x] = __ldcg(slices + 3 * threadIdx.x + 1);
+    red[2 * kFinBlocks + threadIdx.x] = __ldcg(slices + 3 * threadIdx.x + 2);
+    redu[threadIdx.x] = __ldcg(slice_pairs + threadIdx.x);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   double e_near = 0.0, e_far = 0.0, self_acc = 0.0;
   unsigned long long pairs = 0;
   for (int k = 0; k < kFinBlocks; ++k) {
-    e_near += vs[3 * k];
-    e_far += vs[3 * k + 1];
-    self_acc += vs[3 * k + 2];
-    pairs += vp[k];
+    e_near += red[k];
+    e_far += red[kFinBlocks + k];
+    self_acc += red[2 * kFinBlocks + k];
+    pairs += redu[k];
   }
   res->red[kENear] = e_near;
   res->red[kEFar] = e_far;

@@ -71,6 +71,62 @@ __global__ void __launch_bounds__(256) k_dmma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// Do DFMA (FP64 pipe) and DMMA (FP64 tensor subpipe) share issue capacity?
+// MODE 0: every warp runs DFMA chains; 1: every warp runs m8n8k4 DMMAs; 2: even
+// warps DFMA, odd warps DMMA (half of each).  With the iteration counts
+// balanced so that T0 ~ T1, T2 ~ T0 means one shared pipe, T2 ~ T0/2 two.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_mix(double* out, int it_f, int it_m) {
+  const bool f = MODE == 0 || (MODE == 2 && ((threadIdx.x >> 5) & 1) == 0);
+  double s = 0.0;
+  if (f) {
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3 + k;
+    for (int i = 0; i < it_f; ++i) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = fma(a[k], 0.999999, 1e-7);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+  } else {
+    double c[8][2];
+    const double a = 1e-3 * threadIdx.x, b = 1e-3 * (threadIdx.x + 1);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = 0.0;
+    for (int i = 0; i < it_m; ++i) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[t][0]), "+d"(c[t][1])
+                     : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int MODE>
+float time_mix(int it_f, int it_m, int blocks, double* d) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_mix<MODE><<<blocks, 256>>>(d, it_f / 4 + 1, it_m / 4 + 1);
+  cudaEventRecord(e0);
+  k_mix<MODE><<<blocks, 256>>>(d, it_f, it_m);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms;
+}
+
 template <int SHAPE>
 double time_dmma(int iters, int sms, double* d) {
   cudaEvent_t e0, e1;
@@ -104,6 +160,20 @@ double probe_dmma_tflops(int shape, int iters) {
   else r = time_dmma<2>(iters / 8, sms, d);
   cudaFree(d);
   return r;
+}
+
+double probe_fp64_mix_ms(int mode, int it_f, int it_m) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  cudaMalloc(&d, sizeof(double));
+  float ms = 0.f;
+  if (mode == 0) ms = time_mix<0>(it_f, it_m, sms * 4, d);
+  else if (mode == 1) ms = time_mix<1>(it_f, it_m, sms * 4, d);
+  else ms = time_mix<2>(it_f, it_m, sms * 4, d);
+  cudaFree(d);
+  return ms;
 }
 
 double probe_fp64_tflops(int iters) {

@@ -53,6 +53,9 @@ enum RedSlot {
   kNearPairs = kRedShared, kRedCount = 8
 };
 
+// streamed host path: at most this many moment chunks (per-chunk leaf lists)
+constexpr int kMaxStreamChunks = 32;
+
 struct DevResult {
   double red[kRedCount];
   unsigned long long min_nonfinite;  // lowest index with a non-finite value (same on every shard)
@@ -77,8 +80,8 @@ struct M2LOp {
 
 // ---- launchers (defined in the .cu files) ----
 void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
-                double inv_side, int n_axis, double xi, unsigned* keys, unsigned* idx,
-                unsigned* counts, double* self_partial, DevResult* res, cudaStream_t st);
+                double inv_side, int n_axis, unsigned* keys, unsigned* idx, unsigned* counts,
+                DevResult* res, cudaStream_t st);
 std::size_t sort_temp_bytes(std::size_t n, int n_leaves);
 void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
                  const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
@@ -87,15 +90,16 @@ void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, un
 void upload_p2m_basis(int order, const double* hd, cudaStream_t st);
 // list != nullptr (L <= 6 only): the leaves list[bounds[0] .. bounds[1]),
 // list_count of them (streamed host path)
+/// Also the self-energy summand sum of every visited leaf (kernel.cpp:206-213
+/// without the -xi/sqrt(pi) factor) into self_leaf[Morton leaf].
 void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int order,
                 double box_radius, const double* hd, double* exp_leaf, const DevResult* res,
-                unsigned m_begin, unsigned m_end, cudaStream_t st, const unsigned* list = nullptr,
+                double* self_leaf, double xi, unsigned m_begin, unsigned m_end, cudaStream_t st, const unsigned* list = nullptr,
                 const unsigned* bounds = nullptr, unsigned list_count = 0);
 // streamed host path (k_bin.cu): one arrived chunk [i0, i1) of the moments --
 // validation, self-energy partials, records scattered to their sorted slots
 void launch_src_chunk(const double* pos, const double* src, const unsigned* inv, std::size_t i0,
-                      std::size_t i1, double xi, double* self_partial, DevResult* res, double* part,
-                      cudaStream_t st);
+                      std::size_t i1, DevResult* res, double* part, cudaStream_t st);
 // inverse permutation, per-leaf readiness chunk (P2M: own records; P2P: + the
 // 13 half-shell neighbours), per-chunk leaf lists and their bounds
 // (bounds[0..C] P2M, bounds[C+1..2C+1] P2P)
@@ -144,8 +148,7 @@ std::size_t finalize_scratch_bytes();
 /// Bound-positions path: moment validation + self-energy partials (k_bin's
 /// block layout) and the records gathered through an existing sorted index.
 void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
-                       std::size_t n, double xi, double* self_partial, DevResult* res,
-                       double* part, cudaStream_t st);
+                       std::size_t n, DevResult* res, double* part, cudaStream_t st);
 void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole = 0);
 /// Counting sort into leaves (after launch_bin with counts): scan -> offsets,
 /// scatter, per-leaf ascending order (sorted = the leaf CSR's index array) and
@@ -157,8 +160,11 @@ void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos,
                           const unsigned* keys, const unsigned* slots, const unsigned* counts,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
                           unsigned* sorted, std::size_t n, int n_leaves,
-                          const unsigned char* need, double* part, cudaStream_t st);
+                          const unsigned char* need, double* part, cudaStream_t st,
+                          bool check_src = false, DevResult* res = nullptr);
 double probe_fp64_tflops(int iters);
+/// ms of k_mix<mode> (k_probe.cu): DFMA-only, DMMA-only, or half/half warps
+double probe_fp64_mix_ms(int mode, int it_f, int it_m);
 /// Direct screened lattice sum (k_direct.cu): per-CTA halves of the pair sums
 /// into partial[direct_partials(n, p)]; rec: n x kRec scratch.
 int direct_partials(int n, int p);

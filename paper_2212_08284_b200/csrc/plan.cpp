@@ -75,12 +75,26 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
     pending_msg_ = "order_cheb > 10 is not supported by the B200 engine";
   }
   ANKH_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  ANKH_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+  // The far chain (P2M -> exchange -> M2M -> M2L) and the streamed path's
+  // record gathers run at the highest stream priority: the block scheduler
+  // hands them SMs first and P2P (caller's stream, default priority) fills
+  // the rest, so the dependency chain never waits behind P2P's CTA backlog.
+  int prio_least = 0, prio_greatest = 0;
+  ANKH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+  hi_prio_ = std::getenv("ANKH_NO_PRIORITY") ? 0 : prio_greatest;
+  {
+    // leaf-level M2L beside M2M: measured slower (config 3: 5.272 vs 5.261 ms,
+    // world-8 shard 0.889 vs 0.861 ms -- twice the class launches and tails)
+    const char* e = std::getenv("ANKH_M2L_SPLIT");
+    m2l_split_ = e && e[0] == '1';
+  }
+  ANKH_CUDA(cudaStreamCreateWithPriority(&side_stream_, cudaStreamNonBlocking, hi_prio_));
   ANKH_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   ANKH_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   ANKH_CUDA(cudaEventCreateWithFlags(&ev_m2l_fork_, cudaEventDisableTiming));
+  ANKH_CUDA(cudaEventCreateWithFlags(&ev_m2m_done_, cudaEventDisableTiming));
   for (int k = 0; k < kM2LStreams; ++k) {
-    ANKH_CUDA(cudaStreamCreateWithFlags(&m2l_streams_[k], cudaStreamNonBlocking));
+    ANKH_CUDA(cudaStreamCreateWithPriority(&m2l_streams_[k], cudaStreamNonBlocking, hi_prio_));
     ANKH_CUDA(cudaEventCreateWithFlags(&ev_m2l_join_[k], cudaEventDisableTiming));
   }
   for (auto& e : ev_) ANKH_CUDA(cudaEventCreate(&e));
@@ -132,6 +146,7 @@ Plan::~Plan() {
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (ev_m2l_fork_) cudaEventDestroy(ev_m2l_fork_);
+  if (ev_m2m_done_) cudaEventDestroy(ev_m2m_done_);
   for (int k = 0; k < kM2LStreams; ++k) {
     if (m2l_streams_[k]) {
       cudaStreamSynchronize(m2l_streams_[k]);
@@ -290,8 +305,7 @@ void Plan::allocate() {
   d_level_off_ = static_cast<long long*>(dalloc(level_off_.size() * sizeof(long long)));
   ANKH_CUDA(cudaMemcpyAsync(d_level_off_, level_off_.data(), level_off_.size() * sizeof(long long),
                             cudaMemcpyHostToDevice, stream_));
-  n_self_blocks_ = static_cast<int>((nn + 255) / 256);
-  d_self_part_ = static_cast<double*>(dalloc(n_self_blocks_ * sizeof(double)));
+  d_self_leaf_ = static_cast<double*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(double)));
   d_near_part_ = static_cast<double*>(dalloc(std::max(leaf_end_ - leaf_begin_, 1) *
                                              std::max(p2p_pipe_warps(256), 1) * sizeof(double)));
   d_pair_count_ = static_cast<unsigned long long*>(
@@ -626,10 +640,15 @@ void Plan::build_m2l() {
   // group owned tiles by kp class
   class_range_.assign(kMaxKp8 + 1, {0, 0});
   std::vector<int> ids;
+  class_leaf_.assign(kMaxKp8 + 1, 0);
   for (int c = 1; c <= kMaxKp8; ++c) {
+    // leaf-level tiles first: they need no M2M and can run beside it
     const int begin = static_cast<int>(ids.size());
     for (int t : owned)
-      if (h_ops_[tiles[t].op].kp / 8 == c) ids.push_back(t);
+      if (h_ops_[tiles[t].op].kp / 8 == c && tiles[t].level == depth) ids.push_back(t);
+    class_leaf_[c] = static_cast<int>(ids.size()) - begin;
+    for (int t : owned)
+      if (h_ops_[tiles[t].op].kp / 8 == c && tiles[t].level != depth) ids.push_back(t);
     class_range_[c] = {begin, static_cast<int>(ids.size()) - begin};
   }
   stamp("pack");
@@ -695,8 +714,7 @@ void Plan::validate_only(const double* d_pos, const double* d_src, cudaStream_t 
   launch_init_result(d_res_, st);
   const int nax8 = 256;  // depth-8 bins keep the duplicate scan local
   const double inv_side = nax8 / (2.0 * rb);
-  launch_bin(d_pos, d_src, n, rb, inv_side, nax8, cfg.xi, d_keys_, d_idx_, nullptr, d_self_part_,
-             d_res_, st);
+  launch_bin(d_pos, d_src, n, rb, inv_side, nax8, d_keys_, d_idx_, nullptr, d_res_, st);
   launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 24, nullptr, nullptr,
               0, st);
   launch_dup_check(d_keys2_, d_idx2_, d_pos, n, d_res_, st);
@@ -712,7 +730,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     // positions validated and sorted by set_positions: start from their flags,
     // validate the moments, gather the records through the sorted index
     ANKH_CUDA(cudaMemcpyAsync(d_res_, d_res_pos_, sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
-    launch_src_gather(d_pos, d_src, d_idx2_, n, cfg.xi, d_self_part_, d_res_, d_part_, st);
+    launch_src_gather(d_pos, d_src, d_idx2_, n, d_res_, d_part_, st);
     launches += 2;
   } else if (mode != 2) {
     ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
@@ -722,17 +740,20 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     ++launches;
     // binning + sort + gather (build_tree, octree.cpp:27-45)
     const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
-    launch_bin(d_pos, slice_src_ ? nullptr : d_src, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_,
-               d_counts_, d_self_part_, d_res_, st);
+    // moments: checked by the record gather when it visits every leaf (one
+    // read of them), by a slice pass on sliced shards, else by k_bin
+    const bool gather_src = gather_checks_src();
+    launch_bin(d_pos, (slice_src_ || gather_src) ? nullptr : d_src, n, rb, inv_side, nax, d_keys_, d_idx_,
+               d_counts_, d_res_, st);
     ++launches;
     if (slice_src_ && src_i1_ > src_i0_) {  // this shard's moment slice (self partials, flags)
-      launch_src_chunk(d_pos, d_src, nullptr, src_i0_, src_i1_, cfg.xi, d_self_part_, d_res_, nullptr, st);
+      launch_src_chunk(d_pos, d_src, nullptr, src_i0_, src_i1_, d_res_, nullptr, st);
       ++launches;
     }
     // counting sort by leaf: d_idx_ holds the arrival slots, d_keys2_ the
     // scattered indices, d_idx2_ the leaf CSR's ascending indices
     launch_bucket_gather(d_temp_, temp_bytes_, d_pos, d_src, d_keys_, d_idx_, d_counts_, d_off_,
-                         d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, d_part_, st);
+                         d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, d_part_, st, gather_src, d_res_);
     launches += 2;
   }
   if (csr_only_) {
@@ -755,7 +776,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[1], st));
   // interpolation: P2M over this shard's Morton leaf range (fmm.cpp:181-201) ...
   if (mode != 2) {
-    launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_,
+    launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, d_self_leaf_, cfg.xi,
                static_cast<unsigned>(p2m_begin_), static_cast<unsigned>(p2m_end_), far);
     ++launches;
   }
@@ -765,16 +786,25 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   }
   // ... the leaf level completed by the shard exchange, then M2M (fmm.cpp:203-236)
   if (mode == 0 || mode == 3) exchange_leaves(far);
-  for (int l = depth - 1; l >= 0; --l) {
-    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, far);
-    ++launches;
+  if (serial) {
+    for (int l = depth - 1; l >= 0; --l) {
+      launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, far);
+      ++launches;
+    }
+    if (timing) ANKH_CUDA(cudaEventRecord(ev_[2], st));
+    // far field: M2L (fmm.cpp:238-276); the periodic term follows P2P below
+    for (int c = 1; c <= kMaxKp8; ++c) {
+      const auto r = class_range_[c];
+      if (r.second == 0) continue;
+      launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c, d_tile_ids_ + r.first, d_inst_,
+                 K, Kp, d_far_part_, far);
+      ++launches;
+    }
+    if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
+  } else {
+    // M2M, M2L and the periodic far images (counted once, rank 0) in branches
+    launches += launch_far_chain(far, true, do_periodic);
   }
-  if (timing) ANKH_CUDA(cudaEventRecord(ev_[2], st));
-  // far field: M2L (fmm.cpp:238-276)
-  // + periodic far images (fmm.cpp:421-427), counted once (rank 0), off the
-  // timed path here (serial mode runs it after P2P)
-  launches += launch_m2l_classes(far, !serial, !serial && do_periodic);
-  if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
   if (!serial) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
   const int n_near_parts =
@@ -789,12 +819,13 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   }
   if (!serial) ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[5], st));
-  // self energy: rank 0 sums all N (or, sliced, every shard its slice)
-  const bool count_self = include_self_ || (slice_src_ && mode != 3);
+  // self energy: per-leaf sums from P2M over this shard's P2M rows -- split
+  // across shards when P2M is (shard_upward_), else counted by rank 0
+  const bool count_self = include_self_ || shard_upward_;
   launch_finalize(d_near_part_, n_near_parts, d_pair_count_, leaf_end_ - leaf_begin_, d_far_part_,
-                  n_tiles_,
-                  d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
-                  count_self ? 1 : 0, d_fin_scratch_, d_res_, st);
+                  n_tiles_, d_self_leaf_ + p2m_begin_, static_cast<int>(p2m_end_ - p2m_begin_),
+                  -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0, count_self ? 1 : 0, d_fin_scratch_, d_res_,
+                  st);
   ++launches;
   // shards: one all-reduce of the energy / counter / flag vector (the path's
   // only exchange besides the leaf all-gather), grouped with the MIN of the
@@ -813,47 +844,99 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   launches_ = launches;
 }
 
-// The rank classes of M2L (one kernel instantiation per padded rank) in
-// parallel branches: greedy longest-first over `far` and the kM2LStreams extra
-// streams by estimated work (tiles x padded rank), joined back into `far`.
-// With `with_periodic` the far-image term (independent of M2L) follows on the
-// least-loaded branch.
-std::uint32_t Plan::launch_m2l_classes(cudaStream_t far, bool fork, bool with_periodic) {
+// The far chain after the leaf level is complete: M2M (fmm.cpp:203-236),
+// M2L by rank class (fmm.cpp:238-276; one kernel instantiation per padded
+// rank) and, with `with_periodic`, the far-image term (fmm.cpp:421-427).
+// Unforked: back to back on `far`.  Forked: the classes' leaf-level tiles
+// (no M2M dependency) start at once on the kM2LStreams side branches while
+// the M2M chain runs on `far`; the coarse-level tiles and the periodic term
+// follow M2M on the least-loaded branches (greedy by tiles x padded rank);
+// every branch joins back into `far`.
+std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_periodic) {
+  std::uint32_t launches = 0;
   std::vector<int> cls;
   for (int c = 1; c <= kMaxKp8; ++c)
     if (class_range_[c].second > 0) cls.push_back(c);
-  std::sort(cls.begin(), cls.end(), [&](int a, int b) {
-    return static_cast<long long>(class_range_[a].second) * a > static_cast<long long>(class_range_[b].second) * b;
+  auto work = [&](int c, int tiles) { return static_cast<long long>(tiles) * c; };
+  auto m2l = [&](int c, int first, int count, cudaStream_t s) {
+    if (count <= 0) return;
+    launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, count, c, d_tile_ids_ + first, d_inst_, K, Kp,
+               d_far_part_, s);
+    ++launches;
+  };
+  auto m2m = [&](cudaStream_t s) {
+    for (int l = depth - 1; l >= 0; --l) {
+      launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, s);
+      ++launches;
+    }
+  };
+  if (!fork) {
+    m2m(far);
+    for (int c : cls) m2l(c, class_range_[c].first, class_range_[c].second, far);
+    if (with_periodic) {
+      launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, far);
+      ++launches;
+    }
+    return launches;
+  }
+  cudaStream_t lane[1 + kM2LStreams] = {far};
+  for (int k = 0; k < kM2LStreams; ++k) lane[1 + k] = m2l_streams_[k];
+  long long load[1 + kM2LStreams] = {};
+  bool forked[1 + kM2LStreams] = {true}, after_m2m[1 + kM2LStreams] = {true};
+  ANKH_CUDA(cudaEventRecord(ev_m2l_fork_, far));
+  auto pick = [&](int first) {
+    int k = first;
+    for (int j = first; j <= kM2LStreams; ++j)
+      if (load[j] < load[k]) k = j;
+    if (!forked[k]) {
+      ANKH_CUDA(cudaStreamWaitEvent(lane[k], ev_m2l_fork_, 0));
+      forked[k] = true;
+    }
+    return k;
+  };
+  // leaf-level tiles beside the M2M chain, largest first
+  std::vector<int> order = cls;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return work(a, class_leaf_[a]) > work(b, class_leaf_[b]); });
+  for (int c : order) {
+    if (class_leaf_[c] == 0 || !m2l_split_) continue;
+    const int k = pick(1);
+    load[k] += work(c, class_leaf_[c]);
+    m2l(c, class_range_[c].first, class_leaf_[c], lane[k]);
+  }
+  m2m(far);
+  ANKH_CUDA(cudaEventRecord(ev_m2m_done_, far));
+  auto after = [&](int k) {
+    if (!after_m2m[k]) {
+      ANKH_CUDA(cudaStreamWaitEvent(lane[k], ev_m2m_done_, 0));
+      after_m2m[k] = true;
+    }
+  };
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    const int ra = class_range_[a].second - (m2l_split_ ? class_leaf_[a] : 0);
+    const int rb_ = class_range_[b].second - (m2l_split_ ? class_leaf_[b] : 0);
+    return work(a, ra) > work(b, rb_);
   });
-  const int lanes = fork ? std::max(1, std::min<int>(1 + kM2LStreams, static_cast<int>(cls.size()))) : 1;
-  if (lanes > 1) ANKH_CUDA(cudaEventRecord(ev_m2l_fork_, far));
-  std::vector<long long> load(lanes, 0);
-  std::vector<bool> used(lanes, false);
-  for (int c : cls) {
-    const int k = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-    load[k] += static_cast<long long>(class_range_[c].second) * c;
-    cudaStream_t s = k == 0 ? far : m2l_streams_[k - 1];
-    if (k > 0 && !used[k]) ANKH_CUDA(cudaStreamWaitEvent(s, ev_m2l_fork_, 0));
-    used[k] = true;
-    const auto r = class_range_[c];
-    launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c, d_tile_ids_ + r.first, d_inst_, K,
-               Kp, d_far_part_, s);
+  for (int c : order) {
+    const int skip = m2l_split_ ? class_leaf_[c] : 0;
+    const int rest = class_range_[c].second - skip;
+    if (rest <= 0) continue;
+    const int k = pick(0);
+    after(k);
+    load[k] += work(c, rest);
+    m2l(c, class_range_[c].first + skip, rest, lane[k]);
   }
-  std::uint32_t extra = 0;
   if (with_periodic) {
-    const int k = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-    cudaStream_t s = k == 0 ? far : m2l_streams_[k - 1];
-    if (k > 0 && !used[k]) ANKH_CUDA(cudaStreamWaitEvent(s, ev_m2l_fork_, 0));
-    used[k] = true;
-    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, s);
-    extra = 1;
+    const int k = pick(0);
+    after(k);
+    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, lane[k]);
+    ++launches;
   }
-  for (int k = 1; k < lanes; ++k)
-    if (used[k]) {
-      ANKH_CUDA(cudaEventRecord(ev_m2l_join_[k - 1], m2l_streams_[k - 1]));
+  for (int k = 1; k <= kM2LStreams; ++k)
+    if (forked[k]) {
+      ANKH_CUDA(cudaEventRecord(ev_m2l_join_[k - 1], lane[k]));
       ANKH_CUDA(cudaStreamWaitEvent(far, ev_m2l_join_[k - 1], 0));
     }
-  return static_cast<std::uint32_t>(cls.size()) + extra;
+  return launches;
 }
 
 void Plan::exchange_leaves(cudaStream_t st) {
@@ -906,7 +989,7 @@ void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
       throw;
     }
     ANKH_CUDA(cudaStreamEndCapture(st, &g));
-    const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
+    const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(g);
     ANKH_CUDA(e);
     graph_pos_ = d_pos;
@@ -941,7 +1024,7 @@ void Plan::stream_setup() {
     d_list_p2p_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
     ANKH_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_sbounds_), 2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
     ANKH_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
-    ANKH_CUDA(cudaStreamCreateWithFlags(&gather_stream_, cudaStreamNonBlocking));
+    ANKH_CUDA(cudaStreamCreateWithPriority(&gather_stream_, cudaStreamNonBlocking, hi_prio_));
     for (cudaEvent_t* e : {&ev_s_start_, &ev_s_pos_, &ev_s_sorted_})
       ANKH_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (int c = 0; c < kMaxStreamChunks; ++c) {
@@ -961,7 +1044,7 @@ void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, 
   ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
   launch_init_result(res, st);
   const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
-  launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_, d_self_part_, res, st);
+  launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, res, st);
   launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_, d_off_, d_keys2_,
                        d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
   launch_stream_prepare(d_off_, d_idx2_, n, depth, periodic ? 1 : 0, static_cast<unsigned>(chunk), C, d_inv_,
@@ -1034,14 +1117,15 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   for (int c = 0; c < C; ++c) {
     const std::size_t i0 = c * chunk, i1 = std::min(n, i0 + chunk);
     ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_chunk_[c], 0));
-    launch_src_chunk(d_pos_, d_src_, d_inv_, i0, i1, cfg.xi, d_self_part_, d_res_, d_part_, gather_stream_);
+    launch_src_chunk(d_pos_, d_src_, d_inv_, i0, i1, d_res_, d_part_, gather_stream_);
     ANKH_CUDA(cudaEventRecord(ev_s_gath_[c], gather_stream_));
     mark("gather " + std::to_string(c), gather_stream_);
     const unsigned n_m = h_sbounds_[c + 1] - h_sbounds_[c];
     const unsigned n_p = h_sbounds_[C + 1 + c + 1] - h_sbounds_[C + 1 + c];
     if (n_m) {
       ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[c], 0));
-      launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, 0u, 0u, side_stream_,
+      launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, d_self_leaf_, cfg.xi, 0u,
+                 0u, side_stream_,
                  d_list_p2m_, d_sbounds_ + c, n_m);
       ++launches;
       mark("p2m " + std::to_string(c) + " (" + std::to_string(n_m) + " leaves)", side_stream_);
@@ -1065,24 +1149,34 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
     if (!near_started) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
     ANKH_CUDA(cudaEventRecord(ev_t_[3], st));
   }
-  for (int l = depth - 1; l >= 0; --l) {
-    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, side_stream_);
-    ++launches;
+  if (timing) {  // phase spans: M2M, M2L, periodic back to back
+    for (int l = depth - 1; l >= 0; --l) {
+      launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, side_stream_);
+      ++launches;
+    }
+    ANKH_CUDA(cudaEventRecord(ev_t_[4], side_stream_));
+    for (int c = 1; c <= kMaxKp8; ++c) {
+      const auto r = class_range_[c];
+      if (r.second == 0) continue;
+      launch_m2l(d_exp_, d_level_off_, d_factors_, d_ops_, d_tiles_, r.second, c, d_tile_ids_ + r.first, d_inst_,
+                 K, Kp, d_far_part_, side_stream_);
+      ++launches;
+    }
+    ANKH_CUDA(cudaEventRecord(ev_t_[5], side_stream_));
+    if (do_periodic) {
+      launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, side_stream_);
+      ++launches;
+    }
+    ANKH_CUDA(cudaEventRecord(ev_t_[6], side_stream_));
+  } else {
+    launches += launch_far_chain(side_stream_, true, do_periodic);
   }
-  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[4], side_stream_));
-  launches += launch_m2l_classes(side_stream_, !timing, false);
-  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[5], side_stream_));
-  if (do_periodic) {
-    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, side_stream_);
-    ++launches;
-  }
-  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[6], side_stream_));
   mark("far chain (m2m, m2l, periodic)", side_stream_);
   ANKH_CUDA(cudaEventRecord(ev_join_, side_stream_));
   ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[7], st));
   launch_finalize(d_near_part_, n_near_parts, d_pair_count_, leaf_end_ - leaf_begin_, d_far_part_, n_tiles_,
-                  d_self_part_, n_self_blocks_, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
+                  d_self_leaf_, n_leaves, -cfg.xi * kInvSqrtPi, d_per_, do_periodic ? 1 : 0,
                   include_self_ ? 1 : 0, d_fin_scratch_, d_res_, st);
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[8], st));
@@ -1147,8 +1241,7 @@ void Plan::set_positions(const double* h_pos, cudaStream_t st) {
     ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
     launch_init_result(d_res_pos_, st);
     const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
-    launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, cfg.xi, d_keys_, d_idx_, d_counts_,
-               d_self_part_, d_res_pos_, st);
+    launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, d_res_pos_, st);
     launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_,
                          d_off_, d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
   }
@@ -1191,7 +1284,7 @@ void Plan::enqueue_sources(const double* h_src, cudaStream_t st) {
       throw;
     }
     ANKH_CUDA(cudaStreamEndCapture(st, &g));
-    const cudaError_t e = cudaGraphInstantiate(&graph_src_exec_, g, 0);
+    const cudaError_t e = cudaGraphInstantiate(&graph_src_exec_, g, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(g);
     ANKH_CUDA(e);
   }

@@ -135,7 +135,7 @@ class Plan {
   void stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C);
   void enqueue_streamed(const double* h_pos, const double* h_src, cudaStream_t st);
   bool stream_bound_ = false;  // set_positions built the streamed path's lists
-  static constexpr int kMaxStreamChunks = 32;
+  static constexpr int kMaxStreamChunks = ankh_b200::kMaxStreamChunks;
   int stream_chunks_ = 8;
   bool stream_init_ = false;
   unsigned *d_inv_ = nullptr, *d_scnt_ = nullptr, *d_sbounds_ = nullptr, *d_scursor_ = nullptr;
@@ -157,13 +157,16 @@ class Plan {
   int device_ = 0;
   cudaStream_t stream_ = nullptr;
   cudaStream_t side_stream_ = nullptr;  // far-field chain, concurrent with P2P
+  int hi_prio_ = 0;                     // stream priority of the far chain / gathers
+  bool m2l_split_ = false;              // leaf-level M2L tiles beside M2M (ANKH_M2L_SPLIT=1)
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   // M2L rank classes run as parallel branches (their tails overlap; the
   // small latency-bound classes hide under the large ones)
   static constexpr int kM2LStreams = 3;
   cudaStream_t m2l_streams_[kM2LStreams] = {};
-  cudaEvent_t ev_m2l_fork_ = nullptr, ev_m2l_join_[kM2LStreams] = {};
-  std::uint32_t launch_m2l_classes(cudaStream_t far, bool fork, bool with_periodic);
+  cudaEvent_t ev_m2l_fork_ = nullptr, ev_m2m_done_ = nullptr, ev_m2l_join_[kM2LStreams] = {};
+  std::vector<int> class_leaf_;  // leading leaf-level tiles of each class's range
+  std::uint32_t launch_far_chain(cudaStream_t far, bool fork, bool with_periodic);
   // CUDA-graph replay of launch_all for repeated inputs
   cudaGraphExec_t graph_exec_ = nullptr;
   const double *graph_pos_ = nullptr, *graph_src_ = nullptr;
@@ -188,6 +191,10 @@ class Plan {
   // with NCCL attached the per-slice first violations are MIN-reduced (phase
   // API: each shard reports its slice, positions are checked by all)
   bool slice_src_ = false;
+  // the record gather visits every leaf: it validates the moments, so
+  // binning reads positions only
+  bool gather_checks_src() const { return !slice_src_ && d_need_ == nullptr && !csr_only_; }
+  double* d_self_leaf_ = nullptr;  // per Morton leaf: self-energy summand sums (P2M)
   std::size_t src_i0_ = 0, src_i1_ = 0;
 
   // inputs / sort
@@ -216,10 +223,8 @@ class Plan {
   std::size_t n_factors_ = 0;  // doubles in d_factors_ (m2l_factors reads them back)
   std::vector<M2LOp> h_ops_;
   // partials
-  double *d_near_part_ = nullptr, *d_far_part_ = nullptr, *d_self_part_ = nullptr,
-         *d_per_ = nullptr;
+  double *d_near_part_ = nullptr, *d_far_part_ = nullptr, *d_per_ = nullptr;
   unsigned long long* d_pair_count_ = nullptr;
-  int n_self_blocks_ = 0;
   DevResult* d_res_ = nullptr;
   DevResult* h_res_ = nullptr;
   P2PRadial radial_{};  // near-field radial polynomials (fit_radial)
