@@ -88,7 +88,10 @@ __global__ void __launch_bounds__(256) k_scatter(const unsigned* __restrict__ ke
   unsorted[offsets[keys[i]] + slots[i]] = static_cast<unsigned>(i);
 }
 
-constexpr int kLeafThreads = 128;
+#ifndef ANKH_LEAF_THREADS
+#define ANKH_LEAF_THREADS 128
+#endif
+constexpr int kLeafThreads = ANKH_LEAF_THREADS;
 constexpr int kLeafSmem = 512;  // leaves up to this size are sorted in shared memory
 
 __device__ __forceinline__ void write_record(const double* __restrict__ pos,
@@ -278,18 +281,24 @@ __global__ void __launch_bounds__(256) k_stream_ready(const unsigned* __restrict
 
 // bounds[0..C] / bounds[C+1..2C+1]: exclusive scans of the two count sets;
 // cursors reset to the bucket starts
+// (bounds also stored to host_bounds -- mapped page-locked memory the host
+// reads after the kernel: no device-to-host copy queued behind the moment
+// chunks' host-to-device copies)
 __global__ void k_stream_scan(const unsigned* __restrict__ cnt, int n_chunks, unsigned* __restrict__ bounds,
-                              unsigned* __restrict__ cursor) {
+                              unsigned* __restrict__ cursor, unsigned* host_bounds) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   for (int s = 0; s < 2; ++s) {
     unsigned acc = 0;
     for (int c = 0; c < n_chunks; ++c) {
       bounds[s * (n_chunks + 1) + c] = acc;
+      if (host_bounds) host_bounds[s * (n_chunks + 1) + c] = acc;
       cursor[s * n_chunks + c] = acc;
       acc += cnt[s * n_chunks + c];
     }
     bounds[s * (n_chunks + 1) + n_chunks] = acc;
+    if (host_bounds) host_bounds[s * (n_chunks + 1) + n_chunks] = acc;
   }
+  __threadfence_system();
 }
 
 // Per-chunk leaf lists: each block reserves one contiguous range per key in
@@ -396,13 +405,13 @@ void launch_src_chunk(const double* pos, const double* src, const unsigned* inv,
 void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,
                            int periodic, unsigned chunk, int n_chunks, unsigned* inv,
                            unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
-                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st) {
+                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st, unsigned* host_bounds) {
   const unsigned n_leaves = 1u << (3 * depth);
   if (n > 0) k_inverse<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(sorted, n, inv);
   cudaMemsetAsync(cnt, 0, 2 * n_chunks * sizeof(unsigned), st);
   k_stream_ready<<<(n_leaves + 255) / 256, 256, 0, st>>>(offsets, sorted, depth, periodic, chunk,
                                                         n_chunks, ready, cnt);
-  k_stream_scan<<<1, 32, 0, st>>>(cnt, n_chunks, bounds, cursor);
+  k_stream_scan<<<1, 32, 0, st>>>(cnt, n_chunks, bounds, cursor, host_bounds);
   k_stream_lists<<<(n_leaves + 255) / 256, 256, 0, st>>>(ready, n_leaves, n_chunks, cursor, list_p2m,
                                                         list_p2p);
 }

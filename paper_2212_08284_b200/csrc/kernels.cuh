@@ -106,7 +106,8 @@ void launch_src_chunk(const double* pos, const double* src, const unsigned* inv,
 void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,
                            int periodic, unsigned chunk, int n_chunks, unsigned* inv,
                            unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
-                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st);
+                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st,
+                           unsigned* host_bounds = nullptr);
 void launch_m2m(const double* child, double* parent, int parent_level, int order,
                 const double* m2m, cudaStream_t st);
 void launch_m2l(const double* exp, const long long* level_off, const double* factors,

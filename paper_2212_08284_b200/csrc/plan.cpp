@@ -1022,7 +1022,9 @@ void Plan::stream_setup() {
     d_sbounds_ = static_cast<unsigned*>(dalloc(2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
     d_list_p2m_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
     d_list_p2p_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
-    ANKH_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_sbounds_), 2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
+    ANKH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_sbounds_), 2 * (kMaxStreamChunks + 1) * sizeof(unsigned),
+                            cudaHostAllocMapped));
+    ANKH_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_sbounds_dev_), h_sbounds_, 0));
     ANKH_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
     ANKH_CUDA(cudaStreamCreateWithPriority(&gather_stream_, cudaStreamNonBlocking, hi_prio_));
     for (cudaEvent_t* e : {&ev_s_start_, &ev_s_pos_, &ev_s_sorted_})
@@ -1048,8 +1050,7 @@ void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, 
   launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_, d_off_, d_keys2_,
                        d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
   launch_stream_prepare(d_off_, d_idx2_, n, depth, periodic ? 1 : 0, static_cast<unsigned>(chunk), C, d_inv_,
-                        d_ready_, d_scnt_, d_sbounds_, d_scursor_, d_list_p2m_, d_list_p2p_, st);
-  ANKH_CUDA(cudaMemcpyAsync(h_sbounds_, d_sbounds_, 2 * (C + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+                        d_ready_, d_scnt_, d_sbounds_, d_scursor_, d_list_p2m_, d_list_p2p_, st, h_sbounds_dev_);
 }
 
 std::size_t Plan::stream_chunk_size() const {

@@ -140,6 +140,7 @@ class Plan {
   bool stream_init_ = false;
   unsigned *d_inv_ = nullptr, *d_scnt_ = nullptr, *d_sbounds_ = nullptr, *d_scursor_ = nullptr;
   unsigned *d_list_p2m_ = nullptr, *d_list_p2p_ = nullptr, *h_sbounds_ = nullptr;
+  unsigned* h_sbounds_dev_ = nullptr;  // its device alias (k_stream_scan writes it)
   unsigned char* d_ready_ = nullptr;
   cudaStream_t copy_stream_ = nullptr, gather_stream_ = nullptr;
   cudaEvent_t ev_s_start_ = nullptr, ev_s_pos_ = nullptr, ev_s_sorted_ = nullptr;

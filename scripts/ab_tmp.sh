@@ -1,6 +1,3 @@
-mkdir -p gpurun_out/s2ab
-for i in 1 2; do
-AB_TAG=split python scripts/ab_quick.py; ANKH_M2L_SPLIT=0 AB_TAG=nosplit python scripts/ab_quick.py
-WORLD=8 python scripts/shard_step.py; ANKH_M2L_SPLIT=0 WORLD=8 python scripts/shard_step.py
-done
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s2ab/stream.csv python scripts/stream_trace.py > /dev/null 2>&1; echo ncu $?
+mkdir -p gpurun_out/s2ab2
+for r in 1 2; do for v in t32 t64 t128; do ANKH_B200_LIB=$PWD/paper_2212_08284_b200/variants/libankh_b200_bin_$v.so python scripts/p2p_ab.py; done; done
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s2ab2/stream.csv python scripts/stream_trace.py > /dev/null 2>&1; echo ncu $?
