@@ -179,6 +179,12 @@ int ankh_device_copy_v1(void* dst, const void* src, size_t bytes, void* stream, 
  *     exchange in its CUDA graph and P2P concurrent with the far chain) can be
  *     timed.  Energies are this shard's partials. */
 int ankh_plan_attach_loopback_v1(ankh_plan_v1* plan, char* err, size_t errlen);
+/* (d) Tests on one GPU: the `world` plans of one sharding (ranks 0..world-1,
+ *     one process, one device) exchange by stream-ordered pushes -- at its
+ *     exchange point each shard copies its own expansion slabs into the other
+ *     plans' arrays.  From the second evaluation of the same inputs on, every
+ *     shard reports its true partial energies (sum over shards = the job). */
+int ankh_plan_attach_push_group_v1(ankh_plan_v1** plans, int world, char* err, size_t errlen);
 
 /* ---- spatial sharding (host only; no device needed) ----
  * Shards own contiguous Morton ranges of leaves; a level-l cell belongs to the

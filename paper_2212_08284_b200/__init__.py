@@ -14,6 +14,7 @@ from .api import (  # noqa: F401
     InvalidArgument,
     ParticleSystem,
     Plan,
+    attach_push_group,
     build_tree_csr,
     default_depth,
     device_copy,

@@ -42,6 +42,7 @@ __all__ = [
     "nccl_unique_id",
     "device_copy",
     "exchange_leaf_levels",
+    "attach_push_group",
 ]
 
 
@@ -267,6 +268,16 @@ def exchange_leaf_levels(plans, stream: int = 0) -> None:
                 continue
             off = b * stride * 8
             device_copy(dst + off, src + off, (e - b) * stride * 8, stream)
+
+
+def attach_push_group(plans) -> None:
+    """Tests on one GPU: the shards of one sharding (plans[r] has rank r)
+    exchange by stream-ordered pushes of their expansion slabs into each
+    other's arrays; from the second evaluation of the same inputs on, each
+    reports its true partial energies (their sum is the job's)."""
+    arr = (ctypes.c_void_p * len(plans))(*[p._h for p in plans])
+    err = ctypes.create_string_buffer(512)
+    _check(lib().ankh_plan_attach_push_group_v1(arr, len(plans), err, 512), err)
 
 
 def build_tree_csr(positions, box_radius: float, depth: int) -> Tuple[np.ndarray, np.ndarray]:

@@ -294,6 +294,22 @@ int ankh_plan_attach_loopback_v1(ankh_plan_v1* plan, char* err, size_t errlen) {
   });
 }
 
+int ankh_plan_attach_push_group_v1(ankh_plan_v1** plans, int world, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!plans || world < 1) throw AnkhError(ANKH_INVALID_ARGUMENT, "bad plan group");
+    std::vector<double*> bases(world);
+    for (int r = 0; r < world; ++r) {
+      if (!plans[r] || plans[r]->plan->cfg.world != world || plans[r]->plan->cfg.rank != r)
+        throw AnkhError(ANKH_INVALID_ARGUMENT, "plan group must hold ranks 0..world-1 of one sharding");
+      bases[r] = plans[r]->plan->expansions_base();
+    }
+    for (int r = 0; r < world; ++r) {
+      std::lock_guard<std::mutex> lock(plans[r]->mu);
+      plans[r]->plan->attach_collective(ankh_b200::make_push_collective(r, world, bases));
+    }
+  });
+}
+
 int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* begin, int64_t* end) {
   if (depth < 1 || depth > 8 || world < 1 || rank < 0 || rank >= world || !begin || !end)
     return ANKH_INVALID_ARGUMENT;

@@ -83,6 +83,18 @@ class NcclCollective final : public Collective {
   void allreduce_sum(double* buf, std::size_t count, cudaStream_t st) override {
     check(nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, comm_, st), "ncclAllReduce");
   }
+  void allgather_inplace_group(double* const* recv, const std::size_t* count, int n,
+                               cudaStream_t st) override {
+    check(nccl().GroupStart(), "ncclGroupStart");
+    int bad = kNcclSuccess;
+    for (int k = 0; k < n; ++k) {
+      const int r = nccl().AllGather(recv[k] + static_cast<std::size_t>(rank_) * count[k], recv[k], count[k],
+                                     kNcclFloat64, comm_, st);
+      if (r != kNcclSuccess && bad == kNcclSuccess) bad = r;
+    }
+    check(nccl().GroupEnd(), "ncclGroupEnd");
+    check(bad, "ncclAllGather");
+  }
   void allreduce_sum_min(double* sum, std::size_t n_sum, unsigned long long* mins, std::size_t n_min,
                          cudaStream_t st) override {
     // one grouped launch for both reductions
@@ -126,6 +138,10 @@ class LoopbackCollective final : public Collective {
                                   count * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
   void allreduce_sum(double*, std::size_t, cudaStream_t) override {}
+  void allgather_inplace_group(double* const* recv, const std::size_t* count, int n,
+                               cudaStream_t st) override {
+    for (int k = 0; k < n; ++k) allgather_inplace(recv[k], count[k], st);
+  }
   void allreduce_sum_min(double*, std::size_t, unsigned long long*, std::size_t, cudaStream_t) override {}
   int rank() const override { return rank_; }
   int world() const override { return world_; }
@@ -138,6 +154,39 @@ class LoopbackCollective final : public Collective {
 
 Collective* make_loopback_collective(int rank, int world) {
   return new LoopbackCollective(rank, world);
+}
+
+namespace {
+
+class PushCollective final : public Collective {
+ public:
+  PushCollective(int rank, int world, std::vector<double*> bases)
+      : rank_(rank), world_(world), bases_(std::move(bases)) {}
+  void allgather_inplace(double* recv, std::size_t count, cudaStream_t st) override {
+    const std::ptrdiff_t off = (recv - bases_[rank_]) + static_cast<std::ptrdiff_t>(rank_ * count);
+    for (int q = 0; q < world_; ++q)
+      if (q != rank_)
+        ANKH_CUDA(cudaMemcpyAsync(bases_[q] + off, bases_[rank_] + off, count * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, st));
+  }
+  void allgather_inplace_group(double* const* recv, const std::size_t* count, int n,
+                               cudaStream_t st) override {
+    for (int k = 0; k < n; ++k) allgather_inplace(recv[k], count[k], st);
+  }
+  void allreduce_sum(double*, std::size_t, cudaStream_t) override {}
+  void allreduce_sum_min(double*, std::size_t, unsigned long long*, std::size_t, cudaStream_t) override {}
+  int rank() const override { return rank_; }
+  int world() const override { return world_; }
+
+ private:
+  int rank_, world_;
+  std::vector<double*> bases_;
+};
+
+}  // namespace
+
+Collective* make_push_collective(int rank, int world, const std::vector<double*>& bases) {
+  return new PushCollective(rank, world, bases);
 }
 
 }  // namespace ankh_b200

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstddef>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace ankh_b200 {
@@ -17,6 +18,10 @@ class Collective {
   /// recv holds world * count doubles; this rank's contribution already sits at
   /// recv + rank * count (in-place all-gather).
   virtual void allgather_inplace(double* recv, std::size_t count, cudaStream_t st) = 0;
+  /// several in-place all-gathers (recv[k] holds world * count[k] doubles),
+  /// issued as one group
+  virtual void allgather_inplace_group(double* const* recv, const std::size_t* count, int n,
+                                       cudaStream_t st) = 0;
   virtual void allreduce_sum(double* buf, std::size_t count, cudaStream_t st) = 0;
   /// sum over `sum[0, n_sum)` and minimum over `mins[0, n_min)`, together
   virtual void allreduce_sum_min(double* sum, std::size_t n_sum, unsigned long long* mins,
@@ -34,5 +39,12 @@ Collective* make_nccl_collective(const unsigned char id[128], int rank, int worl
 /// land in HBM as they would over NVLink, at HBM rather than NVLink speed),
 /// the all-reduce is the identity.  Reports then hold this shard's partial sums.
 Collective* make_loopback_collective(int rank, int world);
+/// Test stand-in for G shards in ONE process on one device: at its exchange
+/// point shard r copies (stream-ordered) its own slabs into the other shards'
+/// expansion arrays (bases[q], same layout); the all-reduces are identities.
+/// Shard r's M2L reads what the others pushed, so from the second evaluation
+/// of the same inputs on, every shard holds all slabs and reports its true
+/// partial energies.
+Collective* make_push_collective(int rank, int world, const std::vector<double*>& bases);
 
 }  // namespace ankh_b200

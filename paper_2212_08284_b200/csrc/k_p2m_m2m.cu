@@ -366,7 +366,8 @@ constexpr int kM2MThreads = 128;
 template <int L>
 __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ child,
                                                      double* __restrict__ parent, int level,
-                                                     const double* __restrict__ m2m_g) {
+                                                     const double* __restrict__ m2m_g,
+                                                     unsigned p_begin) {
   constexpr int L2 = L * L, K = L2 * L, KS = exp_stride(K);
   extern __shared__ __align__(16) double sm[];
   double* M = sm;               // 2 x L x L: M[c][i][a] = T_c(i, a)
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
   // Morton order: the children of parent p are rows 8p + (cx<<2 | cy<<1 | cz),
   // one contiguous 8 KS-double block: loaded as 16-B pieces, a batch of
   // loads in flight per thread before any shared-memory store
-  const unsigned pcell = blockIdx.x;
+  const unsigned pcell = p_begin + blockIdx.x;
   const double2* ch0 = reinterpret_cast<const double2*>(child + static_cast<std::size_t>(pcell) * 8 * KS);
   double2* V2 = reinterpret_cast<double2*>(V);
   constexpr int NV = 8 * KS / 2, kBatch = 8;
@@ -489,7 +490,7 @@ namespace {
 
 template <int L>
 void m2m_order(const double* child, double* parent, int parent_level, const double* m2m,
-               cudaStream_t st) {
+               cudaStream_t st, unsigned p_begin, unsigned p_count) {
   constexpr int K = L * L * L;
   const std::size_t smem = sizeof(double) * (2 * L * L + 8 * exp_stride(K) + 6 * K);
   static bool attr = false;
@@ -498,8 +499,8 @@ void m2m_order(const double* child, double* parent, int parent_level, const doub
                          static_cast<int>(smem));
     attr = true;
   }
-  const unsigned cells = 1u << (3 * parent_level);
-  k_m2m<L><<<cells, kM2MThreads, smem, st>>>(child, parent, parent_level, m2m);
+  const unsigned cells = p_count ? p_count : (1u << (3 * parent_level));
+  k_m2m<L><<<cells, kM2MThreads, smem, st>>>(child, parent, parent_level, m2m, p_begin);
 }
 
 }  // namespace
@@ -530,8 +531,8 @@ void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int ord
 }
 
 void launch_m2m(const double* child, double* parent, int parent_level, int order,
-                const double* m2m, cudaStream_t st) {
-#define ANKH_M2M(N) m2m_order<N>(child, parent, parent_level, m2m, st)
+                const double* m2m, cudaStream_t st, unsigned p_begin, unsigned p_count) {
+#define ANKH_M2M(N) m2m_order<N>(child, parent, parent_level, m2m, st, p_begin, p_count)
   ANKH_ORDER_SWITCH(order, ANKH_M2M)
 #undef ANKH_M2M
 }

@@ -215,6 +215,9 @@ void Plan::build_geometry() {
   shard_upward_ = cfg.world > 1 && (static_cast<long long>(n_leaves) % cfg.world) == 0;
   p2m_begin_ = shard_upward_ ? lb : 0;
   p2m_end_ = shard_upward_ ? le : n_leaves;
+  exch_level_ = depth;
+  if (shard_upward_)
+    for (int l = depth; l >= 1 && (1ll << (3 * l)) % cfg.world == 0; --l) exch_level_ = l;
   slice_src_ = shard_upward_ && std::getenv("ANKH_SHARD_FULL_SRC") == nullptr;
   if (slice_src_) {
     const std::size_t blocks = (n + 255) / 256;
@@ -785,9 +788,10 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     return;
   }
   // ... the leaf level completed by the shard exchange, then M2M (fmm.cpp:203-236)
-  if (mode == 0 || mode == 3) exchange_leaves(far);
+  m2m_top_ = depth - 1;
+  if (mode == 0 || mode == 3) launches += exchange_upward(far);
   if (serial) {
-    for (int l = depth - 1; l >= 0; --l) {
+    for (int l = m2m_top_; l >= 0; --l) {
       launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, far);
       ++launches;
     }
@@ -865,7 +869,7 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
     ++launches;
   };
   auto m2m = [&](cudaStream_t s) {
-    for (int l = depth - 1; l >= 0; --l) {
+    for (int l = m2m_top_; l >= 0; --l) {  // (levels below are done by exchange_upward)
       launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, s);
       ++launches;
     }
@@ -939,13 +943,32 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
   return launches;
 }
 
-void Plan::exchange_leaves(cudaStream_t st) {
-  if (!coll_ || !shard_upward_) return;
-  // in-place all-gather of the Morton-ordered leaf level: rank r owns rows
-  // [r n_leaves / world, (r+1) n_leaves / world)
-  double* leaf_level = d_exp_ + level_off_[depth];
-  const std::size_t count = static_cast<std::size_t>(p2m_end_ - p2m_begin_) * Kp;
-  coll_->allgather_inplace(leaf_level, count, st);
+// Sharded upward pass with a collective attached: M2M of this shard's own
+// subtree cells for the parent levels exch_level_ .. depth-1 (at level l the
+// shard owns Morton cells [r 8^l / G, (r+1) 8^l / G) -- whole subtrees, since
+// G | 8^exch_level_), then ONE grouped in-place all-gather of levels
+// exch_level_ .. depth; the levels above are completed redundantly by every
+// shard (m2m_top_).  Returns the launches.
+std::uint32_t Plan::exchange_upward(cudaStream_t st) {
+  m2m_top_ = depth - 1;
+  if (!coll_ || !shard_upward_) return 0;
+  std::uint32_t launches = 0;
+  const long long G = cfg.world, r = cfg.rank;
+  for (int l = depth - 1; l >= exch_level_; --l) {
+    const long long cells = 1ll << (3 * l);
+    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, st,
+               static_cast<unsigned>(cells * r / G), static_cast<unsigned>(cells / G));
+    ++launches;
+  }
+  std::vector<double*> recv;
+  std::vector<std::size_t> count;
+  for (int l = exch_level_; l <= depth; ++l) {
+    recv.push_back(d_exp_ + level_off_[l]);
+    count.push_back(static_cast<std::size_t>((1ll << (3 * l)) / G) * Kp);
+  }
+  coll_->allgather_inplace_group(recv.data(), count.data(), static_cast<int>(recv.size()), st);
+  m2m_top_ = exch_level_ - 1;
+  return launches;
 }
 
 void Plan::enqueue(const double* d_pos, const double* d_src, cudaStream_t st) {
@@ -1170,6 +1193,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
     }
     ANKH_CUDA(cudaEventRecord(ev_t_[6], side_stream_));
   } else {
+    m2m_top_ = depth - 1;
     launches += launch_far_chain(side_stream_, true, do_periodic);
   }
   mark("far chain (m2m, m2l, periodic)", side_stream_);

@@ -96,6 +96,7 @@ class Plan {
   /// Device pointer to the Morton-ordered leaf level (rows of Kp doubles) and
   /// this shard's P2M row range.
   double* leaf_level(std::int64_t* begin, std::int64_t* end, int* row_stride);
+  double* expansions_base() const { return d_exp_; }
   /// Attach an NCCL (or other) collective: the plan then all-gathers the leaf
   /// level and all-reduces the result itself; reports carry job totals.
   void attach_collective(Collective* c);
@@ -149,7 +150,9 @@ class Plan {
   cudaEvent_t ev_t_[9] = {};
   bool streamed_last_ = false;
   void validate_only(const double* d_pos, const double* d_src, cudaStream_t st);
-  void exchange_leaves(cudaStream_t st);
+  std::uint32_t exchange_upward(cudaStream_t st);
+  int exch_level_ = 0;  // lowest level split evenly across shards (G | 8^l)
+  int m2m_top_ = 0;     // highest parent level the far chain still computes (all cells)
 
   std::unique_ptr<Collective> coll_;
   bool shard_upward_ = false;               // P2M split across shards (+ all-gather)

@@ -532,6 +532,36 @@ def test_loopback_shards_sliced_moments(cuda, world):
         p.close()
 
 
+@pytest.mark.parametrize("world, p", [(2, 15), (4, 15), (8, 15), (8, 0)])
+def test_push_group_shards_match_single_gpu(cuda, world, p):
+    """The collective-attached schedule end to end on one GPU: every shard
+    runs its own graph (sliced moment checks, P2M and M2M of its own subtree,
+    grouped all-gather of the levels it shares, redundant top levels, its M2L
+    and P2P share) and exchanges through stream-ordered pushes into the other
+    shards' arrays.  From the second evaluation on, the shards' partial
+    energies -- far field included -- sum to the single-GPU result."""
+    torch = cuda
+    pos, src, rb, cfg = inputs.make_config(1)  # depth 3
+    n = pos.shape[0]
+    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4, p=p)
+    dp, ds = torch.from_numpy(pos).cuda(), torch.from_numpy(src).cuda()
+    whole = ankh.Plan(n, rb, ec).energy_device(dp, ds)
+    plans = [ankh.Plan(n, rb, ec, rank=r, world=world, phase_timing=False) for r in range(world)]
+    ankh.attach_push_group(plans)
+    for it in range(4):  # plain launch, graph capture, graph replays
+        reps = [pl.energy_device(dp, ds) for pl in plans]
+        torch.cuda.synchronize()
+        if it == 0:
+            continue  # the first round reads slabs the others had not pushed yet
+        for k in ("e_near", "e_far", "e_self", "e_periodic_far"):
+            got = sum(getattr(r, k) for r in reps)
+            assert abs(got - getattr(whole, k)) <= 1e-12 * abs(getattr(whole, k)) + 1e-15, (it, k)
+        assert abs(sum(r.e_total for r in reps) - whole.e_total) <= 1e-12 * abs(whole.e_total)
+        assert sum(r.near_pairs for r in reps) == whole.near_pairs
+    for pl in plans:
+        pl.close()
+
+
 def test_sliced_moment_validation(cuda):
     """Sliced moment pass: positions are validated by every shard, moments
     by the shard whose index slice holds them (the NCCL MIN all-reduce makes
