@@ -61,26 +61,28 @@ def hbm_peak_gbs():
 
 
 def phase_rooflines(n, L, depth, ph_ms, pairs, far_flops, fp64_peak, hbm_peak, dmma_peak=None,
-                    multipoles=True):
+                    multipoles=True, world=1):
     """% of roofline per phase, with SURVEY.md §8d's algorithmic counts
     (each add/mul/... of the reference formula = 1 flop; bytes = compulsory
     traffic).  Phase times are CUDA-event times on the launching stream (phase
-    timing serialises the far-field chain and the near field)."""
+    timing serialises the far-field chain and the near field).  With world > 1
+    the times are one shard's: P2M/M2M work is its 1/world share (binning
+    covers all N on every shard; `pairs` and `far_flops` are per shard)."""
     K = L ** 3
     cells = sum(8 ** l for l in range(depth + 1))
     children = cells - 1
     t = 10 if multipoles else 1
-    p2m_flops = n * (9 * (3 * (L - 2) + 2 * L * L + L) + t * (L + L * L + 2 * L ** 3))
-    m2m_flops = children * (6 * L ** 4 + L ** 3)
+    p2m_flops = n * (9 * (3 * (L - 2) + 2 * L * L + L) + t * (L + L * L + 2 * L ** 3)) / world
+    m2m_flops = children * (6 * L ** 4 + L ** 3) / world
     rows = {
         "bin_sort_gather": ("hbm", 256.0 * n, ph_ms["precompute"],
                             "256 B/atom (SURVEY §8d): read x + moments, keys/index sort, 112-B records out"),
         "p2m_m2m": ("fp64", float(p2m_flops + m2m_flops), ph_ms["interpolation"],
                     "P2M N[9(3(L-2)+2L^2+L)+10(L+L^2+2L^3)] + M2M (6L^4+L^3)/child"),
-        "m2l": ("dmma", float(far_flops), ph_ms["far_field"], "sum over instances 4kK+2k"),
+        "m2l": ("dmma", float(far_flops) if far_flops else None, ph_ms["far_field"], "sum over instances 4kK+2k"),
         "p2p": ("fp64", P2P_FLOP_PER_PAIR * pairs, ph_ms["near_field"], "229 flop per unordered pair"),
         "finalize": ("latency", None, ph_ms["self"],
-                     "final fixed-order reduction (self energy is fused into binning)"),
+                     "final fixed-order reduction (the self energy is summed per leaf inside P2M)"),
         "periodic_far": ("latency", None, ph_ms["periodic_far"], "one CTA, (2L-1)^3 DFT"),
     }
     out = {}
@@ -469,7 +471,7 @@ def main():
                          "traffic": traffic, "peak_source": "in-process DFMA probe (ankh_probe_fp64_tflops_v1)",
                          "algorithmic": f"{P2P_FLOP_PER_PAIR:.0f} flop/pair x {pairs} pairs per launch"},
             "phase_rooflines": phase_rooflines(n, L, plan.info()["depth"], ph_ms, pairs, far_flops,
-                                               fp64_peak, hbm_peak_gbs(), dmma_peak),
+                                               fp64_peak, hbm_peak_gbs(), dmma_peak, world=world),
             "roofline_m2l": {"kernel": "k_m2l (DMMA)", "bound": "fp64 tensor (DMMA)", "achieved": m2l_tflops,
                              "peak": dmma_peak, "peak_source": "in-process DMMA m8n8k4 probe (ankh_probe_dmma_tflops_v1)",
                              "unit": "TFLOP/s", "frac": (m2l_tflops / dmma_peak) if (m2l_tflops and dmma_peak) else None,

@@ -1352,12 +1352,9 @@ void Plan::result(ankh_report_v1* out) {
   // EnergyReport::component_sum order (types.hpp:132-134)
   out->e_total = out->e_self + out->e_near + out->e_far + out->e_periodic_far + out->e_reciprocal;
   out->near_pairs = static_cast<std::uint64_t>(r.red[kNearPairs]);
-  out->far_instances = 0;
+  out->far_instances = m2l_instances;  // this shard's (the instance lists are per shard)
+  out->far_flops = far_flops;
   out->gpu_launches = launches_;
-  if (cfg.world <= 1) {
-    out->far_instances = m2l_instances;
-    out->far_flops = far_flops;
-  }
   if (cfg.phase_timing && streamed_last_) {
     // overlapped phases: wall-clock span of each (they may sum to more than
     // the total); interpolation = chunk gathers + P2M + M2M, precompute =

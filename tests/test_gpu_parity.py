@@ -558,6 +558,7 @@ def test_push_group_shards_match_single_gpu(cuda, world, p):
             assert abs(got - getattr(whole, k)) <= 1e-12 * abs(getattr(whole, k)) + 1e-15, (it, k)
         assert abs(sum(r.e_total for r in reps) - whole.e_total) <= 1e-12 * abs(whole.e_total)
         assert sum(r.near_pairs for r in reps) == whole.near_pairs
+        assert sum(r.far_instances for r in reps) == whole.far_instances
     for pl in plans:
         pl.close()
 
