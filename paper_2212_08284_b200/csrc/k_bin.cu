@@ -167,11 +167,45 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     order = sorted + base;
   }
   if (!part) return;  // sort only (positions bound ahead of the moments)
+  // four threads per particle (more loads in flight than one thread per
+  // record): thread k writes 16-B pieces {k, k+4} of the record
+  //   0 (x, y)  1 (z, q)  2 (mx, my)  3 (mz, txx)  4 (txy, txz)  5 (tyy, tyz)  6 (tzz, tr)
+  // and checks the moments it read (together every one of q, mu, Theta)
   bool mp = false;
-  for (int p = threadIdx.x; p < c; p += kLeafThreads) {
-    const unsigned i = order[p];
-    write_record(pos, src, i, part + static_cast<std::size_t>(base + p) * kRec);
-    if (check_src) mp = check_moments(src + 10 * static_cast<std::size_t>(i), i, res) || mp;
+  for (int e = threadIdx.x; e < 4 * c; e += kLeafThreads) {
+    const int p = e >> 2, k = e & 3;
+    const std::size_t i = order[p];
+    const double* ps = pos + 3 * i;
+    const double* ss = src + 10 * i;
+    double2* out = reinterpret_cast<double2*>(part + static_cast<std::size_t>(base + p) * kRec);
+    double a, b, c2 = 0.0, d = 0.0;  // the moments this thread checks
+    if (k == 0) {
+      a = ss[5];
+      b = ss[6];
+      out[0] = make_double2(ps[0], ps[1]);
+      out[4] = make_double2(a, b);
+    } else if (k == 1) {
+      a = ss[7];
+      b = ss[8];
+      c2 = ss[0];
+      out[1] = make_double2(ps[2], c2);
+      out[5] = make_double2(a, b);
+    } else if (k == 2) {
+      a = ss[1];
+      b = ss[2];
+      d = ss[9];
+      out[2] = make_double2(a, b);
+      out[6] = make_double2(d, (ss[4] + ss[7]) + d);  // SymMat3::trace (types.hpp:57)
+    } else {
+      a = ss[3];
+      b = ss[4];
+      out[3] = make_double2(a, b);
+    }
+    if (check_src) {
+      if (!(isfinite(a) && isfinite(b) && isfinite(c2) && isfinite(d)))
+        atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
+      mp = mp || a != 0.0 || b != 0.0 || d != 0.0;  // (c2 is q: not a multipole)
+    }
   }
   if (check_src && __syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
 }

@@ -20,6 +20,9 @@ namespace ankh_b200 {
 namespace {
 
 constexpr int kP2MThreads = 128;
+#ifndef ANKH_P2M_VEC
+#define ANKH_P2M_VEC 1
+#endif
 
 // self_energy summand of one particle record (kernel.cpp:208-209): q^2 +
 // c_mu |mu|^2 + c_th Theta:Theta (off-diagonals twice, SymMat3::contract)
@@ -54,12 +57,23 @@ template <int L>
 struct P2MWShape {
   static constexpr int L2 = L * L, K = L2 * L;
   static constexpr int QJ = (L2 + 31) / 32;       // (j,k) columns per lane
-  static constexpr int PER = 12 * L;              // staged doubles per particle
+  // kVec: per particle, 16-B aligned groups so the accumulation reads them
+  // with 128-bit shared loads (shared-memory issue rivals FP64 there):
+  //   X [m][i] (3L, padded even) | Y [j][4] = y0 y1 y2 - | Z [k][6] = A0 A1 A2 B0 B1 C0
+  // (config 3: P2M + M2M 0.220 -> 0.213 ms).  L = 6 keeps the scalar layout
+  // (the vector one spills there).  Else: X [m][i] | Y [m][j] | Z [f][k].
+  static constexpr bool kVec = ANKH_P2M_VEC && L <= 5;
+  static constexpr int XP = (3 * L + 1) / 2 * 2;
+  static constexpr int YOFF = kVec ? XP : 3 * L, ZOFF = kVec ? XP + 4 * L : 6 * L;
+  static constexpr int PER = kVec ? XP + 10 * L : 12 * L;  // staged doubles per particle
   static constexpr std::size_t smem_doubles = kP2MWarps * 32 * PER;
 };
 
 template <int L>
-__global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restrict__ part,
+#ifndef ANKH_P2M_MINB
+#define ANKH_P2M_MINB 4
+#endif
+__global__ void __launch_bounds__(kP2MThreads, ANKH_P2M_MINB) k_p2m_w(const double* __restrict__ part,
                                                        const unsigned* __restrict__ leaf_off,
                                                        int depth, double rb,
                                                        const double* __restrict__ hd_g,
@@ -71,7 +85,7 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
                                                        double c_th) {
   using Sh = P2MWShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PER = Sh::PER, KS = exp_stride(K);
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   const double* hd = c_hd + hd_slot(L);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // per particle: sx[3][L] | sy[3][L] | A0 A1 A2 B0 B1 C0 [L]
@@ -153,35 +167,58 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
             vy += h * ty[m];
             vz += h * tz[m];
           }
-          dst[nd * L + i] = scale * vx;            // x basis S^(nd)
-          dst[(3 + nd) * L + i] = scale * vy;      // y basis
+          dst[nd * L + i] = scale * vx;                                     // x basis S^(nd)
+          dst[Sh::YOFF + (Sh::kVec ? 4 * i + nd : nd * L + i)] = scale * vy;  // y basis
           zb[i] = scale * vz;
         }
         scale *= inv_rad;
         // fold the moments into the z factors (A0 A1 A2 B0 B1 C0)
+#define ZF(f, i) dst[Sh::ZOFF + (Sh::kVec ? 6 * (i) + (f) : (f) * L + (i))]
 #pragma unroll
         for (int i = 0; i < L; ++i) {
           const double z = zb[i];
           if (nd == 0) {
-            dst[6 * L + i] = q * z;
-            dst[7 * L + i] = my * z;
-            dst[8 * L + i] = tyy * z;
-            dst[9 * L + i] = mx * z;
-            dst[10 * L + i] = (2.0 * txy) * z;
-            dst[11 * L + i] = txx * z;
+            ZF(0, i) = q * z;
+            ZF(1, i) = my * z;
+            ZF(2, i) = tyy * z;
+            ZF(3, i) = mx * z;
+            ZF(4, i) = (2.0 * txy) * z;
+            ZF(5, i) = txx * z;
           } else if (nd == 1) {
-            dst[6 * L + i] += mz * z;
-            dst[7 * L + i] += (2.0 * tyz) * z;
-            dst[9 * L + i] += (2.0 * txz) * z;
+            ZF(0, i) += mz * z;
+            ZF(1, i) += (2.0 * tyz) * z;
+            ZF(3, i) += (2.0 * txz) * z;
           } else {
-            dst[6 * L + i] += tzz * z;
+            ZF(0, i) += tzz * z;
           }
         }
+#undef ZF
       }
     }
     __syncwarp();
     for (int p = 0; p < pc; ++p) {
       const double* s = st + p * PER;
+      if constexpr (Sh::kVec) {
+      double xv[Sh::XP];
+#pragma unroll
+      for (int u = 0; u < Sh::XP / 2; ++u) {
+        const double2 t = reinterpret_cast<const double2*>(s)[u];
+        xv[2 * u] = t.x;
+        xv[2 * u + 1] = t.y;
+      }
+#pragma unroll
+      for (int q = 0; q < Sh::QJ; ++q) {
+        const double2* y2p = reinterpret_cast<const double2*>(s + Sh::YOFF + 4 * jj[q]);
+        const double2* z2p = reinterpret_cast<const double2*>(s + Sh::ZOFF + 6 * kk[q]);
+        const double2 ya = y2p[0], yb = y2p[1], za = z2p[0], zb2 = z2p[1], zc = z2p[2];
+        const double w0 = fma(ya.x, za.x, fma(ya.y, za.y, yb.x * zb2.x));
+        const double w1 = fma(ya.x, zb2.y, ya.y * zc.x);
+        const double w2 = ya.x * zc.y;
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+          acc[q][i] = fma(xv[i], w0, fma(xv[L + i], w1, fma(xv[2 * L + i], w2, acc[q][i])));
+      }
+      } else {
 #pragma unroll
       for (int q = 0; q < Sh::QJ; ++q) {
         const int j = jj[q], k = kk[q];
@@ -192,6 +229,7 @@ __global__ void __launch_bounds__(kP2MThreads, 4) k_p2m_w(const double* __restri
 #pragma unroll
         for (int i = 0; i < L; ++i)
           acc[q][i] = fma(s[i], w0, fma(s[L + i], w1, fma(s[2 * L + i], w2, acc[q][i])));
+      }
       }
     }
   }
@@ -229,7 +267,7 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
                                                      double c_mu, double c_th) {
   using Sh = P2MShape<L>;
   constexpr int L2 = Sh::L2, K = Sh::K, PB = Sh::PB, RS = Sh::RS, KS = exp_stride(K);
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   double* hd = sm;              // 3 L^2
   double* rec = hd + 3 * L2;    // PB x RS
   double* S = rec + PB * RS;    // PB x 3 axes x 3 orders x L
