@@ -1,2 +1,1 @@
-for r in 1 2; do for v in p2m_novec p2m_vec; do ANKH_B200_LIB=$PWD/paper_2212_08284_b200/variants/libankh_b200_$v.so python scripts/p2p_ab.py; done; done
-for v in p2m_novec p2m_vec; do ANKH_B200_LIB=$PWD/paper_2212_08284_b200/variants/libankh_b200_$v.so AB_CONFIG=1 python scripts/p2p_ab.py; done
+for r in 1 2 3; do for v in t32 t64 t128; do ANKH_B200_LIB=$PWD/paper_2212_08284_b200/variants/libankh_b200_bin_$v.so python scripts/p2p_ab.py; done; done
