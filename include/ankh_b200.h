@@ -195,6 +195,12 @@ int ankh_plan_attach_push_group_v1(ankh_plan_v1** plans, int world, char* err, s
 int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* morton_begin,
                              int64_t* morton_end);
 int ankh_shard_cell_owner_v1(int level, uint32_t lex_cell, int depth, int world);
+/* The particle-index slice [i0, i1) whose moments a collective-attached shard
+ * validates (whole 256-particle blocks; the slices partition [0, n)). */
+int ankh_shard_src_slice_v1(size_t n, int rank, int world, size_t* i0, size_t* i1);
+/* Lowest level l >= 1 with world | 8^l (<= depth): a collective-attached shard
+ * runs M2M on its own subtree down to l and all-gathers levels l .. depth. */
+int ankh_shard_exchange_level_v1(int depth, int world);
 /* Canonical M2L instances (level, t, s, offset[3]) owned by `rank` (rank < 0:
  * all), in the plan's grouping order.  `*count` receives the total; at most
  * `capacity` entries are written (pass 0 to query the count). */

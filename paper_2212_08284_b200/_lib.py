@@ -38,6 +38,8 @@ EXPORTS = [
     "ankh_plan_attach_nccl_v1",
     "ankh_plan_attach_loopback_v1",
     "ankh_plan_attach_push_group_v1",
+    "ankh_shard_src_slice_v1",
+    "ankh_shard_exchange_level_v1",
     "ankh_probe_fp64_mix_ms_v1",
     "ankh_radial_fit_v1",
     "ankh_probe_dmma_tflops_v1",
@@ -91,6 +93,9 @@ def lib() -> ctypes.CDLL:
         I64 = ctypes.POINTER(ctypes.c_int64)
         L.ankh_shard_leaf_range_v1.argtypes = [c_int, c_int, c_int, I64, I64]
         L.ankh_shard_cell_owner_v1.argtypes = [c_int, ctypes.c_uint32, c_int, c_int]
+        L.ankh_shard_src_slice_v1.argtypes = [c_size_t, c_int, c_int, ctypes.POINTER(c_size_t),
+                                              ctypes.POINTER(c_size_t)]
+        L.ankh_shard_exchange_level_v1.argtypes = [c_int, c_int]
         L.ankh_shard_m2l_instances_v1.argtypes = [c_int, c_int, c_int, c_int, U32, U32, U32, I,
                                                   c_size_t, ctypes.POINTER(c_size_t)]
         L.ankh_plan_enqueue_phase_v1.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p, cp,

@@ -317,6 +317,17 @@ int ankh_shard_leaf_range_v1(int depth, int rank, int world, int64_t* begin, int
   return ANKH_OK;
 }
 
+int ankh_shard_src_slice_v1(size_t n, int rank, int world, size_t* i0, size_t* i1) {
+  if (world < 1 || rank < 0 || rank >= world || !i0 || !i1) return ANKH_INVALID_ARGUMENT;
+  ankh_b200::shard_src_slice(n, rank, world, i0, i1);
+  return ANKH_OK;
+}
+
+int ankh_shard_exchange_level_v1(int depth, int world) {
+  if (depth < 1 || depth > 8 || world < 1) return -1;
+  return ankh_b200::shard_exchange_level(depth, world);
+}
+
 int ankh_shard_cell_owner_v1(int level, uint32_t cell, int depth, int world) {
   if (level < 0 || level > depth || depth > 8 || world < 1) return -1;
   return ankh_b200::shard_cell_owner(level, cell, depth, world);

@@ -215,15 +215,9 @@ void Plan::build_geometry() {
   shard_upward_ = cfg.world > 1 && (static_cast<long long>(n_leaves) % cfg.world) == 0;
   p2m_begin_ = shard_upward_ ? lb : 0;
   p2m_end_ = shard_upward_ ? le : n_leaves;
-  exch_level_ = depth;
-  if (shard_upward_)
-    for (int l = depth; l >= 1 && (1ll << (3 * l)) % cfg.world == 0; --l) exch_level_ = l;
+  exch_level_ = shard_upward_ ? shard_exchange_level(depth, cfg.world) : depth;
   slice_src_ = shard_upward_ && std::getenv("ANKH_SHARD_FULL_SRC") == nullptr;
-  if (slice_src_) {
-    const std::size_t blocks = (n + 255) / 256;
-    src_i0_ = std::min(n, blocks * cfg.rank / cfg.world * 256);
-    src_i1_ = std::min(n, blocks * (cfg.rank + 1) / cfg.world * 256);
-  }
+  if (slice_src_) shard_src_slice(n, cfg.rank, cfg.world, &src_i0_, &src_i1_);
   // P2P polynomial length from the largest possible near distance
   // (2 leaf sides per axis): s_max = xi^2 (2 sqrt(3) * 2 r_B / n)^2
   const double side = 2.0 * rb / nax;

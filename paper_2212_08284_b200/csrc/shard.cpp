@@ -28,6 +28,18 @@ void shard_leaf_range(int depth, int rank, int world, std::int64_t* begin, std::
   *end = nl * (rank + 1) / world;
 }
 
+void shard_src_slice(std::size_t n, int rank, int world, std::size_t* i0, std::size_t* i1) {
+  const std::size_t blocks = (n + 255) / 256, r = static_cast<std::size_t>(rank), g = static_cast<std::size_t>(world);
+  *i0 = std::min(n, blocks * r / g * 256);
+  *i1 = std::min(n, blocks * (r + 1) / g * 256);
+}
+
+int shard_exchange_level(int depth, int world) {
+  int l0 = depth;
+  for (int l = depth; l >= 1 && (std::int64_t(1) << (3 * l)) % world == 0; --l) l0 = l;
+  return l0;
+}
+
 int shard_m2l_owner(int level, std::uint32_t t, std::uint32_t s, int depth, int world) {
   if (world <= 1) return 0;
   // the owner of t or of s, by a hash of the pair: every cell has the same

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <array>
+#include <cstddef>
 #include <cstdint>
 #include <vector>
 
@@ -19,6 +20,12 @@ std::uint32_t morton3(std::uint32_t x, std::uint32_t y, std::uint32_t z);
 
 /// Morton leaf range [begin, end) owned by `rank` of `world` at `depth`.
 void shard_leaf_range(int depth, int rank, int world, std::int64_t* begin, std::int64_t* end);
+/// Particle-index slice [i0, i1) whose moments shard `rank` validates (whole
+/// 256-particle blocks; the slices partition [0, n)).
+void shard_src_slice(std::size_t n, int rank, int world, std::size_t* i0, std::size_t* i1);
+/// Lowest level l >= 1 whose 8^l cells split evenly over `world` shards, up to
+/// `depth` (the upward exchange all-gathers levels l .. depth).
+int shard_exchange_level(int depth, int world);
 
 /// Owner shard of lex cell `cell` at `level` in a depth-`depth` tree.
 int shard_cell_owner(int level, std::uint32_t cell, int depth, int world);

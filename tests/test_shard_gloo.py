@@ -61,6 +61,30 @@ def test_leaf_ownership_partition(depth, world):
             assert (b.value <= m < e.value) == (owner[c] == r)
 
 
+@pytest.mark.parametrize("n", [0, 1, 255, 256, 257, 24000, 1029000])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_src_slices_partition(n, world):
+    """The moment slices of collective-attached shards cover [0, n) exactly
+    once, in rank order, at 256-particle block boundaries."""
+    i0, i1 = ctypes.c_size_t(), ctypes.c_size_t()
+    prev = 0
+    for r in range(world):
+        assert lib().ankh_shard_src_slice_v1(n, r, world, ctypes.byref(i0), ctypes.byref(i1)) == 0
+        assert i0.value == prev and i1.value >= i0.value
+        assert i0.value % 256 == 0
+        prev = i1.value
+    assert prev == n
+
+
+@pytest.mark.parametrize("depth,world,want", [(3, 2, 1), (3, 8, 1), (5, 4, 1), (3, 16, 2), (5, 64, 2),
+                                              (3, 512, 3)])
+def test_exchange_level(depth, world, want):
+    """Own-subtree M2M reaches down to the lowest level that splits evenly."""
+    l0 = lib().ankh_shard_exchange_level_v1(depth, world)
+    assert l0 == want and (8 ** l0) % world == 0
+    assert l0 == 1 or (8 ** (l0 - 1)) % world != 0
+
+
 @pytest.mark.parametrize("depth,periodic,world", [(2, True, 2), (2, False, 3), (3, True, 4), (3, False, 8)])
 def test_m2l_instances_partition(depth, periodic, world):
     full = m2l_instances(depth, periodic, -1, 1)
