@@ -1059,13 +1059,16 @@ void Plan::stream_setup() {
 // positions half of the streamed path: validation, binning, per-leaf sort
 // (build_tree, as set_positions) and the per-chunk leaf lists; their bounds
 // land in h_sbounds_ (pinned) once `ev_s_sorted_` completes
-void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C) {
+void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C,
+                            const std::function<void(const std::string&)>& mark) {
   ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
   launch_init_result(res, st);
   const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
   launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, res, st);
+  if (mark) mark("  binned");
   launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_, d_off_, d_keys2_,
                        d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
+  if (mark) mark("  leaf CSR");
   launch_stream_prepare(d_off_, d_idx2_, n, depth, periodic ? 1 : 0, static_cast<unsigned>(chunk), C, d_inv_,
                         d_ready_, d_scnt_, d_sbounds_, d_scursor_, d_list_p2m_, d_list_p2p_, st, h_sbounds_dev_);
 }
@@ -1116,7 +1119,9 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   }
   if (!bound_pos) {
     ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_pos_, 0));
-    stream_positions(st, d_res_, chunk, C);
+    stream_positions(st, d_res_, chunk, C, trace ? std::function<void(const std::string&)>(
+                                                      [&](const std::string& w) { mark(w, st); })
+                                                : std::function<void(const std::string&)>());
   } else {
     ANKH_CUDA(cudaMemcpyAsync(d_res_, d_res_pos_, sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
   }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -133,7 +134,8 @@ class Plan {
   bool stream_eligible() const;
   void stream_setup();
   std::size_t stream_chunk_size() const;
-  void stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C);
+  void stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C,
+                        const std::function<void(const std::string&)>& mark = {});
   void enqueue_streamed(const double* h_pos, const double* h_src, cudaStream_t st);
   bool stream_bound_ = false;  // set_positions built the streamed path's lists
   static constexpr int kMaxStreamChunks = ankh_b200::kMaxStreamChunks;
