@@ -173,6 +173,9 @@ int ankh_plan_leaf_level_v1(ankh_plan_v1* plan, double** d_leaf_level, int64_t* 
                             int64_t* row_end, int* row_stride);
 int ankh_device_copy_v1(void* dst, const void* src, size_t bytes, void* stream, char* err,
                         size_t errlen);
+/* One-rank exercise of every NCCL call the shards issue (grouped all-gathers,
+ * grouped sum + uint64 MIN all-reduce), eager and captured in a CUDA graph. */
+int ankh_nccl_selftest_v1(char* err, size_t errlen);
 /* (c) Diagnostics on a one-GPU box: a loopback "collective" that lands the
  *     leaf-level all-gather's bytes with device copies and makes the
  *     all-reduce the identity, so one shard's complete evaluation (with the

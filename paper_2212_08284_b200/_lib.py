@@ -37,6 +37,7 @@ EXPORTS = [
     "ankh_nccl_unique_id_v1",
     "ankh_plan_attach_nccl_v1",
     "ankh_plan_attach_loopback_v1",
+    "ankh_nccl_selftest_v1",
     "ankh_plan_attach_push_group_v1",
     "ankh_shard_src_slice_v1",
     "ankh_shard_exchange_level_v1",
@@ -105,6 +106,7 @@ def lib() -> ctypes.CDLL:
         L.ankh_nccl_unique_id_v1.argtypes = [ctypes.c_char_p, cp, c_size_t]
         L.ankh_plan_attach_nccl_v1.argtypes = [c_void_p, ctypes.c_char_p, cp, c_size_t]
         L.ankh_plan_attach_loopback_v1.argtypes = [c_void_p, cp, c_size_t]
+        L.ankh_nccl_selftest_v1.argtypes = [cp, c_size_t]
         L.ankh_plan_attach_push_group_v1.argtypes = [ctypes.POINTER(c_void_p), c_int, cp, c_size_t]
         L.ankh_direct_energy_v1.argtypes = [c_size_t, D, D, c_double, c_double, c_int, c_int,
                                             c_double, D, D, cp, c_size_t]

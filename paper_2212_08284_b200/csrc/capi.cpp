@@ -285,6 +285,10 @@ int ankh_plan_attach_nccl_v1(ankh_plan_v1* plan, const unsigned char* id128, cha
   });
 }
 
+int ankh_nccl_selftest_v1(char* err, size_t errlen) {
+  return guarded(err, errlen, [&] { ankh_b200::nccl_selftest(); });
+}
+
 int ankh_plan_attach_loopback_v1(ankh_plan_v1* plan, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");

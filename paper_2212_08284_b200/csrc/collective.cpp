@@ -125,6 +125,62 @@ Collective* make_nccl_collective(const unsigned char id[128], int rank, int worl
   return new NcclCollective(id, rank, world);
 }
 
+// Exercises every collective call the plans issue (grouped multi-slab
+// all-gather, grouped sum + uint64 MIN all-reduce, plain all-reduce) on a
+// one-rank communicator, eagerly and inside a captured CUDA graph, and checks
+// the buffers come back unchanged (a one-rank collective is the identity).
+void nccl_selftest() {
+  unsigned char id[128];
+  nccl_unique_id(id);
+  NcclCollective c(id, 0, 1);
+  cudaStream_t st;
+  ANKH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  constexpr int kN = 96;
+  double* d = nullptr;
+  unsigned long long* u = nullptr;
+  ANKH_CUDA(cudaMalloc(&d, kN * sizeof(double)));
+  ANKH_CUDA(cudaMalloc(&u, 2 * sizeof(unsigned long long)));
+  double h[kN];
+  for (int k = 0; k < kN; ++k) h[k] = 0.5 + k;
+  const unsigned long long hu[2] = {7ull, ~0ull};
+  auto run = [&] {
+    double* slabs[2] = {d, d + 64};
+    const std::size_t counts[2] = {64, 32};
+    c.allgather_inplace_group(slabs, counts, 2, st);
+    c.allreduce_sum_min(d, 8, u, 2, st);
+    c.allreduce_sum(d + 8, 8, st);
+  };
+  for (int pass = 0; pass < 2; ++pass) {
+    ANKH_CUDA(cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, st));
+    ANKH_CUDA(cudaMemcpyAsync(u, hu, sizeof hu, cudaMemcpyHostToDevice, st));
+    if (pass == 0) {
+      run();
+    } else {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      ANKH_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      run();
+      ANKH_CUDA(cudaStreamEndCapture(st, &g));
+      ANKH_CUDA(cudaGraphInstantiate(&ge, g, 0));
+      ANKH_CUDA(cudaGraphLaunch(ge, st));
+      ANKH_CUDA(cudaStreamSynchronize(st));
+      cudaGraphExecDestroy(ge);
+      cudaGraphDestroy(g);
+    }
+    double back[kN];
+    unsigned long long ub[2];
+    ANKH_CUDA(cudaMemcpyAsync(back, d, sizeof back, cudaMemcpyDeviceToHost, st));
+    ANKH_CUDA(cudaMemcpyAsync(ub, u, sizeof ub, cudaMemcpyDeviceToHost, st));
+    ANKH_CUDA(cudaStreamSynchronize(st));
+    for (int k = 0; k < kN; ++k)
+      if (back[k] != h[k]) throw AnkhError(ANKH_CUDA_ERROR, "nccl selftest: all-gather / sum changed a value");
+    if (ub[0] != hu[0] || ub[1] != hu[1]) throw AnkhError(ANKH_CUDA_ERROR, "nccl selftest: uint64 MIN changed a value");
+  }
+  cudaFree(d);
+  cudaFree(u);
+  cudaStreamDestroy(st);
+}
+
 namespace {
 
 class LoopbackCollective final : public Collective {

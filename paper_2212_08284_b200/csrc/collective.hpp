@@ -34,6 +34,9 @@ class Collective {
 void nccl_unique_id(unsigned char out[128]);
 /// Communicator over `world` ranks (one GPU each, current device).
 Collective* make_nccl_collective(const unsigned char id[128], int rank, int world);
+/// One-rank exercise of every NCCL call the plans issue, eager and in a CUDA
+/// graph (throws AnkhError on any failure or changed value).
+void nccl_selftest();
 /// Timing stand-in for a one-GPU box (diagnostics only): the all-gather fills
 /// the other shards' rows with device copies of this shard's slab (the bytes
 /// land in HBM as they would over NVLink, at HBM rather than NVLink speed),

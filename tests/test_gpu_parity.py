@@ -605,6 +605,19 @@ def test_nccl_collective_single_rank(cuda):
         assert rep.e_total == ref_rep.e_total
 
 
+def test_nccl_calls_selftest(cuda):
+    """Every NCCL call the shards issue (grouped multi-level all-gather, the
+    grouped energy-sum + first-violation uint64 MIN all-reduce) on a one-rank
+    communicator, eagerly and inside a CUDA graph: datatypes, ops and group
+    semantics are accepted and a one-rank collective is the identity."""
+    import ctypes
+    err = ctypes.create_string_buffer(512)
+    code = ankh.lib().ankh_nccl_selftest_v1(err, 512)
+    if code != 0 and b"libnccl" in err.value:
+        pytest.skip(err.value.decode())
+    assert code == 0, err.value.decode()
+
+
 def test_direct_lattice_sum_matches_numpy(cuda):
     """ankh_direct_energy_v1 against an explicit numpy image sum built from the
     oracle's pair_interaction (kernel.cpp:157-204) on a tiny system."""
