@@ -278,12 +278,25 @@ def main():
     import paper_2212_08284_b200 as ankh
     from paper_2212_08284_b200 import inputs
 
+    # ANKH_BENCH_LOOPBACK=1 (plumbing dry run, NOT a measurement): ranks may
+    # share GPUs, torch.distributed runs on gloo, and each plan exchanges
+    # through the loopback stand-in -- the multi-rank code path of this script
+    # (barriers, max-over-ranks timing, sharded plans, host-buffer e2e) on a
+    # one-GPU box; its energies are one shard's partials.
+    loopback = os.environ.get("ANKH_BENCH_LOOPBACK") == "1" and world > 1
+    if loopback:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if loopback:
+            dist.init_process_group("gloo")
+            red_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pos, src, rb, cfg = inputs.make_config(args.config)
     L = cfg.orders[0] if args.config != 2 else 5
     n = pos.shape[0]
@@ -304,6 +317,9 @@ def main():
         # inside the plan on its own NCCL communicator; torch.distributed only
         # carries the 128-byte id
         if dist is None:
+            return
+        if loopback:
+            p.attach_loopback()
             return
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -341,7 +357,7 @@ def main():
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1)
     if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     res = plan.result()  # job totals (NCCL all-reduce inside the plan when world > 1)
@@ -395,7 +411,7 @@ def main():
             e2e_step()
         t_e2e = time.perf_counter() - t0
         if dist is not None:
-            t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+            t = torch.tensor([t_e2e], dtype=torch.float64, device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e = float(t.item())
         e2e = {"value": k2 / t_e2e, "unit": "evals/s", "h2d_bytes_per_step": int(pos.nbytes + src.nbytes),
@@ -414,7 +430,7 @@ def main():
             plan.energy_sources(hsrc)
         t_fix = time.perf_counter() - t0
         if dist is not None:
-            t = torch.tensor([t_fix], dtype=torch.float64, device="cuda")
+            t = torch.tensor([t_fix], dtype=torch.float64, device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_fix = float(t.item())
         e2e_fixed = {"value": k2 / t_fix, "unit": "evals/s", "h2d_bytes_per_step": int(src.nbytes),
@@ -481,6 +497,9 @@ def main():
             "e2e_including_precompute": e2e_cold,
             "cpu_baseline": cpu,
         }
+        if loopback:
+            line["dry_run"] = ("ANKH_BENCH_LOOPBACK: loopback exchange, ranks may share a GPU -- "
+                               "plumbing check, not a measurement; energies are shard 0's partials")
         print(json.dumps(line), flush=True)
     plan.close()
     if dist is not None:
