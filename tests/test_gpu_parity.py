@@ -605,6 +605,24 @@ def test_nccl_collective_single_rank(cuda):
         assert rep.e_total == ref_rep.e_total
 
 
+@pytest.mark.parametrize("env", ["ANKH_M2L_SPLIT", "ANKH_NO_PRIORITY"])
+def test_schedule_switches_bitwise(cuda, env, monkeypatch):
+    """Schedule A/B switches (leaf-level M2L beside M2M, stream priorities)
+    change only the launch order: every partial is written per tile / leaf
+    and reduced in a fixed order, so reports are bit-identical."""
+    torch = cuda
+    pos, src, rb, cfg = inputs.make_config(1)
+    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4)
+    dp, ds = torch.from_numpy(pos).cuda(), torch.from_numpy(src).cuda()
+    key = lambda r: (r.e_total, r.e_near, r.e_far, r.e_self, r.e_periodic_far)
+    want = key(ankh.Plan(pos.shape[0], rb, ec, phase_timing=False).energy_device(dp, ds))
+    monkeypatch.setenv(env, "1")
+    plan = ankh.Plan(pos.shape[0], rb, ec, phase_timing=False)
+    for _ in range(3):  # plain launch, graph capture, replay
+        assert key(plan.energy_device(dp, ds)) == want
+    plan.close()
+
+
 def test_nccl_calls_selftest(cuda):
     """Every NCCL call the shards issue (grouped multi-level all-gather, the
     grouped energy-sum + first-violation uint64 MIN all-reduce) on a one-rank
