@@ -58,19 +58,22 @@ __global__ void __launch_bounds__(kSvdWarps * 32) k_jacobi_svd(const double* __r
     const int i = e / K, j = e - i * K;
     w[j * K + i] = c[e];
   }
-  __syncthreads();
-  for (int j = warp; j < K; j += kSvdWarps) {
-    double a = 0.0;
-    for (int i = lane; i < K; i += 32) a = fma(w[j * K + i], w[j * K + i], a);
-    a = warp_sum(a);
-    if (lane == 0) nrm[j] = a;
-  }
   // rotation threshold sqrt(K) eps |w_p||w_q|: the rounding level of a K-term
   // dot product summed in lane partials
   const double eps2 = 2.220446049250313e-16 * 2.220446049250313e-16 * K;
   const int np = K + (K & 1);  // players (one dummy when K is odd)
   int sweep = 0;
   for (; sweep < 100; ++sweep) {
+    // exact squared column norms at every sweep start; within a sweep they
+    // follow the rotations analytically (|w_p'|^2 = alpha - t g,
+    // |w_q'|^2 = beta + t g), so a rotation needs one dot product, not three
+    __syncthreads();
+    for (int j = warp; j < K; j += kSvdWarps) {
+      double a = 0.0;
+      for (int i = lane; i < K; i += 32) a = fma(w[j * K + i], w[j * K + i], a);
+      a = warp_sum(a);
+      if (lane == 0) nrm[j] = a;
+    }
     __syncthreads();
     if (warp == 0) {
       double mx = 0.0;
@@ -124,20 +127,14 @@ __global__ void __launch_bounds__(kSvdWarps * 32) k_jacobi_svd(const double* __r
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
         const double cs = rsqrt(fma(t, t, 1.0));
         const double sn = cs * t;
-        double a2 = 0.0, b2 = 0.0;
         for (int i = hl; i < K; i += 16) {
           const double x = wp[i], y = wq[i];
-          const double a = cs * x - sn * y, b = sn * x + cs * y;
-          wp[i] = a;
-          wq[i] = b;
-          a2 = fma(a, a, a2);
-          b2 = fma(b, b, b2);
+          wp[i] = cs * x - sn * y;
+          wq[i] = sn * x + cs * y;
         }
-        a2 = half_sum(a2, hmask);
-        b2 = half_sum(b2, hmask);
         if (hl == 0) {
-          nrm[p] = a2;
-          nrm[q] = b2;
+          nrm[p] = fma(-t, g, alpha);
+          nrm[q] = fma(t, g, beta);
           rotated = 1;
         }
       }
