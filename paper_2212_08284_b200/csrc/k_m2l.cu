@@ -173,7 +173,10 @@ void launch_class(const double* exp, const long long* level_off, const double* f
                   const M2LOp* ops, const M2LTile* tiles, int n_tiles, const int* tile_ids,
                   const uint2* inst, int K, int Kp, double* far_partial, cudaStream_t st) {
   // two instance tiles per warp for the common small-rank classes (register budget)
-  constexpr int NTW = KP8 <= 5 ? 2 : 1;
+#ifndef ANKH_M2L_NTW_SMALL
+#define ANKH_M2L_NTW_SMALL 2  // instance tiles per warp for KP8 <= 3
+#endif
+  constexpr int NTW = KP8 <= 3 ? ANKH_M2L_NTW_SMALL : (KP8 <= 5 ? 2 : 1);
   constexpr int kThr = kM2LTile * 4 / NTW;
   const std::size_t smem = kStages * sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
   static bool attr = false;
