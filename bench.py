@@ -405,7 +405,7 @@ def main():
             e2e_step()
         torch.cuda.synchronize()
         barrier()
-        k2 = max(3, min(args.steps, 20))
+        k2 = max(10, min(3 * args.steps, 60))  # wall-clock: enough calls to average host jitter
         t0 = time.perf_counter()
         for _ in range(k2):
             e2e_step()
