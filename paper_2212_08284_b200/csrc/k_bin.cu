@@ -9,6 +9,8 @@
 // scatter) and each leaf's indices are put back in ascending order, which is
 // the reference's bucket order (bit-exact leaf CSR).  All of it is HBM-bound
 // (104 B read, 8 B of keys/slots, 112-B records written per atom).
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -359,7 +361,13 @@ __global__ void __launch_bounds__(256) k_stream_lists(const unsigned char* __res
   list_p2p[s_base[k1] + s1] = m;
 }
 
-__global__ void k_init_result(DevResult* res, int any_multipole) {
+// Result flags / energies, and (counts != nullptr) the leaf histogram zeroed
+// in the same launch (one graph node instead of a memset plus a kernel).
+__global__ void k_init_result(DevResult* res, int any_multipole, unsigned* counts, unsigned n_counts) {
+  const unsigned g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (counts)
+    for (unsigned e = g; e < n_counts; e += gridDim.x * blockDim.x) counts[e] = 0u;
+  if (g != 0) return;
   for (int k = 0; k < kRedCount; ++k) res->red[k] = 0.0;
   res->min_nonfinite = ~0ull;
   res->min_outside = ~0ull;
@@ -387,8 +395,10 @@ __global__ void k_dup_check(const unsigned* __restrict__ keys, const unsigned* _
 
 }  // namespace
 
-void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole) {
-  k_init_result<<<1, 1, 0, st>>>(res, any_multipole);
+void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole, unsigned* counts,
+                        unsigned n_counts) {
+  const unsigned blocks = counts ? std::min(1024u, (n_counts + 255) / 256) : 1u;
+  k_init_result<<<blocks, counts ? 256 : 1, 0, st>>>(res, any_multipole, counts, n_counts);
 }
 
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,

@@ -151,7 +151,9 @@ std::size_t finalize_scratch_bytes();
 /// block layout) and the records gathered through an existing sorted index.
 void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
                        std::size_t n, DevResult* res, double* part, cudaStream_t st);
-void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole = 0);
+/// counts != nullptr: also zero counts[0, n_counts) (the leaf histogram).
+void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole = 0,
+                        unsigned* counts = nullptr, unsigned n_counts = 0);
 /// Counting sort into leaves (after launch_bin with counts): scan -> offsets,
 /// scatter, per-leaf ascending order (sorted = the leaf CSR's index array) and
 /// the gather of 112-B records.  unsorted / scratch: N uints each; need

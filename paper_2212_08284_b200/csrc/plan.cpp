@@ -730,10 +730,9 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     launch_src_gather(d_pos, d_src, d_idx2_, n, d_res_, d_part_, st);
     launches += 2;
   } else if (mode != 2) {
-    ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
     // sliced moments: other slices' multipoles are unseen, so the kernels
     // that branch on the global flag take the multipole path (same energies)
-    launch_init_result(d_res_, st, slice_src_ ? 1 : 0);
+    launch_init_result(d_res_, st, slice_src_ ? 1 : 0, d_counts_, static_cast<unsigned>(n_leaves + 1));
     ++launches;
     // binning + sort + gather (build_tree, octree.cpp:27-45)
     const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
@@ -1061,8 +1060,7 @@ void Plan::stream_setup() {
 // land in h_sbounds_ (pinned) once `ev_s_sorted_` completes
 void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C,
                             const std::function<void(const std::string&)>& mark) {
-  ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
-  launch_init_result(res, st);
+  launch_init_result(res, st, 0, d_counts_, static_cast<unsigned>(n_leaves + 1));
   const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
   launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, res, st);
   if (mark) mark("  binned");
@@ -1262,8 +1260,7 @@ void Plan::set_positions(const double* h_pos, cudaStream_t st) {
   }
   ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
   if (pending_code_ == 0 && !csr_only_) {
-    ANKH_CUDA(cudaMemsetAsync(d_counts_, 0, (n_leaves + 1) * sizeof(unsigned), st));
-    launch_init_result(d_res_pos_, st);
+    launch_init_result(d_res_pos_, st, 0, d_counts_, static_cast<unsigned>(n_leaves + 1));
     const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
     launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, d_res_pos_, st);
     launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_,
