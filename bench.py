@@ -266,12 +266,35 @@ def cpu_baseline_sample(args, pos, src, rb, L):
             "wall_times": wt, "e_total": rep["e_total"]}
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(nproc: int) -> int:
+    """`bench.py --gpus N` started without torchrun: re-launch this script as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] spawning {nproc} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
     if args.impl == "reference":
+        # the reference is a CPU library: rank 0 alone runs it (others exit 0)
         run_reference(args, world, rank)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if world != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but the launcher started {world} ranks", file=sys.stderr)
+        sys.exit(2)
 
     import torch
 
@@ -286,6 +309,9 @@ def main():
     loopback = os.environ.get("ANKH_BENCH_LOOPBACK") == "1" and world > 1
     if loopback:
         local = local % max(1, torch.cuda.device_count())
+    elif world > torch.cuda.device_count():
+        print(f"[bench] {world} ranks need {world} GPUs; {torch.cuda.device_count()} visible", file=sys.stderr)
+        sys.exit(2)
     torch.cuda.set_device(local)
     dist = None
     red_dev = "cuda"

@@ -87,11 +87,23 @@ typedef struct ankh_plan_v1 ankh_plan_v1;
 void ankh_config_default_v1(ankh_config_v1* cfg);
 
 /* Drop-in for ankh::fmm_energy.  Host buffers; host<->device copies inside.
- * A process-wide plan cache keyed by (n, box_radius, config) makes repeated
- * calls skip the geometry-only precompute. */
+ * A process-wide plan cache keyed by (n, box_radius, config, resolved device)
+ * makes repeated calls skip the geometry-only precompute.  Reentrant: the
+ * cache lock covers only the lookup; an evaluation locks its own plan, so
+ * calls on different devices run concurrently.  Runs on cfg->device (or the
+ * calling thread's current device when -1) and leaves the current device as
+ * it found it. */
 int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
                        double box_radius, const ankh_config_v1* cfg, ankh_report_v1* out,
                        char* err, size_t errlen);
+
+/* The call-level checks of fmm_energy in the reference's order, for wrappers
+ * whose containers carry separate position / source lengths:
+ * validate_config (fmm.cpp:384, types.cpp:65-79), then validate_system's
+ * box_radius rule and its size-mismatch rule (types.cpp:20-26).  The
+ * per-particle rules run on the device inside the evaluation. */
+int ankh_check_call_v1(const ankh_config_v1* cfg, double box_radius, size_t n_positions,
+                       size_t n_sources, char* err, size_t errlen);
 
 /* Plan for n particles in the box [-box_radius, box_radius]^3 under cfg. */
 int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg,
@@ -210,18 +222,6 @@ int ankh_shard_exchange_level_v1(int depth, int world);
 int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, uint32_t* level,
                                 uint32_t* t, uint32_t* s, int32_t* offset, size_t capacity,
                                 size_t* count);
-
-/* Direct screened lattice sum -- the exact quantity the FMM approximates,
- * for validation (SPEC's `direct` method; the reference has no direct engine):
- *   *e_lattice = 1/2 sum_{|I|inf <= p} sum_{i,j: i != j or I != 0}
- *                pair_interaction(x_i, x_j + 2 r_B I)          (kernel.cpp:157-204)
- *   *e_self    = self_energy (kernel.cpp:206-213);  e_total = sum of the two.
- * Cost n^2 (2p+1)^3 pair evaluations on the GPU; refused above
- * max_pair_evaluations (<= 0: 1e12) with ANKH_RUNTIME_ERROR. */
-int ankh_direct_energy_v1(size_t n, const double* positions, const double* sources,
-                          double box_radius, double xi, int p, int device,
-                          double max_pair_evaluations, double* e_lattice, double* e_self,
-                          char* err, size_t errlen);
 
 /* Near-field radial polynomials the plan uses for a given s_max = xi^2 d_max^2
  * (d_max = the largest near-pair distance, 2 sqrt(3) leaf sides): coefficients

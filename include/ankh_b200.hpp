@@ -111,12 +111,13 @@ template <class System, class Config, class Report = EnergyReport>
 Report fmm_energy(const System& system, const Config& config, int threads = 1) {
   static_assert(sizeof(system.positions[0]) == 3 * sizeof(double), "Vec3 layout");
   static_assert(sizeof(system.sources[0]) == 10 * sizeof(double), "MultipoleSource layout");
-  if (system.positions.size() != system.sources.size())
-    throw std::invalid_argument(
-        "fmm_energy: invalid system: positions and sources must have equal length");
   const ankh_config_v1 c = to_c(config, threads);
   ankh_report_v1 r;
   char err[512];
+  // validate_config, box radius, size mismatch: the reference's order (fmm.cpp:384-388)
+  rethrow(ankh_check_call_v1(&c, system.box_radius, system.positions.size(), system.sources.size(),
+                             err, sizeof(err)),
+          err);
   const int code = ankh_fmm_energy_v1(
       system.positions.size(), reinterpret_cast<const double*>(system.positions.data()),
       reinterpret_cast<const double*>(system.sources.data()), system.box_radius, &c, &r, err,

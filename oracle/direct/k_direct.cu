@@ -1,3 +1,6 @@
+// TEST INFRASTRUCTURE ONLY (checker, not the product): built into
+// oracle/direct/libankh_direct.so, loaded by tests/ through oracle/direct.py.
+//
 // Direct screened lattice sum on sm_100a -- the exact quantity the FMM
 // approximates, for validating it (SPEC's `direct` method; the reference has no
 // direct engine):
@@ -15,6 +18,12 @@
 // stages the sources in shared memory in tiles and walks I_z; a thread keeps
 // its target in registers and shifts it by -2 r_B I (r = x_i - 2 r_B I - x_j).
 // Per-CTA partials, summed in a fixed order on the host (deterministic).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include "kernels.cuh"
 #include "pair.cuh"
 
@@ -109,3 +118,54 @@ void launch_direct(const double* pos, const double* src, int n, double box_radiu
 }
 
 }  // namespace ankh_b200
+
+// C-ABI of the checker.  The radial polynomials come from the product's
+// ankh_radial_fit_v1(1e9) (valid to s = 0.25, libm beyond: any distance).
+//   *e_lattice = 1/2 sum_{|I|inf <= p} sum_{i,j: i != j or I != 0}
+//                pair_interaction(x_i, x_j + 2 r_B I)          (kernel.cpp:157-204)
+// Returns 0, or 1 with a message in err.
+extern "C" int ankh_direct_lattice_v1(size_t n, const double* positions, const double* sources,
+                                      double box_radius, double xi, int p, int nterms, double s_lim,
+                                      const double* pcoef, const double* gcoef, double* e_lattice,
+                                      char* err, size_t errlen) {
+  using namespace ankh_b200;
+  auto fail = [&](const std::string& m) {
+    if (err && errlen) {
+      std::strncpy(err, m.c_str(), errlen - 1);
+      err[errlen - 1] = '\0';
+    }
+    return 1;
+  };
+  *e_lattice = 0.0;
+  if (n == 0) return 0;
+  if (n >= (1u << 30)) return fail("direct: too many particles");
+  const int ni = static_cast<int>(n);
+  const int np = direct_partials(ni, p);
+  P2PRadial rad{};
+  rad.nterms = nterms;
+  rad.s_lim = s_lim;
+  std::memcpy(rad.p, pcoef, sizeof rad.p);
+  std::memcpy(rad.g, gcoef, sizeof rad.g);
+  double *d_pos = nullptr, *d_src = nullptr, *d_rec = nullptr, *d_part = nullptr;
+  cudaError_t e = cudaSuccess;
+  std::vector<double> part(np);
+  if ((e = cudaMalloc(&d_pos, n * 3 * sizeof(double))) == cudaSuccess &&
+      (e = cudaMalloc(&d_src, n * 10 * sizeof(double))) == cudaSuccess &&
+      (e = cudaMalloc(&d_rec, n * kRec * sizeof(double))) == cudaSuccess &&
+      (e = cudaMalloc(&d_part, np * sizeof(double))) == cudaSuccess &&
+      (e = cudaMemcpy(d_pos, positions, n * 3 * sizeof(double), cudaMemcpyHostToDevice)) == cudaSuccess &&
+      (e = cudaMemcpy(d_src, sources, n * 10 * sizeof(double), cudaMemcpyHostToDevice)) == cudaSuccess) {
+    launch_direct(d_pos, d_src, ni, box_radius, xi, p, rad, d_rec, d_part, nullptr);
+    if ((e = cudaGetLastError()) == cudaSuccess)
+      e = cudaMemcpy(part.data(), d_part, np * sizeof(double), cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d_pos);
+  cudaFree(d_src);
+  cudaFree(d_rec);
+  cudaFree(d_part);
+  if (e != cudaSuccess) return fail(std::string("direct: ") + cudaGetErrorString(e));
+  double acc = 0.0;
+  for (double v : part) acc += v;  // fixed order
+  *e_lattice = acc;
+  return 0;
+}

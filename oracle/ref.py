@@ -49,6 +49,7 @@ def lib() -> ctypes.CDLL:
         sz = ctypes.c_size_t
         L.ref_fmm_energy.argtypes = [sz, _D, _D, ctypes.c_double, _D, _I, ctypes.c_int, _D,
                                      ctypes.c_char_p, sz]
+        L.ref_fmm_energy_sized.argtypes = [sz, sz, _D, _D, ctypes.c_double, _D, _I, ctypes.c_char_p, sz]
         L.ref_leaf_csr.argtypes = [sz, _D, ctypes.c_double, ctypes.c_int, _U32, _U32, ctypes.c_char_p, sz]
         L.ref_expansions.argtypes = [sz, _D, _D, ctypes.c_double, ctypes.c_int, ctypes.c_int, _D,
                                      ctypes.c_char_p, sz]
@@ -100,6 +101,20 @@ def fmm_energy(pos, src, r_b, xi=0.01, p=15, order_cheb=8, order_equi=8, depth=0
     tk = ["precompute", "interpolation", "far_field", "near_field", "periodic_far", "self", "total"]
     rep["wall_times"] = {k: float(out[6 + j]) for j, k in enumerate(tk)}
     return rep
+
+
+def fmm_energy_error(pos, src, r_b, xi=0.01, p=15, order_cheb=8, order_equi=8, depth=0, svd_tol=1e-7,
+                     recip_cutoff=12):
+    """(code, message) the reference's fmm_energy raises on this input (the
+    two arrays may differ in length); (0, "") when it does not raise."""
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    src = np.ascontiguousarray(src, dtype=np.float64).reshape(-1, 10)
+    d = np.array([xi, svd_tol], dtype=np.float64)
+    i = np.array([p, order_cheb, order_equi, depth, recip_cutoff], dtype=np.int32)
+    err = ctypes.create_string_buffer(512)
+    code = lib().ref_fmm_energy_sized(pos.shape[0], src.shape[0], _p(pos), _p(src), float(r_b), _p(d),
+                                      i.ctypes.data_as(_I), err, 512)
+    return code, err.value.decode()
 
 
 def leaf_csr(pos, r_b, depth):

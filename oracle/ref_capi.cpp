@@ -101,6 +101,23 @@ int ref_fmm_energy(std::size_t n, const double* pos, const double* src, double b
   });
 }
 
+// fmm_energy on a system whose position and source arrays differ in length
+// (the reference's size-mismatch rule, types.cpp:23-26): only the exception
+// is of interest; returns the code / message of the call.
+int ref_fmm_energy_sized(std::size_t n_pos, std::size_t n_src, const double* pos, const double* src,
+                         double box_radius, const double* dcfg, const int* icfg, char* err,
+                         std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    ankh::ParticleSystem s;
+    s.box_radius = box_radius;
+    s.positions.resize(n_pos);
+    s.sources.resize(n_src);
+    if (n_pos) std::memcpy(s.positions.data(), pos, n_pos * 3 * sizeof(double));
+    if (n_src) std::memcpy(s.sources.data(), src, n_src * 10 * sizeof(double));
+    ankh::fmm_energy(s, make_config(dcfg, icfg), 1);
+  });
+}
+
 // Leaf CSR of build_tree (octree.cpp:27-45): offsets[8^depth + 1], indices[n].
 int ref_leaf_csr(std::size_t n, const double* pos, double box_radius, int depth,
                  std::uint32_t* offsets, std::uint32_t* indices, char* err, std::size_t errlen) {

@@ -18,7 +18,6 @@ from .api import (  # noqa: F401
     build_tree_csr,
     default_depth,
     device_copy,
-    direct_energy,
     exchange_leaf_levels,
     fmm_energy,
     nccl_unique_id,

@@ -15,6 +15,7 @@ _lib: Optional[ctypes.CDLL] = None
 EXPORTS = [
     "ankh_config_default_v1",
     "ankh_fmm_energy_v1",
+    "ankh_check_call_v1",
     "ankh_plan_create_v1",
     "ankh_plan_destroy_v1",
     "ankh_plan_energy_v1",
@@ -44,7 +45,6 @@ EXPORTS = [
     "ankh_probe_fp64_mix_ms_v1",
     "ankh_radial_fit_v1",
     "ankh_probe_dmma_tflops_v1",
-    "ankh_direct_energy_v1",
     "ankh_plan_set_positions_v1",
     "ankh_plan_energy_sources_v1",
 ]
@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
         L.ankh_config_default_v1.argtypes = [c_void_p]
         L.ankh_config_default_v1.restype = None
         L.ankh_fmm_energy_v1.argtypes = [c_size_t, D, D, c_double, c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_check_call_v1.argtypes = [c_void_p, c_double, c_size_t, c_size_t, cp, c_size_t]
         L.ankh_plan_create_v1.argtypes = [c_size_t, c_double, c_void_p, c_void_p, cp, c_size_t]
         L.ankh_plan_destroy_v1.argtypes = [c_void_p]
         L.ankh_plan_destroy_v1.restype = None
@@ -108,8 +109,6 @@ def lib() -> ctypes.CDLL:
         L.ankh_plan_attach_loopback_v1.argtypes = [c_void_p, cp, c_size_t]
         L.ankh_nccl_selftest_v1.argtypes = [cp, c_size_t]
         L.ankh_plan_attach_push_group_v1.argtypes = [ctypes.POINTER(c_void_p), c_int, cp, c_size_t]
-        L.ankh_direct_energy_v1.argtypes = [c_size_t, D, D, c_double, c_double, c_int, c_int,
-                                            c_double, D, D, cp, c_size_t]
         L.ankh_plan_set_positions_v1.argtypes = [c_void_p, D, cp, c_size_t]
         L.ankh_plan_energy_sources_v1.argtypes = [c_void_p, D, c_void_p, cp, c_size_t]
         L.ankh_probe_dmma_tflops_v1.argtypes = [c_int, c_int]

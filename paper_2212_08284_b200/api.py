@@ -208,39 +208,16 @@ def fmm_energy(system: ParticleSystem, config: Optional[EwaldConfig] = None,
     config = config or EwaldConfig()
     pos = _as_host(system.positions, 3)
     src = _as_host(system.sources, 10)
-    if pos.shape[0] != src.shape[0]:
-        raise InvalidArgument("fmm_energy: invalid system: positions and sources must have equal length")
     rep = _Report()
     err = ctypes.create_string_buffer(512)
+    c = config._c(threads=threads)
+    # validate_config, box radius, size mismatch: the reference's order (fmm.cpp:384-388)
+    _check(lib().ankh_check_call_v1(ctypes.byref(c), float(system.box_radius), pos.shape[0],
+                                    src.shape[0], err, 512), err)
     code = lib().ankh_fmm_energy_v1(pos.shape[0], _ptr(pos), _ptr(src), float(system.box_radius),
-                                    ctypes.byref(config._c(threads=threads)), ctypes.byref(rep),
-                                    err, 512)
+                                    ctypes.byref(c), ctypes.byref(rep), err, 512)
     _check(code, err)
     return EnergyReport._from_c(rep)
-
-
-def direct_energy(system: ParticleSystem, xi: float = 0.01, p: int = 15,
-                  max_pair_evaluations: float = 0.0, device: int = -1) -> EnergyReport:
-    """Direct screened lattice sum on the GPU (ankh_direct_energy_v1): the
-    exact quantity the FMM approximates, 1/2 sum over |I|inf <= p images and
-    all pairs of pair_interaction, plus the self energy.  There is no near /
-    far split: the whole pair sum is reported as ``e_near``.  Cost n^2 (2p+1)^3
-    pair evaluations (refused above ``max_pair_evaluations``, default 1e12)."""
-    import time
-
-    pos = _as_host(system.positions, 3)
-    src = _as_host(system.sources, 10)
-    if pos.shape[0] != src.shape[0]:
-        raise InvalidArgument("direct: positions and sources must have equal length")
-    lat, slf = ctypes.c_double(), ctypes.c_double()
-    err = ctypes.create_string_buffer(512)
-    t0 = time.perf_counter()
-    _check(lib().ankh_direct_energy_v1(pos.shape[0], _ptr(pos), _ptr(src), float(system.box_radius),
-                                       float(xi), int(p), int(device), float(max_pair_evaluations),
-                                       ctypes.byref(lat), ctypes.byref(slf), err, 512), err)
-    wall = time.perf_counter() - t0
-    return EnergyReport(e_total=lat.value + slf.value, e_self=slf.value, e_near=lat.value,
-                        wall_times={"total": wall})
 
 
 def nccl_unique_id() -> bytes:

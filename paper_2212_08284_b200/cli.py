@@ -6,17 +6,16 @@
     python -m paper_2212_08284_b200 gen     --config 3 --output c3.txt
     python -m paper_2212_08284_b200 bench   --sizes 3000,24000,192000 [--order-cheb 5]
 
-`energy` runs the B200 `fmm_energy` (`--method fmm`, the reference's engine)
-or the direct screened lattice sum the FMM approximates (`--method direct`,
-GPU, n^2 (2p+1)^3 pair evaluations; SPEC's fft / ewald engines are absent from
-the reference and are rejected with exit code 3).  Documents are JSON with every float printed
+`energy` runs the B200 `fmm_energy` (`--method fmm`, the reference's engine;
+SPEC's fft / direct / ewald engines are absent from the reference and are
+rejected with exit code 3 -- the GPU direct lattice sum used to check the FMM's
+accuracy is test infrastructure, oracle/direct.py).  Documents are JSON with every float printed
 round-trip exact (>= 17 significant digits where needed), holding the run
 manifest and the EnergyReport, so `load_document` restores both without loss.
 
 Exit codes (SPEC: stable contract for harnesses): 0 success, 2 parse error
 (particle file / manifest), 3 configuration or invariant violation (the
-reference's invalid_argument / domain_error), 4 budget guard (--max-atoms,
---max-pairs),
+reference's invalid_argument / domain_error), 4 budget guard (--max-atoms),
 1 any other failure (e.g. CUDA).
 """
 from __future__ import annotations
@@ -34,9 +33,8 @@ import numpy as np
 from . import api, inputs
 
 EXIT_OK, EXIT_OTHER, EXIT_PARSE, EXIT_CONFIG, EXIT_BUDGET = 0, 1, 2, 3, 4
-# SPEC methods fmm | fft | direct | ewald: the reference implements fmm; `direct`
-# is the GPU lattice sum (api.direct_energy) the FMM approximates, for checks
-METHODS = ("fmm", "direct")
+# SPEC methods fmm | fft | direct | ewald: the reference implements fmm only
+METHODS = ("fmm",)
 CONFIG_FIELDS = ("xi", "p", "order_cheb", "order_equi", "depth", "svd_tol", "recip_cutoff")
 
 
@@ -110,16 +108,8 @@ def _read_system(path: str, max_atoms: Optional[int]) -> api.ParticleSystem:
     return api.ParticleSystem(pos, src, rb)
 
 
-def _run(system: api.ParticleSystem, m: RunManifest, max_pairs: float = 0.0) -> api.EnergyReport:
+def _run(system: api.ParticleSystem, m: RunManifest) -> api.EnergyReport:
     try:
-        if m.method == "direct":
-            cfg = m.ewald()
-            try:
-                return api.direct_energy(system, cfg.xi, cfg.p, max_pair_evaluations=max_pairs)
-            except api.AnkhRuntimeError as e:
-                if "budget" in str(e):
-                    raise CliError(EXIT_BUDGET, str(e)) from None
-                raise
         return api.fmm_energy(system, m.ewald(), threads=m.threads)
     except (api.InvalidArgument, api.DomainError) as e:
         raise CliError(EXIT_CONFIG, str(e)) from None
@@ -167,7 +157,7 @@ def cmd_energy(a) -> int:
     if not m.input:
         raise CliError(EXIT_PARSE, "energy: --input is required")
     system = _read_system(m.input, a.max_atoms)
-    r = _run(system, m, a.max_pairs)
+    r = _run(system, m)
     _emit(document(m, r, {"atoms": system.size()}), m.output)
     return EXIT_OK
 
@@ -181,7 +171,7 @@ def cmd_compare(a) -> int:
     ref = None
     for m in runs:
         m.input, m.threads = a.input, a.threads
-        r = _run(system, m, a.max_pairs)
+        r = _run(system, m)
         if ref is None:
             ref = r.e_total
         rows.append({"run": m.method + ":" + ",".join(f"{k}={v}" for k, v in m.config.items()),
@@ -296,9 +286,6 @@ def _add_config(p) -> None:
     p.add_argument("--threads", type=int, default=int(os.environ.get("ANKH_THREADS", "0")))
     p.add_argument("--max-atoms", dest="max_atoms", type=int, default=None,
                    help="budget guard: refuse larger inputs (exit 4)")
-    p.add_argument("--max-pairs", dest="max_pairs", type=float, default=0.0,
-                   help="budget guard of the direct method: n^2 (2p+1)^3 pair evaluations "
-                        "(default 1e12; exit 4)")
 
 
 def build_parser() -> argparse.ArgumentParser:

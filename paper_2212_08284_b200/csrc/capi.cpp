@@ -47,22 +47,44 @@ int guarded(char* err, std::size_t errlen, F&& f) {
 
 // Process-wide cache of plans for the one-shot drop-in call: the geometry-only
 // precompute (M2L factors, periodic spectrum, buffers) is reused whenever the
-// particle count, box radius and configuration repeat.
+// particle count, box radius, configuration and (resolved) device repeat.
+// The cache lock covers only the lookup / insert; an evaluation holds its
+// plan's own mutex, so calls on different GPUs (or different systems) run
+// concurrently, as the reference's reentrant call does.  Entries are shared:
+// an entry evicted while a call still uses it lives until that call returns.
 struct CacheEntry {
   std::size_t n;
   double rb;
   ankh_config_v1 cfg;
-  std::unique_ptr<Plan> plan;
+  int device;
+  std::shared_ptr<ankh_plan_v1> h;
 };
 std::mutex g_cache_mu;
 std::list<CacheEntry> g_cache;
-constexpr std::size_t kCacheMax = 2;
+constexpr std::size_t kCacheMax = 4;
 
 bool same_cfg(const ankh_config_v1& a, const ankh_config_v1& b) {
   return a.xi == b.xi && a.p == b.p && a.order_cheb == b.order_cheb &&
          a.order_equi == b.order_equi && a.depth == b.depth && a.svd_tol == b.svd_tol &&
-         a.recip_cutoff == b.recip_cutoff && a.device == b.device && a.rank == b.rank &&
-         a.world == b.world && a.phase_timing == b.phase_timing;
+         a.recip_cutoff == b.recip_cutoff && a.rank == b.rank && a.world == b.world &&
+         a.phase_timing == b.phase_timing;
+}
+
+int resolve_device(const ankh_config_v1& c) {
+  if (c.device >= 0) return c.device;
+  int d = 0;
+  ANKH_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+// Run f(plan) on the plan's device (the caller's current device restored
+// after) under the plan's mutex.
+template <class F>
+void on_plan(ankh_plan_v1* h, F&& f) {
+  if (!h || !h->plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> lock(h->mu);
+  ankh_b200::DeviceGuard dev(h->plan->device());
+  f(*h->plan);
 }
 
 }  // namespace
@@ -94,23 +116,31 @@ int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
     if (n > 0 && (!positions || !sources)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
     ankh_b200::validate_config(*cfg);
     const auto t0 = std::chrono::steady_clock::now();
-    std::lock_guard<std::mutex> lock(g_cache_mu);
-    Plan* plan = nullptr;
-    for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
-      if (it->n == n && it->rb == box_radius && same_cfg(it->cfg, *cfg)) {
-        g_cache.splice(g_cache.begin(), g_cache, it);
-        plan = g_cache.front().plan.get();
-        break;
+    const int dev = resolve_device(*cfg);
+    std::shared_ptr<ankh_plan_v1> h;
+    {
+      std::lock_guard<std::mutex> lock(g_cache_mu);
+      for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+        if (it->n == n && it->rb == box_radius && it->device == dev && same_cfg(it->cfg, *cfg)) {
+          g_cache.splice(g_cache.begin(), g_cache, it);
+          h = g_cache.front().h;
+          break;
+        }
       }
     }
-    if (!plan) {
+    if (!h) {  // built outside the cache lock (plan builds on other devices proceed)
+      ankh_config_v1 c = *cfg;
+      c.device = dev;
+      h = std::make_shared<ankh_plan_v1>();
+      h->plan = std::make_unique<Plan>(n, box_radius, c);
+      std::lock_guard<std::mutex> lock(g_cache_mu);
       while (g_cache.size() >= kCacheMax) g_cache.pop_back();
-      auto p = std::make_unique<Plan>(n, box_radius, *cfg);
-      g_cache.push_front({n, box_radius, *cfg, std::move(p)});
-      plan = g_cache.front().plan.get();
+      g_cache.push_front({n, box_radius, *cfg, dev, h});
     }
-    plan->enqueue_host(positions, sources, nullptr);
-    plan->result(out);
+    on_plan(h.get(), [&](Plan& plan) {
+      plan.enqueue_host(positions, sources, nullptr);
+      plan.result(out);
+    });
     // wall_times["total"]: the whole call, as fmm.cpp:433 times it
     out->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
@@ -126,34 +156,53 @@ int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg, 
   });
 }
 
-void ankh_plan_destroy_v1(ankh_plan_v1* plan) { delete plan; }
+void ankh_plan_destroy_v1(ankh_plan_v1* plan) { delete plan; }  // ~Plan selects its own device
+
+int ankh_check_call_v1(const ankh_config_v1* cfg, double box_radius, size_t n_positions,
+                       size_t n_sources, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!cfg) throw AnkhError(ANKH_INVALID_ARGUMENT, "null config");
+    ankh_b200::validate_config(*cfg);  // fmm.cpp:384
+    // validate_system's system-level rules, in order (types.cpp:20-26)
+    if (!(box_radius > 0.0) || !std::isfinite(box_radius))
+      throw AnkhError(ANKH_INVALID_ARGUMENT, "fmm_energy: invalid system: box_radius must be positive and finite");
+    if (n_positions != n_sources)
+      throw AnkhError(ANKH_INVALID_ARGUMENT,
+                      "fmm_energy: invalid system: positions and sources must have equal length");
+  });
+}
 
 int ankh_plan_energy_v1(ankh_plan_v1* plan, const double* positions, const double* sources,
                         ankh_report_v1* out, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    plan->plan->enqueue_host(positions, sources, nullptr);
-    plan->plan->result(out);
+    on_plan(plan, [&](Plan& p) {
+      if (p.n > 0 && (!positions || !sources)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+      p.enqueue_host(positions, sources, nullptr);
+      p.result(out);
+    });
   });
 }
 
 int ankh_plan_set_positions_v1(ankh_plan_v1* plan, const double* positions, char* err,
                                size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");
-    if (plan->plan->n > 0 && !positions) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
-    plan->plan->set_positions(positions, nullptr);
+    on_plan(plan, [&](Plan& p) {
+      if (p.n > 0 && !positions) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+      p.set_positions(positions, nullptr);
+    });
   });
 }
 
 int ankh_plan_energy_sources_v1(ankh_plan_v1* plan, const double* sources, ankh_report_v1* out,
                                 char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
-    if (plan->plan->n > 0 && !sources) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
-    plan->plan->enqueue_sources(sources, nullptr);
-    plan->plan->result(out);
+    if (!out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null report");
+    on_plan(plan, [&](Plan& p) {
+      if (p.n > 0 && !sources) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+      p.enqueue_sources(sources, nullptr);
+      p.result(out);
+    });
   });
 }
 
@@ -161,27 +210,25 @@ int ankh_plan_energy_device_v1(ankh_plan_v1* plan, const double* d_positions,
                                const double* d_sources, void* stream, ankh_report_v1* out,
                                char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    plan->plan->enqueue(d_positions, d_sources, static_cast<cudaStream_t>(stream));
-    plan->plan->result(out);
+    if (!out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null report");
+    on_plan(plan, [&](Plan& p) {
+      p.enqueue(d_positions, d_sources, static_cast<cudaStream_t>(stream));
+      p.result(out);
+    });
   });
 }
 
 int ankh_plan_enqueue_v1(ankh_plan_v1* plan, const double* d_positions, const double* d_sources,
                          void* stream, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    plan->plan->enqueue(d_positions, d_sources, static_cast<cudaStream_t>(stream));
+    on_plan(plan, [&](Plan& p) { p.enqueue(d_positions, d_sources, static_cast<cudaStream_t>(stream)); });
   });
 }
 
 int ankh_plan_result_v1(ankh_plan_v1* plan, ankh_report_v1* out, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or report");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    plan->plan->result(out);
+    if (!out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null report");
+    on_plan(plan, [&](Plan& p) { p.result(out); });
   });
 }
 
@@ -203,9 +250,8 @@ int ankh_plan_info_v1(const ankh_plan_v1* plan, int* depth, int* order, size_t* 
 int ankh_plan_expansions_v1(ankh_plan_v1* plan, double* out, size_t count, char* err,
                             size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or buffer");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    plan->plan->expansions(out, count);
+    if (!out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null buffer");
+    on_plan(plan, [&](Plan& p) { p.expansions(out, count); });
   });
 }
 
@@ -230,26 +276,26 @@ int ankh_leaf_csr_v1(size_t n, const double* positions, double box_radius, int d
 int ankh_plan_m2l_factors_v1(ankh_plan_v1* plan, int level, const int* offset, double* lmat,
                              double* rmat, int max_rank, int* rank, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || !offset || !rank) throw AnkhError(ANKH_INVALID_ARGUMENT, "null argument");
-    plan->plan->m2l_factors(level, offset, lmat, rmat, max_rank, rank);
+    if (!offset || !rank) throw AnkhError(ANKH_INVALID_ARGUMENT, "null argument");
+    on_plan(plan, [&](Plan& p) { p.m2l_factors(level, offset, lmat, rmat, max_rank, rank); });
   });
 }
 
 int ankh_plan_energies_device_v1(ankh_plan_v1* plan, double* d_out, void* stream, char* err,
                                  size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || !d_out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or buffer");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    plan->plan->energies_to_device(d_out, static_cast<cudaStream_t>(stream));
+    if (!d_out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null buffer");
+    on_plan(plan, [&](Plan& p) { p.energies_to_device(d_out, static_cast<cudaStream_t>(stream)); });
   });
 }
 
 int ankh_plan_enqueue_phase_v1(ankh_plan_v1* plan, int phase, const double* d_positions,
                                const double* d_sources, void* stream, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || (phase != 1 && phase != 2)) throw AnkhError(ANKH_INVALID_ARGUMENT, "bad plan or phase");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    plan->plan->enqueue_phase(phase, d_positions, d_sources, static_cast<cudaStream_t>(stream));
+    if (phase != 1 && phase != 2) throw AnkhError(ANKH_INVALID_ARGUMENT, "bad phase");
+    on_plan(plan, [&](Plan& p) {
+      p.enqueue_phase(phase, d_positions, d_sources, static_cast<cudaStream_t>(stream));
+    });
   });
 }
 
@@ -278,10 +324,10 @@ int ankh_nccl_unique_id_v1(unsigned char* id128, char* err, size_t errlen) {
 int ankh_plan_attach_nccl_v1(ankh_plan_v1* plan, const unsigned char* id128, char* err,
                              size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan || !id128) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan or id");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    const ankh_config_v1& c = plan->plan->cfg;
-    plan->plan->attach_collective(ankh_b200::make_nccl_collective(id128, c.rank, c.world));
+    if (!id128) throw AnkhError(ANKH_INVALID_ARGUMENT, "null id");
+    on_plan(plan, [&](Plan& p) {
+      p.attach_collective(ankh_b200::make_nccl_collective(id128, p.cfg.rank, p.cfg.world));
+    });
   });
 }
 
@@ -291,10 +337,9 @@ int ankh_nccl_selftest_v1(char* err, size_t errlen) {
 
 int ankh_plan_attach_loopback_v1(ankh_plan_v1* plan, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null plan");
-    std::lock_guard<std::mutex> lock(plan->mu);
-    const ankh_config_v1& c = plan->plan->cfg;
-    plan->plan->attach_collective(ankh_b200::make_loopback_collective(c.rank, c.world));
+    on_plan(plan, [&](Plan& p) {
+      p.attach_collective(ankh_b200::make_loopback_collective(p.cfg.rank, p.cfg.world));
+    });
   });
 }
 
@@ -307,10 +352,8 @@ int ankh_plan_attach_push_group_v1(ankh_plan_v1** plans, int world, char* err, s
         throw AnkhError(ANKH_INVALID_ARGUMENT, "plan group must hold ranks 0..world-1 of one sharding");
       bases[r] = plans[r]->plan->expansions_base();
     }
-    for (int r = 0; r < world; ++r) {
-      std::lock_guard<std::mutex> lock(plans[r]->mu);
-      plans[r]->plan->attach_collective(ankh_b200::make_push_collective(r, world, bases));
-    }
+    for (int r = 0; r < world; ++r)
+      on_plan(plans[r], [&](Plan& p) { p.attach_collective(ankh_b200::make_push_collective(r, world, bases)); });
   });
 }
 
@@ -359,81 +402,6 @@ int ankh_shard_m2l_instances_v1(int depth, int periodic, int rank, int world, ui
   } catch (...) {
     return ANKH_RUNTIME_ERROR;
   }
-}
-
-int ankh_direct_energy_v1(size_t n, const double* positions, const double* sources,
-                          double box_radius, double xi, int p, int device,
-                          double max_pair_evaluations, double* e_lattice, double* e_self,
-                          char* err, size_t errlen) {
-  return guarded(err, errlen, [&] {
-    if (!e_lattice || !e_self) throw AnkhError(ANKH_INVALID_ARGUMENT, "null output");
-    if (n > 0 && (!positions || !sources)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
-    if (!(xi > 0.0) || !std::isfinite(xi)) throw AnkhError(ANKH_INVALID_ARGUMENT, "direct: xi must be > 0");
-    if (p < 0) throw AnkhError(ANKH_INVALID_ARGUMENT, "direct: p must be >= 0");
-    if (!(box_radius > 0.0) || !std::isfinite(box_radius))
-      throw AnkhError(ANKH_INVALID_ARGUMENT, "direct: box_radius must be positive and finite");
-    const double side = 2.0 * p + 1.0;
-    const double evals = static_cast<double>(n) * static_cast<double>(n) * side * side * side;
-    const double budget = max_pair_evaluations > 0.0 ? max_pair_evaluations : 1e12;
-    if (evals > budget)
-      throw AnkhError(ANKH_RUNTIME_ERROR, "direct: n^2 (2p+1)^3 = " + std::to_string(evals) +
-                                              " pair evaluations exceed the budget " +
-                                              std::to_string(budget));
-    if (n >= (1u << 30)) throw AnkhError(ANKH_RUNTIME_ERROR, "direct: too many particles");
-    if (device >= 0) ANKH_CUDA(cudaSetDevice(device));
-    // self energy (kernel.cpp:206-213), host, fixed order
-    const double c_mu = 2.0 * xi * xi / 3.0, c_th = 8.0 * xi * xi * xi * xi / 5.0;
-    double acc = 0.0;
-    for (size_t i = 0; i < n; ++i) {
-      const double* s = sources + 10 * i;
-      const double mu2 = s[1] * s[1] + s[2] * s[2] + s[3] * s[3];
-      const double th2 = s[4] * s[4] + s[7] * s[7] + s[9] * s[9] +
-                         2.0 * (s[5] * s[5] + s[6] * s[6] + s[8] * s[8]);
-      acc += s[0] * s[0] + c_mu * mu2 + c_th * th2;
-    }
-    *e_self = -xi / std::sqrt(3.14159265358979323846) * acc;
-    *e_lattice = 0.0;
-    if (n == 0) return;
-    const int ni = static_cast<int>(n);
-    const int np = ankh_b200::direct_partials(ni, p);
-    double *d_pos = nullptr, *d_src = nullptr, *d_rec = nullptr, *d_part = nullptr;
-    cudaStream_t st = nullptr;
-    auto cleanup = [&] {
-      if (st) cudaStreamSynchronize(st), cudaStreamDestroy(st);
-      cudaFree(d_pos);
-      cudaFree(d_src);
-      cudaFree(d_rec);
-      cudaFree(d_part);
-    };
-    try {
-      ANKH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-      ANKH_CUDA(cudaMalloc(&d_pos, n * 3 * sizeof(double)));
-      ANKH_CUDA(cudaMalloc(&d_src, n * 10 * sizeof(double)));
-      ANKH_CUDA(cudaMalloc(&d_rec, n * ankh_b200::kRec * sizeof(double)));
-      ANKH_CUDA(cudaMalloc(&d_part, np * sizeof(double)));
-      ANKH_CUDA(cudaMemcpyAsync(d_pos, positions, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
-      ANKH_CUDA(cudaMemcpyAsync(d_src, sources, n * 10 * sizeof(double), cudaMemcpyHostToDevice, st));
-      // radial polynomials valid to s = 0.25 with libm beyond (any distance)
-      const ankh_b200::RadialFit f = ankh_b200::fit_radial(1e9);
-      ankh_b200::P2PRadial rad{};
-      rad.nterms = f.nterms;
-      rad.s_lim = f.s_lim;
-      std::memcpy(rad.p, f.p, sizeof rad.p);
-      std::memcpy(rad.g, f.g, sizeof rad.g);
-      ankh_b200::launch_direct(d_pos, d_src, ni, box_radius, xi, p, rad, d_rec, d_part, st);
-      ANKH_CUDA(cudaGetLastError());
-      std::vector<double> part(np);
-      ANKH_CUDA(cudaMemcpyAsync(part.data(), d_part, np * sizeof(double), cudaMemcpyDeviceToHost, st));
-      ANKH_CUDA(cudaStreamSynchronize(st));
-      double e = 0.0;
-      for (double v : part) e += v;
-      *e_lattice = e;
-    } catch (...) {
-      cleanup();
-      throw;
-    }
-    cleanup();
-  });
 }
 
 int ankh_radial_fit_v1(double s_max, int* nterms, double* s_lim, double* p, double* g,

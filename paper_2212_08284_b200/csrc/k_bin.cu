@@ -372,7 +372,7 @@ __global__ void k_init_result(DevResult* res, int any_multipole, unsigned* count
   res->min_nonfinite = ~0ull;
   res->min_outside = ~0ull;
   res->any_multipole = any_multipole;
-  res->p2p_next = 0;
+  res->spare = 0;
 }
 
 // Exact-duplicate scan over (key, index)-sorted particles: duplicates share a

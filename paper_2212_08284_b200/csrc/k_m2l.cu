@@ -179,12 +179,8 @@ void launch_class(const double* exp, const long long* level_off, const double* f
   constexpr int NTW = KP8 <= 3 ? ANKH_M2L_NTW_SMALL : (KP8 <= 5 ? 2 : 1);
   constexpr int kThr = kM2LTile * 4 / NTW;
   const std::size_t smem = kStages * sizeof(double) * (2 * 8 * KP8 + 2 * kM2LTile) * kStride;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_m2l<KP8, NTW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  smem_opt_in(attr, k_m2l<KP8, NTW>, smem);
   k_m2l<KP8, NTW><<<n_tiles, kThr, smem, st>>>(exp, level_off, factors, ops, tiles, tile_ids,
                                                inst, K, Kp, far_partial);
 }

@@ -493,24 +493,16 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
   if (L > 6) {  // register budget of the warp-per-leaf variant: block-per-leaf instead
     if (list) return;  // (no list mode: the plan streams only for L <= 6)
     const std::size_t smem = sizeof(double) * P2MShape<L>::smem_doubles;
-    static bool attr_b = false;
-    if (!attr_b) {
-      cudaFuncSetAttribute(k_p2m<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
-      attr_b = true;
-    }
+    static std::atomic<unsigned long long> attr_b{0};
+    smem_opt_in(attr_b, k_p2m<L>, smem);
     k_p2m<L><<<leaves, kP2MThreads, smem, st>>>(part, leaf_off, depth, rb, hd, exp_leaf, res,
                                                 m_begin, self_leaf, c_mu, c_th);
     return;
   }
   constexpr int LW = L > 6 ? 6 : L;  // (never launched with L > 6)
   const std::size_t smem = sizeof(double) * P2MWShape<LW>::smem_doubles;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_p2m_w<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  smem_opt_in(attr, k_p2m_w<LW>, smem);
   k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(
       part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end, list, bounds, self_leaf, c_mu, c_th);
 }
@@ -531,12 +523,8 @@ void m2m_order(const double* child, double* parent, int parent_level, const doub
                cudaStream_t st, unsigned p_begin, unsigned p_count) {
   constexpr int K = L * L * L;
   const std::size_t smem = sizeof(double) * (2 * L * L + 8 * exp_stride(K) + 6 * K);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_m2m<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  smem_opt_in(attr, k_m2m<L>, smem);
   const unsigned cells = p_count ? p_count : (1u << (3 * parent_level));
   k_m2m<L><<<cells, kM2MThreads, smem, st>>>(child, parent, parent_level, m2m, p_begin);
 }

@@ -273,11 +273,8 @@ void launch_periodic_eval(const double* root, const double* to_equi, const doubl
   const int L = order, eb = 2 * L - 1, K = L * L * L;
   const std::size_t smem =
       sizeof(double) * (3 * K + 2 * eb + 2 * K + 2 * L * eb * L + kPerThreads);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_periodic_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  smem_opt_in(attr, k_periodic_eval, 200 * 1024);
   k_periodic_eval<<<1, kPerThreads, smem, st>>>(root, to_equi, spec_re, L, out);
 }
 

@@ -12,10 +12,25 @@
 //   inst    : uint2 (t, s) canonical M2L instances grouped by operator
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace ankh_b200 {
+
+/// Dynamic shared-memory opt-in above 48 KB.  CUDA keeps the attribute per
+/// device and per kernel, so a launcher records, per kernel instantiation,
+/// the devices it has been set on (bit d of `done`).  Lock-free: two threads
+/// racing on a new device both set the same value, which is harmless.
+template <class Kernel>
+inline void smem_opt_in(std::atomic<unsigned long long>& done, Kernel* kernel, std::size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 constexpr int kRec = 14;          // doubles per particle record (112 B: x y z q mu Theta tr)
 constexpr int kM2LTile = 64;      // instances per M2L CTA
@@ -62,7 +77,7 @@ struct DevResult {
   unsigned long long min_outside;    // lowest finite index outside the box (follows min_nonfinite:
                                      // the two are MIN-reduced together across shards)
   int any_multipole;                 // some particle has mu or Theta != 0
-  unsigned p2p_next;                 // dynamic leaf counter of the pipelined P2P kernel
+  unsigned spare;
 };
 
 struct M2LTile {
@@ -123,20 +138,16 @@ struct P2PRadial {
   double p[14], g[14];
 };
 
-/// Near field.  pipe = 0: one CTA per target leaf (near_partial[leaf]);
-/// pipe = 1: persistent CTAs fed by a bulk-copy ring, dynamic leaf
-/// scheduling, near_partial[leaf * p2p_pipe_warps(256) + warp].  Returns the
+/// Near field: one CTA per target leaf (near_partial[leaf]).  Returns the
 /// number of near partials written.
 // list != nullptr: the target leaves are list[bounds[0] .. bounds[1]) (Morton
 // indices, list_grid of them -- the host knows the count), partials still
 // indexed by leaf - leaf_begin (streamed host path)
 int launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
-               double period, double xi, const P2PRadial& rad, int cap, int pipe, int leaf_begin,
+               double period, double xi, const P2PRadial& rad, int cap, int leaf_begin,
                int leaf_end, double* near_partial, unsigned long long* pair_count, DevResult* res,
                cudaStream_t st, const unsigned* list = nullptr, const unsigned* bounds = nullptr,
                int list_grid = 0);
-int p2p_pipe_warps(int tpb);
-int p2p_pipe_max_cap();
 int p2p_max_cap();
 void launch_periodic_gen(double* gen, int order, double box_radius, double xi, int p,
                          cudaStream_t st);
@@ -169,11 +180,6 @@ void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos,
 double probe_fp64_tflops(int iters);
 /// ms of k_mix<mode> (k_probe.cu): DFMA-only, DMMA-only, or half/half warps
 double probe_fp64_mix_ms(int mode, int it_f, int it_m);
-/// Direct screened lattice sum (k_direct.cu): per-CTA halves of the pair sums
-/// into partial[direct_partials(n, p)]; rec: n x kRec scratch.
-int direct_partials(int n, int p);
-void launch_direct(const double* pos, const double* src, int n, double box_radius, double xi,
-                   int p, const P2PRadial& rad, double* rec, double* partial, cudaStream_t st);
 double probe_dmma_tflops(int shape, int iters);
 
 // M2L instance lists on the GPU (k_inst.cu)

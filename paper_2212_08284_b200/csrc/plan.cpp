@@ -54,11 +54,16 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
   if (cfg.world < 1) cfg.world = 1;
   if (cfg.rank < 0 || cfg.rank >= cfg.world) throw AnkhError(ANKH_INVALID_ARGUMENT, "rank out of range");
   if (cfg.device >= 0) {
+    int count = 0;
+    ANKH_CUDA(cudaGetDeviceCount(&count));
+    if (cfg.device >= count) throw AnkhError(ANKH_INVALID_ARGUMENT, "device index out of range");
     device_ = cfg.device;
-    ANKH_CUDA(cudaSetDevice(device_));
   } else {
     ANKH_CUDA(cudaGetDevice(&device_));
   }
+  // the plan's resources live on device_; the caller's current device is
+  // restored when the constructor returns
+  DeviceGuard on_device(device_);
   periodic = cfg.p >= 2;
   depth = cfg.depth > 0 ? cfg.depth : default_depth(n);
   L = cfg.order_cheb;
@@ -134,6 +139,7 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
 }
 
 Plan::~Plan() {
+  DeviceGuard on_device(device_, /*nothrow=*/true);
   for (cudaStream_t s : {stream_, last_stream_, side_stream_, copy_stream_, gather_stream_})
     if (s) cudaStreamSynchronize(s);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
@@ -235,13 +241,8 @@ void Plan::build_geometry() {
   const double per_leaf = static_cast<double>(n) / n_leaves;
   p2p_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.3 / 32.0)) * 32;
   p2p_cap_ = std::max(256, std::min(p2p_cap_, 960));
-  // pipelined P2P (ANKH_P2P_PIPE=1): a 2-slot ring of p2p_pipe_cap_ staged sources
-  p2p_pipe_ = 0;
-  p2p_pipe_cap_ = 320;
-  if (const char* e = std::getenv("ANKH_P2P_PIPE")) p2p_pipe_ = std::atoi(e) != 0 ? 1 : 0;
   if (const char* e = std::getenv("ANKH_P2P_CAP")) {
     p2p_cap_ = std::max(64, std::atoi(e));
-    p2p_pipe_cap_ = std::min(p2p_cap_, p2p_pipe_max_cap());
   }
 }
 
@@ -303,8 +304,7 @@ void Plan::allocate() {
   ANKH_CUDA(cudaMemcpyAsync(d_level_off_, level_off_.data(), level_off_.size() * sizeof(long long),
                             cudaMemcpyHostToDevice, stream_));
   d_self_leaf_ = static_cast<double*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(double)));
-  d_near_part_ = static_cast<double*>(dalloc(std::max(leaf_end_ - leaf_begin_, 1) *
-                                             std::max(p2p_pipe_warps(256), 1) * sizeof(double)));
+  d_near_part_ = static_cast<double*>(dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(double)));
   d_pair_count_ = static_cast<unsigned long long*>(
       dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(unsigned long long)));
   d_per_ = static_cast<double*>(dalloc(sizeof(double)));
@@ -806,7 +806,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   // near field: P2P (fmm.cpp:278-327)
   const int n_near_parts =
       launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
-                 p2p_pipe_ ? p2p_pipe_cap_ : p2p_cap_, p2p_pipe_, leaf_begin_, leaf_end_,
+                 p2p_cap_, leaf_begin_, leaf_end_,
                  d_near_part_, d_pair_count_, d_res_, st);
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));
@@ -1023,7 +1023,7 @@ bool Plan::stream_eligible() const {
   if (e && e[0] == '0') return false;
   const std::size_t min_n = (e && e[0] == '1') ? 1 : 65536;
   return n >= min_n && cfg.world <= 1 && !shard_upward_ && !coll_ && !csr_only_ &&
-         pending_code_ == 0 && L <= 6 && p2p_pipe_ == 0;
+         pending_code_ == 0 && L <= 6;
 }
 
 void Plan::stream_setup() {
@@ -1155,7 +1155,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
       ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[c], 0));
       if (timing && !near_started) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
       near_started = true;
-      n_near_parts = launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, p2p_cap_, 0,
+      n_near_parts = launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, p2p_cap_,
                                 leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, st, d_list_p2p_,
                                 d_sbounds_ + (C + 1) + c, static_cast<int>(n_p));
       ++launches;

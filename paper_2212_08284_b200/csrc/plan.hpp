@@ -29,6 +29,31 @@ struct AnkhError : std::runtime_error {
                                                         cudaGetErrorString(e_));        \
   } while (0)
 
+/// Makes `dev` current for a scope and restores the caller's device after:
+/// every plan entry point runs on its plan's device, whatever the calling
+/// thread has selected (one thread may drive plans on several GPUs).
+struct DeviceGuard {
+  explicit DeviceGuard(int dev, bool nothrow = false) {
+    if (dev < 0 || cudaGetDevice(&prev_) != cudaSuccess) return;
+    if (prev_ != dev) {
+      const cudaError_t e = cudaSetDevice(dev);
+      if (e == cudaSuccess)
+        restore_ = true;
+      else if (!nothrow)
+        ANKH_CUDA(e);
+    }
+  }
+  ~DeviceGuard() {
+    if (restore_) cudaSetDevice(prev_);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+ private:
+  int prev_ = -1;
+  bool restore_ = false;
+};
+
 /// Temporary device buffers from the stream-ordered pool (cudaMallocAsync),
 /// released on the same stream at scope exit.
 struct DeviceScratch {
@@ -103,6 +128,7 @@ class Plan {
   void attach_collective(Collective* c);
 
   cudaStream_t stream() const { return stream_; }
+  int device() const { return device_; }
 
   // ---- geometry (public for introspection) ----
   std::size_t n = 0;
@@ -235,8 +261,6 @@ class Plan {
   DevResult* h_res_ = nullptr;
   P2PRadial radial_{};  // near-field radial polynomials (fit_radial)
   int p2p_cap_ = 512;
-  int p2p_pipe_ = 0;
-  int p2p_pipe_cap_ = 320;
   std::uint32_t launches_ = 0;
   // timing
   cudaEvent_t ev_[8] = {};

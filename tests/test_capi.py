@@ -73,6 +73,52 @@ def test_size_mismatch_message():
         ankh.fmm_energy(ankh.ParticleSystem(np.zeros((2, 3)), np.zeros((1, 10)), 1.0))
 
 
+# Pairs of violations in one call: the error raised is the reference's first
+# (validate_config, then validate_system's box_radius, size-mismatch and
+# per-particle rules -- fmm.cpp:384-388, types.cpp:20-26).  All of these fail
+# before any device work.
+_NAN = float("nan")
+_PRECEDENCE = {
+    "config+box": (dict(xi=-1.0), -1.0, 2, 2, False),
+    "config+size": (dict(p=1), 1.0, 2, 1, False),
+    "config+particle": (dict(order_cheb=1), 1.0, 2, 2, True),
+    "box+size": ({}, float("inf"), 3, 2, False),
+    "box+particle": ({}, 0.0, 2, 2, True),
+    "size+particle": ({}, 1.0, 3, 2, True),
+}
+
+
+@pytest.mark.parametrize("case", sorted(_PRECEDENCE))
+def test_error_precedence_matches_reference(case, ref):
+    kw, rb, n_pos, n_src, nan_particle = _PRECEDENCE[case]
+    pos = np.full((n_pos, 3), 0.25)
+    pos[:, 0] = np.linspace(-0.5, 0.5, n_pos)
+    src = np.zeros((n_src, 10))
+    src[:, 0] = 1.0
+    if nan_particle:
+        pos[0, 1] = _NAN
+    code, want = ref.fmm_energy_error(pos, src, rb, **kw)
+    assert code == 1 and want, (code, want)
+    with pytest.raises(ankh.InvalidArgument) as ei:
+        ankh.fmm_energy(ankh.ParticleSystem(pos, src, rb), ankh.EwaldConfig(**kw))
+    assert str(ei.value) == want
+
+
+def test_check_call_orders_rules():
+    """ankh_check_call_v1 itself (the C++ header's path): config, then box
+    radius, then sizes."""
+    c = api._Config()
+    ankh.lib().ankh_config_default_v1(ctypes.byref(c))
+    err = ctypes.create_string_buffer(512)
+    chk = lambda rb, a, b: (ankh.lib().ankh_check_call_v1(ctypes.byref(c), rb, a, b, err, 512),
+                            err.value.decode())
+    assert chk(1.0, 3, 3) == (0, "")
+    assert chk(-1.0, 3, 2) == (1, "fmm_energy: invalid system: box_radius must be positive and finite")
+    assert chk(1.0, 3, 2) == (1, "fmm_energy: invalid system: positions and sources must have equal length")
+    c.svd_tol = 2.0
+    assert chk(-1.0, 3, 2) == (1, "svd_tol must lie in (0, 1)")
+
+
 def test_default_depth_matches_reference_rule():
     import ankh_oracle as O
 

@@ -99,15 +99,6 @@ def test_budget_guard(tmp_path, capsys):
     assert code == cli.EXIT_BUDGET
 
 
-def test_direct_budget_guard(tmp_path, capsys):
-    """The direct lattice sum refuses n^2 (2p+1)^3 above the budget (exit 4)
-    before any device work."""
-    f = str(tmp_path / "s.txt")
-    assert cli.main(["gen", "--n", "2000", "--box-radius", "9", "-o", f]) == 0
-    code, out = run(["energy", "-i", f, "--method", "direct", "--max-pairs", "1e9"], capsys)
-    assert code == cli.EXIT_BUDGET and "budget" in out.err
-
-
 def test_config_error_exit_code(tmp_path, capsys):
     """validate_config's invalid_argument (types.cpp:65-79) maps to exit 3; the
     check runs in the library before any device work."""
