@@ -214,8 +214,22 @@ int ankh_shard_cell_owner_v1(int level, uint32_t lex_cell, int depth, int world)
  * validates (whole 256-particle blocks; the slices partition [0, n)). */
 int ankh_shard_src_slice_v1(size_t n, int rank, int world, size_t* i0, size_t* i1);
 /* Lowest level l >= 1 with world | 8^l (<= depth): a collective-attached shard
- * runs M2M on its own subtree down to l and all-gathers levels l .. depth. */
+ * runs M2M on its own subtree down to l, all-gathers level l and exchanges
+ * the M2L halos of levels l+1 .. depth (point to point). */
 int ankh_shard_exchange_level_v1(int depth, int world);
+/* The M2L halo of one level: Morton cells (ascending) that
+ * shard `src` owns and shard `dst` reads -- those that can form an M2L
+ * instance with a cell of dst's region (2 cells past its even-aligned faces,
+ * periodic wrap).  Needs world | 8^level.  `*count`
+ * receives the size; at most `capacity` ids are written to `morton`. */
+int ankh_shard_halo_cells_v1(int level, int depth, int periodic, int src, int dst, int world,
+                             uint32_t* morton, size_t capacity, size_t* count);
+/* Bytes shard `rank` receives / sends per evaluation in the upward exchange
+ * at interpolation order `order` (expansion rows padded to 32 doubles):
+ * halo != 0 the plan's schedule (all-gather of the exchange level + deep
+ * halos), halo == 0 the whole-level all-gather of every level it splits. */
+int ankh_shard_exchange_bytes_v1(int depth, int periodic, int order, int rank, int world, int halo,
+                                 size_t* recv_bytes, size_t* send_bytes);
 /* Canonical M2L instances (level, t, s, offset[3]) owned by `rank` (rank < 0:
  * all), in the plan's grouping order.  `*count` receives the total; at most
  * `capacity` entries are written (pass 0 to query the count). */

@@ -42,6 +42,8 @@ EXPORTS = [
     "ankh_plan_attach_push_group_v1",
     "ankh_shard_src_slice_v1",
     "ankh_shard_exchange_level_v1",
+    "ankh_shard_halo_cells_v1",
+    "ankh_shard_exchange_bytes_v1",
     "ankh_probe_fp64_mix_ms_v1",
     "ankh_radial_fit_v1",
     "ankh_probe_dmma_tflops_v1",
@@ -98,6 +100,10 @@ def lib() -> ctypes.CDLL:
         L.ankh_shard_src_slice_v1.argtypes = [c_size_t, c_int, c_int, ctypes.POINTER(c_size_t),
                                               ctypes.POINTER(c_size_t)]
         L.ankh_shard_exchange_level_v1.argtypes = [c_int, c_int]
+        L.ankh_shard_halo_cells_v1.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, U32, c_size_t,
+                                               ctypes.POINTER(c_size_t)]
+        L.ankh_shard_exchange_bytes_v1.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int,
+                                                   ctypes.POINTER(c_size_t), ctypes.POINTER(c_size_t)]
         L.ankh_shard_m2l_instances_v1.argtypes = [c_int, c_int, c_int, c_int, U32, U32, U32, I,
                                                   c_size_t, ctypes.POINTER(c_size_t)]
         L.ankh_plan_enqueue_phase_v1.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_void_p, cp,

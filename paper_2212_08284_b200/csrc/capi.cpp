@@ -352,8 +352,13 @@ int ankh_plan_attach_push_group_v1(ankh_plan_v1** plans, int world, char* err, s
         throw AnkhError(ANKH_INVALID_ARGUMENT, "plan group must hold ranks 0..world-1 of one sharding");
       bases[r] = plans[r]->plan->expansions_base();
     }
+    std::vector<std::vector<double*>> halo_recv(world, std::vector<double*>(world, nullptr));
+    for (int q = 0; q < world; ++q)
+      for (int r = 0; r < world; ++r) halo_recv[q][r] = plans[q]->plan->halo_recv_from(r);
     for (int r = 0; r < world; ++r)
-      on_plan(plans[r], [&](Plan& p) { p.attach_collective(ankh_b200::make_push_collective(r, world, bases)); });
+      on_plan(plans[r], [&](Plan& p) {
+        p.attach_collective(ankh_b200::make_push_collective(r, world, bases, halo_recv));
+      });
   });
 }
 
@@ -373,6 +378,36 @@ int ankh_shard_src_slice_v1(size_t n, int rank, int world, size_t* i0, size_t* i
 int ankh_shard_exchange_level_v1(int depth, int world) {
   if (depth < 1 || depth > 8 || world < 1) return -1;
   return ankh_b200::shard_exchange_level(depth, world);
+}
+
+int ankh_shard_halo_cells_v1(int level, int depth, int periodic, int src, int dst, int world,
+                             uint32_t* morton, size_t capacity, size_t* count) {
+  if (level < 0 || level > depth || depth < 1 || depth > 8 || world < 1 || src < 0 || src >= world ||
+      dst < 0 || dst >= world || !count)
+    return ANKH_INVALID_ARGUMENT;
+  try {
+    const auto cells = ankh_b200::shard_halo_cells(level, depth, periodic != 0, src, dst, world);
+    *count = cells.size();
+    if (morton)
+      for (size_t k = 0; k < cells.size() && k < capacity; ++k) morton[k] = cells[k];
+    return ANKH_OK;
+  } catch (...) {
+    return ANKH_RUNTIME_ERROR;
+  }
+}
+
+int ankh_shard_exchange_bytes_v1(int depth, int periodic, int order, int rank, int world, int halo,
+                                 size_t* recv_bytes, size_t* send_bytes) {
+  if (depth < 1 || depth > 8 || order < 2 || world < 1 || rank < 0 || rank >= world || !recv_bytes ||
+      !send_bytes)
+    return ANKH_INVALID_ARGUMENT;
+  try {
+    ankh_b200::shard_exchange_bytes(depth, periodic != 0, ankh_b200::exp_stride(order * order * order), rank,
+                                    world, halo != 0, recv_bytes, send_bytes);
+    return ANKH_OK;
+  } catch (...) {
+    return ANKH_RUNTIME_ERROR;
+  }
 }
 
 int ankh_shard_cell_owner_v1(int level, uint32_t cell, int depth, int world) {

@@ -207,6 +207,10 @@ void launch_svd_factors(const double* c_all, const double* w_all, const double* 
 void launch_m2l_pack(const M2LPack* ops, int n_ops, int max_rows, const int* perms,
                      const double* lf, const double* rf, int K, int Kp, double* factors,
                      cudaStream_t st);
+/// Halo rows (k_halo.cu): pack buf[j] = exp[row_off[j] ..+Kp] or, unpack,
+/// the reverse; Kp even, row offsets 16-B aligned.
+void launch_halo_rows(double* exp, const long long* row_off, long long n_rows, int Kp, double* buf,
+                      bool unpack, cudaStream_t st);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);
 

@@ -128,6 +128,7 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
   allocate();
   stamp("allocate", ts);
   if (pending_code_ == 0 && n > 0 && !csr_only_) {
+    build_halo();
     build_m2l();
     stamp("m2l", ts);
     if (periodic) build_periodic();
@@ -936,12 +937,78 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
   return launches;
 }
 
+// Halo lists of the deep levels: for every peer q, the rows
+// of this shard's cells q's M2L reads (send) and of q's cells this shard's
+// M2L reads (receive), at levels halo_level_ .. depth.  Both sides enumerate
+// a pair's list with the same rule in the same order, so the packed buffers
+// line up without any index exchange.  ANKH_SHARD_ALLGATHER=1 keeps the
+// whole-level all-gather (A/B).
+void Plan::build_halo() {
+  halo_level_ = depth + 1;
+  halo_.clear();
+  exchange_recv_bytes = exchange_send_bytes = 0;
+  if (!shard_upward_ || cfg.world <= 1) return;
+  const int G = cfg.world, r = cfg.rank;
+  if (!std::getenv("ANKH_SHARD_ALLGATHER")) halo_level_ = shard_halo_level(depth, G);
+  // the all-gathered levels exch_level_ .. halo_level_ - 1
+  for (int l = exch_level_; l < std::min(halo_level_, depth + 1); ++l) {
+    const std::size_t rows = static_cast<std::size_t>(1ll << (3 * l));
+    exchange_recv_bytes += (rows - rows / G) * Kp * sizeof(double);
+    exchange_send_bytes += (rows / G) * Kp * sizeof(double);
+  }
+  if (halo_level_ > depth) return;
+  std::vector<long long> send_off, recv_off;    // row offsets (doubles) into d_exp_
+  std::vector<std::size_t> send_at, recv_at;     // per peer: first packed row
+  for (int q = 0; q < G; ++q) {
+    if (q == r) continue;
+    send_at.push_back(send_off.size());
+    recv_at.push_back(recv_off.size());
+    for (int l = halo_level_; l <= depth; ++l) {
+      for (std::uint32_t m : shard_halo_cells(l, depth, periodic, r, q, G))
+        send_off.push_back(level_off_[l] + static_cast<long long>(m) * Kp);
+      for (std::uint32_t m : shard_halo_cells(l, depth, periodic, q, r, G))
+        recv_off.push_back(level_off_[l] + static_cast<long long>(m) * Kp);
+    }
+  }
+  send_at.push_back(send_off.size());
+  recv_at.push_back(recv_off.size());
+  halo_send_rows_ = static_cast<long long>(send_off.size());
+  halo_recv_rows_ = static_cast<long long>(recv_off.size());
+  d_halo_send_off_ = static_cast<long long*>(dalloc(std::max<std::size_t>(send_off.size(), 1) * sizeof(long long)));
+  d_halo_recv_off_ = static_cast<long long*>(dalloc(std::max<std::size_t>(recv_off.size(), 1) * sizeof(long long)));
+  d_halo_send_ = static_cast<double*>(dalloc(std::max<std::size_t>(send_off.size(), 1) * Kp * sizeof(double)));
+  d_halo_recv_ = static_cast<double*>(dalloc(std::max<std::size_t>(recv_off.size(), 1) * Kp * sizeof(double)));
+  ANKH_CUDA(cudaMemsetAsync(d_halo_recv_, 0, std::max<std::size_t>(recv_off.size(), 1) * Kp * sizeof(double), stream_));
+  if (!send_off.empty())
+    ANKH_CUDA(cudaMemcpyAsync(d_halo_send_off_, send_off.data(), send_off.size() * sizeof(long long),
+                              cudaMemcpyHostToDevice, stream_));
+  if (!recv_off.empty())
+    ANKH_CUDA(cudaMemcpyAsync(d_halo_recv_off_, recv_off.data(), recv_off.size() * sizeof(long long),
+                              cudaMemcpyHostToDevice, stream_));
+  for (int q = 0, k = 0; q < G; ++q) {
+    if (q == r) continue;
+    halo_.push_back({q, d_halo_send_ + send_at[k] * Kp, (send_at[k + 1] - send_at[k]) * Kp,
+                     d_halo_recv_ + recv_at[k] * Kp, (recv_at[k + 1] - recv_at[k]) * Kp});
+    ++k;
+  }
+  exchange_recv_bytes += recv_off.size() * Kp * sizeof(double);
+  exchange_send_bytes += send_off.size() * Kp * sizeof(double);
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+}
+
+double* Plan::halo_recv_from(int src) const {
+  for (const HaloPeer& h : halo_)
+    if (h.peer == src) return h.recv;
+  return nullptr;
+}
+
 // Sharded upward pass with a collective attached: M2M of this shard's own
 // subtree cells for the parent levels exch_level_ .. depth-1 (at level l the
 // shard owns Morton cells [r 8^l / G, (r+1) 8^l / G) -- whole subtrees, since
-// G | 8^exch_level_), then ONE grouped in-place all-gather of levels
-// exch_level_ .. depth; the levels above are completed redundantly by every
-// shard (m2m_top_).  Returns the launches.
+// G | 8^exch_level_), then ONE exchange group: an in-place all-gather of the
+// coarse levels exch_level_ .. halo_level_-1 and the M2L halo rows of the deep
+// levels (packed before, unpacked after); the levels above exch_level_ are
+// completed redundantly by every shard (m2m_top_).  Returns the launches.
 std::uint32_t Plan::exchange_upward(cudaStream_t st) {
   m2m_top_ = depth - 1;
   if (!coll_ || !shard_upward_) return 0;
@@ -955,11 +1022,19 @@ std::uint32_t Plan::exchange_upward(cudaStream_t st) {
   }
   std::vector<double*> recv;
   std::vector<std::size_t> count;
-  for (int l = exch_level_; l <= depth; ++l) {
+  for (int l = exch_level_; l <= std::min(halo_level_ - 1, depth); ++l) {
     recv.push_back(d_exp_ + level_off_[l]);
     count.push_back(static_cast<std::size_t>((1ll << (3 * l)) / G) * Kp);
   }
-  coll_->allgather_inplace_group(recv.data(), count.data(), static_cast<int>(recv.size()), st);
+  if (halo_send_rows_ > 0) {
+    launch_halo_rows(d_exp_, d_halo_send_off_, halo_send_rows_, Kp, d_halo_send_, false, st);
+    ++launches;
+  }
+  coll_->upward_exchange(recv.data(), count.data(), static_cast<int>(recv.size()), halo_, st);
+  if (halo_recv_rows_ > 0) {
+    launch_halo_rows(d_exp_, d_halo_recv_off_, halo_recv_rows_, Kp, d_halo_recv_, true, st);
+    ++launches;
+  }
   m2m_top_ = exch_level_ - 1;
   return launches;
 }

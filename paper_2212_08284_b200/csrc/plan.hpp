@@ -123,6 +123,8 @@ class Plan {
   /// this shard's P2M row range.
   double* leaf_level(std::int64_t* begin, std::int64_t* end, int* row_stride);
   double* expansions_base() const { return d_exp_; }
+  /// Receive buffer of this shard's halo rows from shard `src` (nullptr if none).
+  double* halo_recv_from(int src) const;
   /// Attach an NCCL (or other) collective: the plan then all-gathers the leaf
   /// level and all-reduces the result itself; reports carry job totals.
   void attach_collective(Collective* c);
@@ -139,6 +141,9 @@ class Plan {
   std::size_t m2l_instances = 0, m2l_operators = 0;
   double m2l_rank_mean = 0.0, far_flops = 0.0;
   std::size_t device_bytes = 0;
+  // upward exchange per evaluation (shards with a collective): bytes this
+  // shard receives -- the all-gathered coarse level plus the deep-level halos
+  std::size_t exchange_recv_bytes = 0, exchange_send_bytes = 0;
   double precompute_seconds = 0.0;
   bool precompute_reported = false;
 
@@ -180,6 +185,15 @@ class Plan {
   void validate_only(const double* d_pos, const double* d_src, cudaStream_t st);
   std::uint32_t exchange_upward(cudaStream_t st);
   int exch_level_ = 0;  // lowest level split evenly across shards (G | 8^l)
+  // Deep levels halo_level_ .. depth are exchanged as M2L halos (the cells
+  // within 3 of each peer's region, shard.cpp shard_halo_cells) instead of
+  // all-gathered: rows packed peer-major, then level-major, on both sides.
+  void build_halo();
+  int halo_level_ = 0;
+  std::vector<HaloPeer> halo_;
+  long long *d_halo_send_off_ = nullptr, *d_halo_recv_off_ = nullptr;
+  double *d_halo_send_ = nullptr, *d_halo_recv_ = nullptr;
+  long long halo_send_rows_ = 0, halo_recv_rows_ = 0;
   int m2m_top_ = 0;     // highest parent level the far chain still computes (all cells)
 
   std::unique_ptr<Collective> coll_;

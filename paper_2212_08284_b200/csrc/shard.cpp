@@ -40,6 +40,80 @@ int shard_exchange_level(int depth, int world) {
   return l0;
 }
 
+namespace {
+std::uint32_t compact3(std::uint32_t v) {
+  v &= 0x09249249u;
+  v = (v ^ (v >> 2)) & 0x030c30c3u;
+  v = (v ^ (v >> 4)) & 0x0300f00fu;
+  v = (v ^ (v >> 8)) & 0x030000ffu;
+  v = (v ^ (v >> 16)) & 0x000003ffu;
+  return v;
+}
+}  // namespace
+
+int shard_halo_level(int depth, int world) {
+  return world <= 1 ? depth + 1 : shard_exchange_level(depth, world) + 1;
+}
+
+std::vector<std::uint32_t> shard_halo_cells(int level, int depth, bool periodic, int src, int dst,
+                                            int world) {
+  std::vector<std::uint32_t> out;
+  const std::int64_t cells = std::int64_t(1) << (3 * level);
+  if (world <= 1 || src == dst || cells % world != 0) return out;
+  (void)depth;
+  const int n = 1 << level;
+  // dst's region: the Morton-aligned block [dst cells/G, (dst+1) cells/G) is a
+  // box; its first and last cells are its min and max corners
+  const std::uint32_t m0 = static_cast<std::uint32_t>(cells * dst / world);
+  const std::uint32_t m1 = static_cast<std::uint32_t>(cells * (dst + 1) / world) - 1;
+  const int lo[3] = {static_cast<int>(compact3(m0 >> 2)), static_cast<int>(compact3(m0 >> 1)),
+                     static_cast<int>(compact3(m0))};
+  const int hi[3] = {static_cast<int>(compact3(m1 >> 2)), static_cast<int>(compact3(m1 >> 1)),
+                     static_cast<int>(compact3(m1))};
+  // Reach of the interaction lists past the region's faces: Lambda(t)
+  // offsets are s - t in [-2-c, 3-c] with c = t & 1 (octree.cpp:79-87), so
+  // past an even lower face (odd upper face) only 2 cells can pair with a
+  // cell inside -- in either direction of the unordered instance -- and 3
+  // past a face of the other parity (regions one cell wide).  n is even, so
+  // parities survive the periodic wrap.
+  auto near = [&](int x, int a) {
+    if (x >= lo[a] && x <= hi[a]) return true;
+    const int reach_lo = (lo[a] & 1) ? 3 : 2, reach_hi = (hi[a] & 1) ? 2 : 3;
+    if (periodic) {
+      const int below = ((lo[a] - x) % n + n) % n, above = ((x - hi[a]) % n + n) % n;
+      return below <= reach_lo || above <= reach_hi;
+    }
+    return x < lo[a] ? lo[a] - x <= reach_lo : x - hi[a] <= reach_hi;
+  };
+  const std::uint32_t s0 = static_cast<std::uint32_t>(cells * src / world);
+  const std::uint32_t s1 = static_cast<std::uint32_t>(cells * (src + 1) / world);
+  for (std::uint32_t m = s0; m < s1; ++m)
+    if (near(static_cast<int>(compact3(m >> 2)), 0) && near(static_cast<int>(compact3(m >> 1)), 1) &&
+        near(static_cast<int>(compact3(m)), 2))
+      out.push_back(m);
+  return out;
+}
+
+void shard_exchange_bytes(int depth, bool periodic, int row_doubles, int rank, int world, bool halo,
+                          std::size_t* recv, std::size_t* send) {
+  *recv = *send = 0;
+  if (world <= 1) return;
+  const int l0 = shard_exchange_level(depth, world);
+  const int lh = halo ? shard_halo_level(depth, world) : depth + 1;
+  const std::size_t row = static_cast<std::size_t>(row_doubles) * sizeof(double);
+  for (int l = l0; l <= std::min(lh - 1, depth); ++l) {
+    const std::size_t cells = std::size_t(1) << (3 * l);
+    *recv += (cells - cells / world) * row;
+    *send += (cells / world) * row;
+  }
+  for (int l = lh; l <= depth; ++l)
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) continue;
+      *recv += shard_halo_cells(l, depth, periodic, q, rank, world).size() * row;
+      *send += shard_halo_cells(l, depth, periodic, rank, q, world).size() * row;
+    }
+}
+
 int shard_m2l_owner(int level, std::uint32_t t, std::uint32_t s, int depth, int world) {
   if (world <= 1) return 0;
   // the owner of t or of s, by a hash of the pair: every cell has the same

@@ -27,6 +27,27 @@ void shard_src_slice(std::size_t n, int rank, int world, std::size_t* i0, std::s
 /// `depth` (the upward exchange all-gathers levels l .. depth).
 int shard_exchange_level(int depth, int world);
 
+/// M2L halo of the deep levels: Morton cells of `level`
+/// (ascending) that shard `src` owns and shard `dst` reads -- every cell that
+/// can form an M2L instance with a cell of dst's own region (an instance is
+/// owned by the owner of t or of s, fmm.cpp:43-50): within 2 cells of the
+/// region's faces (3 past a face of odd parity), periodic wrap when
+/// `periodic`.  Requires world | 8^level (shard regions are then
+/// Morton-aligned boxes); src == dst or world == 1 gives an empty list.
+std::vector<std::uint32_t> shard_halo_cells(int level, int depth, bool periodic, int src, int dst,
+                                            int world);
+/// Lowest level whose cells are exchanged as a halo instead of an all-gather:
+/// shard_exchange_level + 1 (the exchange level itself is all-gathered, the
+/// redundant M2M above it needs every cell).  > depth: no halo levels.
+int shard_halo_level(int depth, int world);
+
+/// Bytes shard `rank` receives / sends in one upward exchange (rows of
+/// `row_doubles` doubles): the all-gathered levels exch .. halo-1 plus the
+/// deep-level halos.  `halo` false: the whole-level all-gather of every level
+/// exch .. depth (the former schedule, for comparison).
+void shard_exchange_bytes(int depth, bool periodic, int row_doubles, int rank, int world, bool halo,
+                          std::size_t* recv, std::size_t* send);
+
 /// Owner shard of lex cell `cell` at `level` in a depth-`depth` tree.
 int shard_cell_owner(int level, std::uint32_t cell, int depth, int world);
 

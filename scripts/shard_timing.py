@@ -7,9 +7,10 @@ Two modes per world size:
                 back to back on one stream, no exchange;
   * overlap  -- the production schedule: the plan's CUDA graph with P2P
                 concurrent with the far chain, and a loopback exchange
-                (ankh_plan_attach_loopback_v1: the leaf all-gather's bytes
+                (ankh_plan_attach_loopback_v1: the exchange's bytes -- the
+                all-gathered exchange level and the deep-level M2L halos --
                 land by device copies, the all-reduce is the identity).  The
-                NVLink time of the real all-gather is not included; it is
+                NVLink time of the real exchange is not included; it is
                 printed beside as bytes received per rank.
 """
 import os
@@ -64,8 +65,13 @@ for world in (1, 2, 4, 8):
             plan.close()
         t = max(times)
         base.setdefault(mode, t)
-        leaf_bytes = (8 ** info["depth"]) * (-(-(L ** 3) // 32) * 32) * 8 * (world - 1) / world
+        import ctypes
+        rv, sd = ctypes.c_size_t(), ctypes.c_size_t()
+        halo = 0 if os.environ.get("ANKH_SHARD_ALLGATHER") else 1
+        ankh.lib().ankh_shard_exchange_bytes_v1(info["depth"], 1, L, 0, world, halo, ctypes.byref(rv),
+                                                ctypes.byref(sd))
+        leaf_bytes = rv.value
         print(f"world {world} {mode:7s}: per-rank {t:.3f} ms (ranks {sorted({0, world - 1})}: "
               f"{', '.join(f'{x:.3f}' for x in times)}), efficiency bound {base[mode] / (world * t):.2f}"
-              f"{'' if mode == 'serial' else f', all-gather receives {leaf_bytes / 1e6:.1f} MB per rank'}",
+              f"{'' if mode == 'serial' else f', exchange receives {leaf_bytes / 1e6:.1f} MB per rank'}",
               flush=True)

@@ -519,18 +519,22 @@ def test_loopback_shards_sliced_moments(cuda, world):
         p.close()
 
 
-@pytest.mark.parametrize("world, p", [(2, 15), (4, 15), (8, 15), (8, 0)])
-def test_push_group_shards_match_single_gpu(cuda, world, p):
+@pytest.mark.parametrize("world, p, config, L", [(2, 15, 1, 4), (4, 15, 1, 4), (8, 15, 1, 4), (8, 0, 1, 4),
+                                                 (8, 15, 2, 3), (4, 0, 2, 3), (64, 15, 2, 3)])
+def test_push_group_shards_match_single_gpu(cuda, world, p, config, L):
     """The collective-attached schedule end to end on one GPU: every shard
     runs its own graph (sliced moment checks, P2M and M2M of its own subtree,
-    grouped all-gather of the levels it shares, redundant top levels, its M2L
-    and P2P share) and exchanges through stream-ordered pushes into the other
-    shards' arrays.  From the second evaluation on, the shards' partial
-    energies -- far field included -- sum to the single-GPU result."""
+    all-gather of the exchange level, point-to-point M2L halos of the deep
+    levels -- packed, pushed into the peers' receive buffers, unpacked --
+    redundant top levels, its M2L and P2P share) and exchanges through
+    stream-ordered pushes into the other shards' arrays.  From the second
+    evaluation on, the shards' partial energies -- far field included -- sum
+    to the single-GPU result.  Config 2 (depth 4) has halos that are a strict
+    part of the level, so a missing halo cell would change e_far."""
     torch = cuda
-    pos, src, rb, cfg = inputs.make_config(1)  # depth 3
+    pos, src, rb, cfg = inputs.make_config(config)
     n = pos.shape[0]
-    ec = ankh.EwaldConfig(order_cheb=4, order_equi=4, p=p)
+    ec = ankh.EwaldConfig(order_cheb=L, order_equi=L, p=p)
     dp, ds = torch.from_numpy(pos).cuda(), torch.from_numpy(src).cuda()
     whole = ankh.Plan(n, rb, ec).energy_device(dp, ds)
     plans = [ankh.Plan(n, rb, ec, rank=r, world=world, phase_timing=False) for r in range(world)]

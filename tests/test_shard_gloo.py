@@ -199,3 +199,59 @@ def test_two_shards_gloo_allreduce(tmp_path):
     assert abs(got[1] - want["e_near"]) <= 1e-12 * comps
     assert abs(got[2] - want["e_far"]) <= 1e-12 * comps
     assert abs(got.sum() - want["e_total"]) <= 1e-11 * comps
+
+
+def halo_cells(level, depth, periodic, src, dst, world):
+    cnt = ctypes.c_size_t(0)
+    assert lib().ankh_shard_halo_cells_v1(level, depth, int(periodic), src, dst, world, None, 0,
+                                           ctypes.byref(cnt)) == 0
+    out = np.zeros(max(cnt.value, 1), np.uint32)
+    assert lib().ankh_shard_halo_cells_v1(level, depth, int(periodic), src, dst, world,
+                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                           cnt.value, ctypes.byref(cnt)) == 0
+    return set(int(v) for v in out[:cnt.value])
+
+
+@pytest.mark.parametrize("depth,world,periodic", [(3, 2, True), (3, 8, True), (4, 8, True),
+                                                  (4, 4, False), (4, 64, True), (3, 8, False)])
+def test_halo_covers_every_m2l_read(depth, world, periodic):
+    """Every cell a shard's M2L instances read at a halo level is either its
+    own or in the halo list its owner sends it, and halo lists
+    hold only the sender's own cells."""
+    lh = lib().ankh_shard_exchange_level_v1(depth, world) + 1
+    for r in range(world):
+        lv, t, s, off = m2l_instances(depth, periodic, r, world)
+        for level in range(lh, depth + 1):
+            n = 1 << level
+            cells = 8 ** level
+            own = lambda m, q: cells * q // world <= m < cells * (q + 1) // world
+            sel = lv == level
+            recv = {q: halo_cells(level, depth, periodic, q, r, world) for q in range(world) if q != r}
+            for q, hs in recv.items():
+                assert all(own(m, q) for m in hs)
+            for c in np.concatenate([t[sel], s[sel]]):
+                c = int(c)
+                m = morton(c // (n * n), (c // n) % n, c % n)
+                if own(m, r):
+                    continue
+                q = m * world // cells
+                assert m in recv[q], (level, r, q, m)
+
+
+def test_halo_exchange_bytes_config4():
+    """§8e: at config 4 (depth 6, L = 5) on 8 GPUs a shard receives <= 30 MB
+    per evaluation (20.0 MB; the whole-level all-gather received 235 MB); at
+    config 3 (depth 5) 5.8 MB instead of 29.4 MB."""
+    def bytes_(depth, rank, halo):
+        rv, sd = ctypes.c_size_t(), ctypes.c_size_t()
+        assert lib().ankh_shard_exchange_bytes_v1(depth, 1, 5, rank, 8, int(halo), ctypes.byref(rv),
+                                                  ctypes.byref(sd)) == 0
+        return rv.value, sd.value
+    for r in range(8):
+        h4, _ = bytes_(6, r, True)
+        a4, _ = bytes_(6, r, False)
+        assert h4 <= 30e6, h4
+        assert a4 > 200e6
+        h3, _ = bytes_(5, r, True)
+        a3, _ = bytes_(5, r, False)
+        assert h3 < 0.5 * a3, (h3, a3)
