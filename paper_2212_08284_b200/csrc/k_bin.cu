@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
                                              double rb, double inv_side, int nax,
                                              unsigned* __restrict__ keys,
                                              unsigned* __restrict__ idx,
-                                             unsigned* __restrict__ counts, DevResult* res) {
+                                             unsigned* __restrict__ counts,
+                                             const unsigned char* __restrict__ need, DevResult* res) {
   const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
   bool mp = false;
   if (i < n) {
@@ -73,8 +74,13 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
     keys[i] = key;
     // counting sort: idx receives the particle's arrival slot in its leaf
     // (ascending order inside the leaf is restored by k_leaf_gather);
-    // without counts (validation path) idx is the identity for the radix sort
-    idx[i] = counts ? atomicAdd(&counts[key], 1u) : static_cast<unsigned>(i);
+    // without counts (validation path) idx is the identity for the radix sort.
+    // A shard (need != nullptr) sorts only the leaves it reads: the others
+    // stay empty in its CSR (every particle is still validated above).
+    if (!counts)
+      idx[i] = static_cast<unsigned>(i);
+    else
+      idx[i] = (need && !need[key]) ? ~0u : atomicAdd(&counts[key], 1u);
   }
   if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
 }
@@ -86,7 +92,7 @@ __global__ void __launch_bounds__(256) k_scatter(const unsigned* __restrict__ ke
                                                  const unsigned* __restrict__ offsets,
                                                  std::size_t n, unsigned* __restrict__ unsorted) {
   const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || slots[i] == ~0u) return;  // ~0u: a leaf this shard does not read
   unsorted[offsets[keys[i]] + slots[i]] = static_cast<unsigned>(i);
 }
 
@@ -124,13 +130,16 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     const unsigned* __restrict__ offsets, unsigned* __restrict__ unsorted,
     unsigned* __restrict__ scratch, unsigned* __restrict__ sorted,
     const unsigned char* __restrict__ need, double* __restrict__ part, bool check_src,
-    DevResult* res) {
+    DevResult* res, unsigned* __restrict__ leaf_mp) {
   __shared__ unsigned a[kLeafSmem], b[kLeafSmem];
   const unsigned leaf = blockIdx.x;
   if (need && !need[leaf]) return;  // another shard's leaf
   const unsigned base = offsets[leaf];
   const int c = static_cast<int>(offsets[leaf + 1] - base);
-  if (c == 0) return;
+  if (c == 0) {
+    if (part && leaf_mp && threadIdx.x == 0) leaf_mp[leaf] = 0u;
+    return;
+  }
   const unsigned* order;
   if (c <= kLeafSmem) {
     for (int e = threadIdx.x; e < c; e += kLeafThreads) a[e] = unsorted[base + e];
@@ -203,24 +212,46 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
       b = ss[4];
       out[3] = make_double2(a, b);
     }
-    if (check_src) {
-      if (!(isfinite(a) && isfinite(b) && isfinite(c2) && isfinite(d)))
-        atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
-      mp = mp || a != 0.0 || b != 0.0 || d != 0.0;  // (c2 is q: not a multipole)
-    }
+    if (check_src && !(isfinite(a) && isfinite(b) && isfinite(c2) && isfinite(d)))
+      atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
+    mp = mp || a != 0.0 || b != 0.0 || d != 0.0;  // (c2 is q: not a multipole)
   }
-  if (check_src && __syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
+  mp = __syncthreads_or(mp);
+  if (threadIdx.x == 0) {
+    if (leaf_mp) leaf_mp[leaf] = mp ? 1u : 0u;  // the P2P kernel's per-leaf pair code
+    if (check_src && mp) atomicOr(&res->any_multipole, 1);
+  }
 }
 
 // Records in leaf order from an existing sorted index (the moments of a
 // plan whose positions were bound by ankh_plan_set_positions_v1).
+// Per-leaf multipole flag of a scattered record: lanes with the same leaf
+// combine first (consecutive particles mostly share a leaf), one atomic each.
+__device__ __forceinline__ void flag_leaf(bool active, bool mp, unsigned key, unsigned* leaf_mp) {
+  const bool want = active && mp;
+  const unsigned k = want ? key : ~0u;
+  const unsigned peers = __match_any_sync(0xffffffffu, k);
+  if (want && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicOr(&leaf_mp[key], 1u);
+}
+
+__device__ __forceinline__ bool src_has_multipole(const double* __restrict__ s) {
+  bool m = false;
+#pragma unroll
+  for (int k = 1; k < 10; ++k) m = m || s[k] != 0.0;
+  return m;
+}
+
 __global__ void __launch_bounds__(256) k_gather_sorted(const double* __restrict__ pos,
                                                        const double* __restrict__ src,
                                                        const unsigned* __restrict__ sorted,
-                                                       std::size_t n, double* __restrict__ part) {
+                                                       std::size_t n, double* __restrict__ part,
+                                                       const unsigned* __restrict__ keys,
+                                                       unsigned* __restrict__ leaf_mp) {
   const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (j >= n) return;
-  write_record(pos, src, sorted[j], part + j * kRec);
+  const bool ok = j < n;
+  const unsigned i = ok ? sorted[j] : 0u;
+  if (ok) write_record(pos, src, i, part + j * kRec);
+  if (leaf_mp) flag_leaf(ok, ok && src_has_multipole(src + 10 * static_cast<std::size_t>(i)), ok ? keys[i] : 0u, leaf_mp);
 }
 
 // The moment half of validate_system (types.cpp:16-63) for particles
@@ -231,13 +262,16 @@ __global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ sr
                                                    DevResult* res, unsigned block0,
                                                    const double* __restrict__ pos,
                                                    const unsigned* __restrict__ inv,
-                                                   double* __restrict__ part) {
+                                                   double* __restrict__ part,
+                                                   const unsigned* __restrict__ keys,
+                                                   unsigned* __restrict__ leaf_mp) {
   const std::size_t i = (static_cast<std::size_t>(block0) + blockIdx.x) * 256 + threadIdx.x;
   bool mp = false;
   if (i < n) {
     if (inv) write_record(pos, src, static_cast<unsigned>(i), part + static_cast<std::size_t>(inv[i]) * kRec);
     mp = check_moments(src + 10 * i, i, res);
   }
+  if (leaf_mp) flag_leaf(i < n, src_has_multipole(src + 10 * (i < n ? i : 0)), i < n ? keys[i] : 0u, leaf_mp);
   if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
 }
 
@@ -410,10 +444,10 @@ void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, c
 
 void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
                 double inv_side, int n_axis, unsigned* keys, unsigned* idx, unsigned* counts,
-                DevResult* res, cudaStream_t st) {
+                DevResult* res, cudaStream_t st, const unsigned char* need) {
   if (n == 0) return;
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  k_bin<<<blocks, 256, 0, st>>>(pos, src, n, box_radius, inv_side, n_axis, keys, idx, counts, res);
+  k_bin<<<blocks, 256, 0, st>>>(pos, src, n, box_radius, inv_side, n_axis, keys, idx, counts, need, res);
 }
 
 void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
@@ -421,29 +455,32 @@ void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
                           unsigned* sorted, std::size_t n, int n_leaves,
                           const unsigned char* need, double* part, cudaStream_t st,
-                          bool check_src, DevResult* res) {
+                          bool check_src, DevResult* res, unsigned* leaf_mp) {
   std::size_t bytes = temp_bytes;
   cub::DeviceScan::ExclusiveSum(temp, bytes, counts, offsets, n_leaves + 1, st);
   if (n == 0) return;
   k_scatter<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, slots, offsets, n,
                                                                     unsorted);
   k_leaf_gather<<<static_cast<unsigned>(n_leaves), kLeafThreads, 0, st>>>(
-      pos, src, offsets, unsorted, scratch, sorted, need, part, check_src && part != nullptr, res);
+      pos, src, offsets, unsorted, scratch, sorted, need, part, check_src && part != nullptr, res, leaf_mp);
 }
 
 void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
-                       std::size_t n, DevResult* res, double* part, cudaStream_t st) {
+                       std::size_t n, DevResult* res, double* part, cudaStream_t st,
+                       const unsigned* keys, unsigned* leaf_mp) {
   if (n == 0) return;
   const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  k_src_check<<<blocks, 256, 0, st>>>(src, n, res, 0u, nullptr, nullptr, nullptr);
-  k_gather_sorted<<<blocks, 256, 0, st>>>(pos, src, sorted, n, part);
+  k_src_check<<<blocks, 256, 0, st>>>(src, n, res, 0u, nullptr, nullptr, nullptr, nullptr, nullptr);
+  k_gather_sorted<<<blocks, 256, 0, st>>>(pos, src, sorted, n, part, keys, leaf_mp);
 }
 
 void launch_src_chunk(const double* pos, const double* src, const unsigned* inv, std::size_t i0,
-                      std::size_t i1, DevResult* res, double* part, cudaStream_t st) {
+                      std::size_t i1, DevResult* res, double* part, cudaStream_t st,
+                      const unsigned* keys, unsigned* leaf_mp) {
   if (i1 <= i0) return;  // i0 is a multiple of 256
   const unsigned blocks = static_cast<unsigned>((i1 - i0 + 255) / 256);
-  k_src_check<<<blocks, 256, 0, st>>>(src, i1, res, static_cast<unsigned>(i0 / 256), pos, inv, part);
+  k_src_check<<<blocks, 256, 0, st>>>(src, i1, res, static_cast<unsigned>(i0 / 256), pos, inv, part, keys,
+                                      leaf_mp);
 }
 
 void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,

@@ -96,7 +96,7 @@ struct M2LOp {
 // ---- launchers (defined in the .cu files) ----
 void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
                 double inv_side, int n_axis, unsigned* keys, unsigned* idx, unsigned* counts,
-                DevResult* res, cudaStream_t st);
+                DevResult* res, cudaStream_t st, const unsigned char* need = nullptr);
 std::size_t sort_temp_bytes(std::size_t n, int n_leaves);
 void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
                  const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
@@ -114,7 +114,8 @@ void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int ord
 // streamed host path (k_bin.cu): one arrived chunk [i0, i1) of the moments --
 // validation, self-energy partials, records scattered to their sorted slots
 void launch_src_chunk(const double* pos, const double* src, const unsigned* inv, std::size_t i0,
-                      std::size_t i1, DevResult* res, double* part, cudaStream_t st);
+                      std::size_t i1, DevResult* res, double* part, cudaStream_t st,
+                      const unsigned* keys = nullptr, unsigned* leaf_mp = nullptr);
 // inverse permutation, per-leaf readiness chunk (P2M: own records; P2P: + the
 // 13 half-shell neighbours), per-chunk leaf lists and their bounds
 // (bounds[0..C] P2M, bounds[C+1..2C+1] P2P)
@@ -143,7 +144,9 @@ struct P2PRadial {
 // list != nullptr: the target leaves are list[bounds[0] .. bounds[1]) (Morton
 // indices, list_grid of them -- the host knows the count), partials still
 // indexed by leaf - leaf_begin (streamed host path)
-int launch_p2p(const double* part, const unsigned* leaf_off, int depth, int periodic,
+/// leaf_mp[lex leaf] != 0: the leaf holds a dipole or quadrupole (written
+/// with the records: launch_bucket_gather / launch_src_gather / launch_src_chunk).
+int launch_p2p(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth, int periodic,
                double period, double xi, const P2PRadial& rad, int cap, int leaf_begin,
                int leaf_end, double* near_partial, unsigned long long* pair_count, DevResult* res,
                cudaStream_t st, const unsigned* list = nullptr, const unsigned* bounds = nullptr,
@@ -160,8 +163,10 @@ void launch_finalize(const double* near_partial, int n_near, const unsigned long
 std::size_t finalize_scratch_bytes();
 /// Bound-positions path: moment validation + self-energy partials (k_bin's
 /// block layout) and the records gathered through an existing sorted index.
+/// keys[i]: particle i's lex leaf; leaf_mp (zeroed by the caller) is OR-ed.
 void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
-                       std::size_t n, DevResult* res, double* part, cudaStream_t st);
+                       std::size_t n, DevResult* res, double* part, cudaStream_t st,
+                       const unsigned* keys, unsigned* leaf_mp);
 /// counts != nullptr: also zero counts[0, n_counts) (the leaf histogram).
 void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole = 0,
                         unsigned* counts = nullptr, unsigned n_counts = 0);
@@ -176,7 +181,7 @@ void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
                           unsigned* sorted, std::size_t n, int n_leaves,
                           const unsigned char* need, double* part, cudaStream_t st,
-                          bool check_src = false, DevResult* res = nullptr);
+                          bool check_src = false, DevResult* res = nullptr, unsigned* leaf_mp = nullptr);
 double probe_fp64_tflops(int iters);
 /// ms of k_mix<mode> (k_probe.cu): DFMA-only, DMMA-only, or half/half warps
 double probe_fp64_mix_ms(int mode, int it_f, int it_m);

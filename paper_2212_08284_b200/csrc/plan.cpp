@@ -257,6 +257,8 @@ void Plan::allocate() {
   d_idx2_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
   d_counts_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
   d_off_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
+  d_leaf_mp_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
+  ANKH_CUDA(cudaMemsetAsync(d_leaf_mp_, 0, static_cast<std::size_t>(n_leaves) * sizeof(unsigned), stream_));
   d_fin_scratch_ = static_cast<double*>(dalloc(finalize_scratch_bytes()));
   ANKH_CUDA(cudaMemsetAsync(d_fin_scratch_, 0, finalize_scratch_bytes(), stream_));  // completion counter
   // A shard gathers particle records only for the leaves it reads: its P2P
@@ -728,7 +730,8 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     // positions validated and sorted by set_positions: start from their flags,
     // validate the moments, gather the records through the sorted index
     ANKH_CUDA(cudaMemcpyAsync(d_res_, d_res_pos_, sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
-    launch_src_gather(d_pos, d_src, d_idx2_, n, d_res_, d_part_, st);
+    ANKH_CUDA(cudaMemsetAsync(d_leaf_mp_, 0, static_cast<std::size_t>(n_leaves) * sizeof(unsigned), st));
+    launch_src_gather(d_pos, d_src, d_idx2_, n, d_res_, d_part_, st, d_keys_, d_leaf_mp_);
     launches += 2;
   } else if (mode != 2) {
     // sliced moments: other slices' multipoles are unseen, so the kernels
@@ -741,7 +744,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     // read of them), by a slice pass on sliced shards, else by k_bin
     const bool gather_src = gather_checks_src();
     launch_bin(d_pos, (slice_src_ || gather_src) ? nullptr : d_src, n, rb, inv_side, nax, d_keys_, d_idx_,
-               d_counts_, d_res_, st);
+               d_counts_, d_res_, st, d_need_);
     ++launches;
     if (slice_src_ && src_i1_ > src_i0_) {  // this shard's moment slice (self partials, flags)
       launch_src_chunk(d_pos, d_src, nullptr, src_i0_, src_i1_, d_res_, nullptr, st);
@@ -750,7 +753,8 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     // counting sort by leaf: d_idx_ holds the arrival slots, d_keys2_ the
     // scattered indices, d_idx2_ the leaf CSR's ascending indices
     launch_bucket_gather(d_temp_, temp_bytes_, d_pos, d_src, d_keys_, d_idx_, d_counts_, d_off_,
-                         d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, d_part_, st, gather_src, d_res_);
+                         d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, d_part_, st, gather_src, d_res_,
+                         d_leaf_mp_);
     launches += 2;
   }
   if (csr_only_) {
@@ -806,7 +810,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   if (!serial) ANKH_CUDA(cudaEventRecord(ev_join_, far));
   // near field: P2P (fmm.cpp:278-327)
   const int n_near_parts =
-      launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
+      launch_p2p(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
                  p2p_cap_, leaf_begin_, leaf_end_,
                  d_near_part_, d_pair_count_, d_res_, st);
   ++launches;
@@ -1198,6 +1202,8 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   } else {
     ANKH_CUDA(cudaMemcpyAsync(d_res_, d_res_pos_, sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
   }
+  // per-leaf multipole flags: OR-ed by the chunk gathers below
+  ANKH_CUDA(cudaMemsetAsync(d_leaf_mp_, 0, static_cast<std::size_t>(n_leaves) * sizeof(unsigned), st));
   ANKH_CUDA(cudaEventRecord(ev_s_sorted_, st));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[1], st));
   mark("sorted + lists", st);
@@ -1213,7 +1219,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   for (int c = 0; c < C; ++c) {
     const std::size_t i0 = c * chunk, i1 = std::min(n, i0 + chunk);
     ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_chunk_[c], 0));
-    launch_src_chunk(d_pos_, d_src_, d_inv_, i0, i1, d_res_, d_part_, gather_stream_);
+    launch_src_chunk(d_pos_, d_src_, d_inv_, i0, i1, d_res_, d_part_, gather_stream_, d_keys_, d_leaf_mp_);
     ANKH_CUDA(cudaEventRecord(ev_s_gath_[c], gather_stream_));
     mark("gather " + std::to_string(c), gather_stream_);
     const unsigned n_m = h_sbounds_[c + 1] - h_sbounds_[c];
@@ -1230,7 +1236,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
       ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[c], 0));
       if (timing && !near_started) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
       near_started = true;
-      n_near_parts = launch_p2p(d_part_, d_off_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, p2p_cap_,
+      n_near_parts = launch_p2p(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, p2p_cap_,
                                 leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, st, d_list_p2p_,
                                 d_sbounds_ + (C + 1) + c, static_cast<int>(n_p));
       ++launches;
@@ -1337,7 +1343,7 @@ void Plan::set_positions(const double* h_pos, cudaStream_t st) {
   if (pending_code_ == 0 && !csr_only_) {
     launch_init_result(d_res_pos_, st, 0, d_counts_, static_cast<unsigned>(n_leaves + 1));
     const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
-    launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, d_res_pos_, st);
+    launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, d_res_pos_, st, d_need_);
     launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_,
                          d_off_, d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
   }
