@@ -486,9 +486,11 @@ void launch_src_chunk(const double* pos, const double* src, const unsigned* inv,
 void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,
                            int periodic, unsigned chunk, int n_chunks, unsigned* inv,
                            unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
-                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st, unsigned* host_bounds) {
+                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st, unsigned* host_bounds,
+                           cudaEvent_t after_inverse) {
   const unsigned n_leaves = 1u << (3 * depth);
   if (n > 0) k_inverse<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(sorted, n, inv);
+  if (after_inverse) cudaEventRecord(after_inverse, st);  // the chunk gathers need only `inv`
   cudaMemsetAsync(cnt, 0, 2 * n_chunks * sizeof(unsigned), st);
   k_stream_ready<<<(n_leaves + 255) / 256, 256, 0, st>>>(offsets, sorted, depth, periodic, chunk,
                                                         n_chunks, ready, cnt);

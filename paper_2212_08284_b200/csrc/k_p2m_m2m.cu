@@ -93,8 +93,10 @@ __global__ void __launch_bounds__(kP2MThreads, ANKH_P2M_MINB) k_p2m_w(const doub
   (void)hd_g;
   const int n = 1 << depth;
   // leaves are visited (and their expansions stored) in Morton order
-  // list mode (streamed host path): the leaves list[bounds[0] .. bounds[1])
-  const unsigned item = blockIdx.x * kP2MWarps + warp;
+  // list mode (streamed host path): the leaves list[bounds[0] .. bounds[1]),
+  // warps striding over them (the grid is sized without knowing the count)
+  const unsigned stride = list ? gridDim.x * kP2MWarps : 0u;
+  for (unsigned item = blockIdx.x * kP2MWarps + warp;; item += stride) {
   unsigned m;
   if (list) {
     if (item >= bounds[1] - bounds[0]) return;
@@ -245,6 +247,8 @@ __global__ void __launch_bounds__(kP2MThreads, ANKH_P2M_MINB) k_p2m_w(const doub
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) self_acc += __shfl_down_sync(0xffffffffu, self_acc, o);
   if (lane == 0) self_leaf[m] = self_acc;
+  if (!list) return;
+  }  // list mode: next leaf
 }
 
 template <int L>
@@ -503,6 +507,7 @@ void p2m_order(const double* part, const unsigned* leaf_off, int depth, double r
   const std::size_t smem = sizeof(double) * P2MWShape<LW>::smem_doubles;
   static std::atomic<unsigned long long> attr{0};
   smem_opt_in(attr, k_p2m_w<LW>, smem);
+  // list mode: list_count is an upper bound of the leaves (the warps stride)
   k_p2m_w<LW><<<(leaves + kP2MWarps - 1) / kP2MWarps, kP2MThreads, smem, st>>>(
       part, leaf_off, depth, rb, hd, exp_leaf, m_begin, m_end, list, bounds, self_leaf, c_mu, c_th);
 }

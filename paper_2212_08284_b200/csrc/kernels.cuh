@@ -123,7 +123,7 @@ void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std:
                            int periodic, unsigned chunk, int n_chunks, unsigned* inv,
                            unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
                            unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st,
-                           unsigned* host_bounds = nullptr);
+                           unsigned* host_bounds = nullptr, cudaEvent_t after_inverse = nullptr);
 /// Parents [p_begin, p_begin + p_count) of `parent_level` (Morton); p_count 0: all.
 void launch_m2m(const double* child, double* parent, int parent_level, int order,
                 const double* m2m, cudaStream_t st, unsigned p_begin = 0, unsigned p_count = 0);

@@ -166,7 +166,7 @@ Plan::~Plan() {
       cudaStreamSynchronize(s);
       cudaStreamDestroy(s);
     }
-  for (cudaEvent_t e : {ev_s_start_, ev_s_pos_, ev_s_sorted_})
+  for (cudaEvent_t e : {ev_s_start_, ev_s_pos_, ev_s_sorted_, ev_s_inv_, ev_s_p2p2_})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_t_)
     if (e) cudaEventDestroy(e);
@@ -174,7 +174,10 @@ Plan::~Plan() {
     if (ev_s_chunk_[c]) cudaEventDestroy(ev_s_chunk_[c]);
     if (ev_s_gath_[c]) cudaEventDestroy(ev_s_gath_[c]);
   }
-  if (h_sbounds_) cudaFreeHost(h_sbounds_);
+  if (p2p_stream2_) {
+    cudaStreamSynchronize(p2p_stream2_);
+    cudaStreamDestroy(p2p_stream2_);
+  }
   if (side_stream_) {
     cudaStreamSynchronize(side_stream_);
     cudaStreamDestroy(side_stream_);
@@ -1117,12 +1120,11 @@ void Plan::stream_setup() {
     d_sbounds_ = static_cast<unsigned*>(dalloc(2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
     d_list_p2m_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
     d_list_p2p_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
-    ANKH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_sbounds_), 2 * (kMaxStreamChunks + 1) * sizeof(unsigned),
-                            cudaHostAllocMapped));
-    ANKH_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_sbounds_dev_), h_sbounds_, 0));
+    ANKH_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device_));
+    ANKH_CUDA(cudaStreamCreateWithFlags(&p2p_stream2_, cudaStreamNonBlocking));
     ANKH_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
     ANKH_CUDA(cudaStreamCreateWithPriority(&gather_stream_, cudaStreamNonBlocking, hi_prio_));
-    for (cudaEvent_t* e : {&ev_s_start_, &ev_s_pos_, &ev_s_sorted_})
+    for (cudaEvent_t* e : {&ev_s_start_, &ev_s_pos_, &ev_s_sorted_, &ev_s_inv_, &ev_s_p2p2_})
       ANKH_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (int c = 0; c < kMaxStreamChunks; ++c) {
       ANKH_CUDA(cudaEventCreateWithFlags(&ev_s_chunk_[c], cudaEventDisableTiming));
@@ -1136,9 +1138,10 @@ void Plan::stream_setup() {
 
 // positions half of the streamed path: validation, binning, per-leaf sort
 // (build_tree, as set_positions) and the per-chunk leaf lists; their bounds
-// land in h_sbounds_ (pinned) once `ev_s_sorted_` completes
+// stay on the device (the chunk kernels read them there); `after_inverse` is
+// recorded once the inverse permutation -- all the chunk gathers need -- is in
 void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C,
-                            const std::function<void(const std::string&)>& mark) {
+                            const std::function<void(const std::string&)>& mark, cudaEvent_t after_inverse) {
   launch_init_result(res, st, 0, d_counts_, static_cast<unsigned>(n_leaves + 1));
   const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
   launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, res, st);
@@ -1147,7 +1150,8 @@ void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, 
                        d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
   if (mark) mark("  leaf CSR");
   launch_stream_prepare(d_off_, d_idx2_, n, depth, periodic ? 1 : 0, static_cast<unsigned>(chunk), C, d_inv_,
-                        d_ready_, d_scnt_, d_sbounds_, d_scursor_, d_list_p2m_, d_list_p2p_, st, h_sbounds_dev_);
+                        d_ready_, d_scnt_, d_sbounds_, d_scursor_, d_list_p2m_, d_list_p2p_, st, nullptr,
+                        after_inverse);
 }
 
 std::size_t Plan::stream_chunk_size() const {
@@ -1196,61 +1200,58 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   }
   if (!bound_pos) {
     ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_pos_, 0));
-    stream_positions(st, d_res_, chunk, C, trace ? std::function<void(const std::string&)>(
-                                                      [&](const std::string& w) { mark(w, st); })
-                                                : std::function<void(const std::string&)>());
+    stream_positions(st, d_res_, chunk, C,
+                     trace ? std::function<void(const std::string&)>([&](const std::string& w) { mark(w, st); })
+                           : std::function<void(const std::string&)>(),
+                     ev_s_inv_);
   } else {
     ANKH_CUDA(cudaMemcpyAsync(d_res_, d_res_pos_, sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
+    ANKH_CUDA(cudaEventRecord(ev_s_inv_, st));
   }
-  // per-leaf multipole flags: OR-ed by the chunk gathers below
-  ANKH_CUDA(cudaMemsetAsync(d_leaf_mp_, 0, static_cast<std::size_t>(n_leaves) * sizeof(unsigned), st));
   ANKH_CUDA(cudaEventRecord(ev_s_sorted_, st));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[1], st));
   mark("sorted + lists", st);
   ANKH_CUDA(cudaGetLastError());
-  if (!bound_pos) ANKH_CUDA(cudaEventSynchronize(ev_s_sorted_));  // per-chunk leaf counts -> exact grids
+  // No host wait: the chunk kernels read their leaf-list bounds on the device,
+  // with grids sized by upper bounds (warps / CTAs stride over the list).
+  // Records (gather stream) start once the inverse permutation is in; P2M
+  // (far stream) and P2P wait for the lists; P2P chunks alternate between two
+  // streams so one chunk's tail overlaps the next chunk's start.
   std::uint32_t launches = 9;
-  // per chunk: records (gather stream), P2M (far stream), P2P (this stream)
-  ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_sorted_, 0));
+  ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_inv_, 0));
+  // per-leaf multipole flags: OR-ed by the chunk gathers below
+  ANKH_CUDA(cudaMemsetAsync(d_leaf_mp_, 0, static_cast<std::size_t>(n_leaves) * sizeof(unsigned), gather_stream_));
   ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_sorted_, 0));
+  ANKH_CUDA(cudaStreamWaitEvent(p2p_stream2_, ev_s_sorted_, 0));
+  const unsigned p2m_cap = static_cast<unsigned>(std::min<long long>(n_leaves, 32ll * sm_count_));
+  const int p2p_grid = static_cast<int>(std::min<long long>(n_leaves, 6ll * sm_count_));
   const bool do_periodic = periodic && include_self_;
   int n_near_parts = leaf_end_ - leaf_begin_;
-  bool near_started = false;
   for (int c = 0; c < C; ++c) {
     const std::size_t i0 = c * chunk, i1 = std::min(n, i0 + chunk);
     ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_chunk_[c], 0));
     launch_src_chunk(d_pos_, d_src_, d_inv_, i0, i1, d_res_, d_part_, gather_stream_, d_keys_, d_leaf_mp_);
     ANKH_CUDA(cudaEventRecord(ev_s_gath_[c], gather_stream_));
     mark("gather " + std::to_string(c), gather_stream_);
-    const unsigned n_m = h_sbounds_[c + 1] - h_sbounds_[c];
-    const unsigned n_p = h_sbounds_[C + 1 + c + 1] - h_sbounds_[C + 1 + c];
-    if (n_m) {
-      ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[c], 0));
-      launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, d_self_leaf_, cfg.xi, 0u,
-                 0u, side_stream_,
-                 d_list_p2m_, d_sbounds_ + c, n_m);
-      ++launches;
-      mark("p2m " + std::to_string(c) + " (" + std::to_string(n_m) + " leaves)", side_stream_);
-    }
-    if (n_p) {
-      ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[c], 0));
-      if (timing && !near_started) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
-      near_started = true;
-      n_near_parts = launch_p2p(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, p2p_cap_,
-                                leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, st, d_list_p2p_,
-                                d_sbounds_ + (C + 1) + c, static_cast<int>(n_p));
-      ++launches;
-      mark("p2p " + std::to_string(c) + " (" + std::to_string(n_p) + " leaves)", st);
-    }
-    launches += 1;
+    ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[c], 0));
+    launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, d_self_leaf_, cfg.xi, 0u,
+               0u, side_stream_, d_list_p2m_, d_sbounds_ + c, p2m_cap);
+    mark("p2m " + std::to_string(c), side_stream_);
+    cudaStream_t ps = (c & 1) ? p2p_stream2_ : st;
+    ANKH_CUDA(cudaStreamWaitEvent(ps, ev_s_gath_[c], 0));
+    if (timing && c == 0) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
+    n_near_parts = launch_p2p(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
+                              p2p_cap_, leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, ps,
+                              d_list_p2p_, d_sbounds_ + (C + 1) + c, p2p_grid);
+    mark("p2p " + std::to_string(c), ps);
+    launches += 3;
   }
   // the last chunk's records are in before the tail (far stream waits below)
   ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[C - 1], 0));
+  ANKH_CUDA(cudaEventRecord(ev_s_p2p2_, p2p_stream2_));
+  ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_p2p2_, 0));
   ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[C - 1], 0));
-  if (timing) {
-    if (!near_started) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
-    ANKH_CUDA(cudaEventRecord(ev_t_[3], st));
-  }
+  if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[3], st));
   if (timing) {  // phase spans: M2M, M2L, periodic back to back
     for (int l = depth - 1; l >= 0; --l) {
       launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, side_stream_);

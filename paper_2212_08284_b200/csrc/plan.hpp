@@ -166,18 +166,21 @@ class Plan {
   void stream_setup();
   std::size_t stream_chunk_size() const;
   void stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C,
-                        const std::function<void(const std::string&)>& mark = {});
+                        const std::function<void(const std::string&)>& mark = {},
+                        cudaEvent_t after_inverse = nullptr);
   void enqueue_streamed(const double* h_pos, const double* h_src, cudaStream_t st);
   bool stream_bound_ = false;  // set_positions built the streamed path's lists
   static constexpr int kMaxStreamChunks = ankh_b200::kMaxStreamChunks;
   int stream_chunks_ = 8;
   bool stream_init_ = false;
   unsigned *d_inv_ = nullptr, *d_scnt_ = nullptr, *d_sbounds_ = nullptr, *d_scursor_ = nullptr;
-  unsigned *d_list_p2m_ = nullptr, *d_list_p2p_ = nullptr, *h_sbounds_ = nullptr;
-  unsigned* h_sbounds_dev_ = nullptr;  // its device alias (k_stream_scan writes it)
+  unsigned *d_list_p2m_ = nullptr, *d_list_p2p_ = nullptr;
+  int sm_count_ = 148;
+  cudaStream_t p2p_stream2_ = nullptr;  // odd chunks' P2P (tails overlap the next chunk's start)
   unsigned char* d_ready_ = nullptr;
   cudaStream_t copy_stream_ = nullptr, gather_stream_ = nullptr;
-  cudaEvent_t ev_s_start_ = nullptr, ev_s_pos_ = nullptr, ev_s_sorted_ = nullptr;
+  cudaEvent_t ev_s_start_ = nullptr, ev_s_pos_ = nullptr, ev_s_sorted_ = nullptr, ev_s_inv_ = nullptr,
+              ev_s_p2p2_ = nullptr;
   cudaEvent_t ev_s_chunk_[kMaxStreamChunks] = {}, ev_s_gath_[kMaxStreamChunks] = {};
   // phase spans of a streamed evaluation (phases overlap: start/end per phase)
   cudaEvent_t ev_t_[9] = {};

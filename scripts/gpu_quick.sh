@@ -9,3 +9,4 @@ print("value", d["value"], "ms", d["ms_per_step"], "e2e", d["e2e"]["value"], "fi
 print({k:(round(v["ms"],4), round(v.get("frac") or 0,3)) for k,v in d["phase_rooflines"].items()})
 print("clocks", d["clocks"])
 PY
+ANKH_STREAM_TRACE=1 timeout 300 python scripts/stream_trace.py > $D/stream_trace.txt 2>&1; grep -E "untraced|copy positions|sorted|chunk 7|far chain|finalize" $D/stream_trace.txt
