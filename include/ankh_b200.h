@@ -97,6 +97,19 @@ int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
                        double box_radius, const ankh_config_v1* cfg, ankh_report_v1* out,
                        char* err, size_t errlen);
 
+/* Forces (the reference computes energies only):
+ * forces[3 i + d] = -dE/dx_{i,d} of the same energy ankh_fmm_energy_v1
+ * returns (moments held fixed in the lab frame) -- near field by the
+ * gradient of pair_interaction over every leaf's 27-leaf stencil, far field
+ * by the adjoint (dE/dM per cell from the M2L factors, the periodic root
+ * operator, L2L = M2M^T, L2P = differentiated P2M).  The report holds the
+ * energies.  One GPU (a sharded plan raises ANKH_RUNTIME_ERROR). */
+int ankh_fmm_forces_v1(size_t n, const double* positions, const double* sources, double box_radius,
+                       const ankh_config_v1* cfg, double* forces, ankh_report_v1* out, char* err,
+                       size_t errlen);
+int ankh_plan_forces_v1(ankh_plan_v1* plan, const double* positions, const double* sources, double* forces,
+                        ankh_report_v1* out, char* err, size_t errlen);
+
 /* The call-level checks of fmm_energy in the reference's order, for wrappers
  * whose containers carry separate position / source lengths:
  * validate_config (fmm.cpp:384, types.cpp:65-79), then validate_system's

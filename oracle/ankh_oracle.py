@@ -174,6 +174,60 @@ def pair_interaction(xa, sa, xb, sb, xi):
     return e
 
 
+def pair_gradient(xa, sa, xb, sb, xi):
+    """Gradient of pair_interaction (kernel.cpp:157-204) with respect to
+    r = xa - xb, moments held fixed: the near-field force on a is -grad.
+    NOT a reference function (the reference computes energies only; forces
+    are SURVEY.md §8f-3): the exact derivative of the same polynomial,
+    e = sum_n C_n(r) b_n(r) with grad b_n = -r b_{n+1} (radial recurrence,
+    kernel.cpp:26-38), checked against central differences of
+    pair_interaction (tests/test_oracle.py)."""
+    xa = np.atleast_2d(xa)
+    xb = np.atleast_2d(xb)
+    sa = np.atleast_2d(sa)
+    sb = np.atleast_2d(sb)
+    rv = xa - xb
+    r2 = (rv * rv).sum(axis=1)
+    if (r2 == 0.0).any():
+        raise DomainError("pair_interaction: coincident points")
+    r = np.sqrt(r2)
+    b = radial(r, xi, 5)
+    qa, qb = sa[:, 0], sb[:, 0]
+    mua, mub = sa[:, 1:4], sb[:, 1:4]
+    ta, tb = sa[:, 4:10], sb[:, 4:10]
+    uar = (mua * rv).sum(axis=1)
+    ubr = (mub * rv).sum(axis=1)
+    tra = ta[:, 0] + ta[:, 3] + ta[:, 5]
+    trb = tb[:, 0] + tb[:, 3] + tb[:, 5]
+    Qar = _symmul(ta, rv)
+    Qbr = _symmul(tb, rv)
+    raQar = (Qar * rv).sum(axis=1)
+    rbQbr = (Qbr * rv).sum(axis=1)
+    dot = lambda u, v: (u * v).sum(axis=1)
+    col = lambda s: s[:, None]
+    # e = C0 b0 + C1 b1 + ... + C4 b4 (the reference's terms, F_n = (-1)^n b_n)
+    C = [qa * qb,
+         -(qb * uar - qa * ubr) - (qb * tra + qa * trb) + dot(mua, mub),
+         (-uar * ubr + qb * raQar + qa * rbQbr + 2.0 * dot(mua, Qbr) + uar * trb
+          - 2.0 * dot(mub, Qar) - ubr * tra + tra * trb + 2.0 * _contract(ta, tb)),
+         -uar * rbQbr + ubr * raQar - (tra * rbQbr + trb * raQar + 4.0 * dot(Qar, Qbr)),
+         raQar * rbQbr]
+    taub = _symmul(ta, mub)
+    tbua = _symmul(tb, mua)
+    gC = [None,
+          -(col(qb) * mua - col(qa) * mub),
+          (-(col(ubr) * mua + col(uar) * mub) + 2.0 * col(qb) * Qar + 2.0 * col(qa) * Qbr
+           + 2.0 * tbua + col(trb) * mua - 2.0 * taub - col(tra) * mub),
+          (-(col(rbQbr) * mua + 2.0 * col(uar) * Qbr) + (col(raQar) * mub + 2.0 * col(ubr) * Qar)
+           - (2.0 * col(tra) * Qbr + 2.0 * col(trb) * Qar
+              + 4.0 * (_symmul(ta, Qbr) + _symmul(tb, Qar)))),
+         2.0 * col(rbQbr) * Qar + 2.0 * col(raQar) * Qbr]
+    g = -rv * col(sum(C[n] * b[n + 1] for n in range(5)))
+    for n in range(1, 5):
+        g = g + gC[n] * col(b[n])
+    return g
+
+
 def self_energy(src: np.ndarray, xi: float) -> float:
     """kernel.cpp:206-213."""
     if src.shape[0] == 0:

@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     device_copy,
     exchange_leaf_levels,
     fmm_energy,
+    fmm_forces,
     nccl_unique_id,
 )
 from ._lib import LIB_PATH, build, lib  # noqa: F401

@@ -36,6 +36,7 @@ __all__ = [
     "AnkhRuntimeError",
     "CudaError",
     "fmm_energy",
+    "fmm_forces",
     "default_depth",
     "build_tree_csr",
     "Plan",
@@ -220,6 +221,25 @@ def fmm_energy(system: ParticleSystem, config: Optional[EwaldConfig] = None,
     return EnergyReport._from_c(rep)
 
 
+def fmm_forces(system: ParticleSystem, config: Optional[EwaldConfig] = None,
+               threads: int = 1):
+    """Energy and forces F = -dE/dx (n x 3 array, the input's particle order),
+    moments held fixed in the lab frame (the reference
+    computes energies only).  Returns (EnergyReport, forces)."""
+    config = config or EwaldConfig()
+    pos = _as_host(system.positions, 3)
+    src = _as_host(system.sources, 10)
+    rep = _Report()
+    err = ctypes.create_string_buffer(512)
+    c = config._c(threads=threads)
+    _check(lib().ankh_check_call_v1(ctypes.byref(c), float(system.box_radius), pos.shape[0],
+                                    src.shape[0], err, 512), err)
+    forces = np.zeros((pos.shape[0], 3), dtype=np.float64)
+    _check(lib().ankh_fmm_forces_v1(pos.shape[0], _ptr(pos), _ptr(src), float(system.box_radius),
+                                    ctypes.byref(c), _ptr(forces), ctypes.byref(rep), err, 512), err)
+    return EnergyReport._from_c(rep), forces
+
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id (rank 0 creates it; broadcast to the other shards)."""
     buf = ctypes.create_string_buffer(128)
@@ -320,6 +340,18 @@ class Plan:
         err = ctypes.create_string_buffer(512)
         _check(lib().ankh_plan_energy_v1(self._h, _ptr(pos), _ptr(src), ctypes.byref(rep), err, 512), err)
         return EnergyReport._from_c(rep)
+
+    def forces(self, positions, sources):
+        """Energy and forces F = -dE/dx (n x 3) of host arrays: (EnergyReport, forces)."""
+        pos = _as_host(positions, 3)
+        src = _as_host(sources, 10)
+        self._check_n(pos, src)
+        rep = _Report()
+        err = ctypes.create_string_buffer(512)
+        forces = np.zeros((pos.shape[0], 3), dtype=np.float64)
+        _check(lib().ankh_plan_forces_v1(self._h, _ptr(pos), _ptr(src), _ptr(forces), ctypes.byref(rep), err,
+                                         512), err)
+        return EnergyReport._from_c(rep), forces
 
     def set_positions(self, positions) -> None:
         """Bind host positions (copied, validated, binned and sorted once) for

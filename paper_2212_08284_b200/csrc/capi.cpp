@@ -146,6 +146,51 @@ int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
   });
 }
 
+int ankh_fmm_forces_v1(size_t n, const double* positions, const double* sources, double box_radius,
+                       const ankh_config_v1* cfg, double* forces, ankh_report_v1* out, char* err,
+                       size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!cfg || !out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null config or report");
+    if (n > 0 && (!positions || !sources || !forces)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+    ankh_b200::validate_config(*cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    const int dev = resolve_device(*cfg);
+    std::shared_ptr<ankh_plan_v1> h;
+    {
+      std::lock_guard<std::mutex> lock(g_cache_mu);
+      for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+        if (it->n == n && it->rb == box_radius && it->device == dev && same_cfg(it->cfg, *cfg)) {
+          g_cache.splice(g_cache.begin(), g_cache, it);
+          h = g_cache.front().h;
+          break;
+        }
+      }
+    }
+    if (!h) {
+      ankh_config_v1 c = *cfg;
+      c.device = dev;
+      h = std::make_shared<ankh_plan_v1>();
+      h->plan = std::make_unique<Plan>(n, box_radius, c);
+      std::lock_guard<std::mutex> lock(g_cache_mu);
+      while (g_cache.size() >= kCacheMax) g_cache.pop_back();
+      g_cache.push_front({n, box_radius, *cfg, dev, h});
+    }
+    on_plan(h.get(), [&](Plan& plan) { plan.forces(positions, sources, forces, out); });
+    out->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int ankh_plan_forces_v1(ankh_plan_v1* plan, const double* positions, const double* sources, double* forces,
+                        ankh_report_v1* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null report");
+    on_plan(plan, [&](Plan& p) {
+      if (p.n > 0 && (!positions || !sources || !forces)) throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+      p.forces(positions, sources, forces, out);
+    });
+  });
+}
+
 int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg, ankh_plan_v1** plan,
                         char* err, size_t errlen) {
   return guarded(err, errlen, [&] {

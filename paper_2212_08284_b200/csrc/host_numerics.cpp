@@ -204,6 +204,18 @@ std::array<std::vector<double>, 3> diff_operator(int order) {
   return hd;
 }
 
+std::vector<double> diff_operator_hd3(int order) {
+  const int L = order;
+  const auto hd = diff_operator(L);
+  std::vector<double> d(L * L, 0.0), out(L * L, 0.0);
+  for (int m = 1; m < L; ++m)
+    for (int j = m - 1; j >= 0; j -= 2) d[m * L + j] = (j == 0) ? m : 2.0 * m;
+  for (int i = 0; i < L; ++i)
+    for (int k = 0; k < L; ++k)
+      for (int j = 0; j < L; ++j) out[i * L + j] += hd[2][i * L + k] * d[k * L + j];
+  return out;
+}
+
 std::vector<double> transfer_cheb(int order, const std::vector<double>& src) {
   const int n = static_cast<int>(src.size());
   std::vector<double> t(order * n);

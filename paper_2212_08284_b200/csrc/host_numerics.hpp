@@ -43,6 +43,8 @@ double lagrange_equi(int order, int k, double x);
 
 /// DiffOperator (chebyshev.cpp:85-108): hd[n] = H D^n, n = 0..2, row-major L x L.
 std::array<std::vector<double>, 3> diff_operator(int order);
+/// H D^3 (L x L, row-major): the next basis derivative, for the forces' L2P.
+std::vector<double> diff_operator_hd3(int order);
 
 /// transfer_1d (chebyshev.cpp:236-244): T(k, l) = S_k^{dst}(src[l]), row-major.
 std::vector<double> transfer_cheb(int order, const std::vector<double>& src_local);

@@ -216,6 +216,28 @@ void launch_m2l_pack(const M2LPack* ops, int n_ops, int max_rows, const int* per
 /// the reverse; Kp even, row offsets 16-B aligned.
 void launch_halo_rows(double* exp, const long long* row_off, long long n_rows, int Kp, double* buf,
                       bool unpack, cudaStream_t st);
+// Forces (k_forces.cu): near-field gradient over the full
+// 27-leaf stencil (f_near, sorted record order, F = -grad); per-cell dE/dM
+// (loc, the expansion layout) from M2L instances -- tiles (level, parity
+// class, first class index, count <= 32), op_of[level * 343 + offset slot] =
+// (first operator block, blocks) -- the periodic root term, L2L, L2P (f_far);
+// then forces[sorted[j]] = f_near[j] + f_far[j].
+int force_max_cap();
+void launch_force_near(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth,
+                       int periodic, double period, double xi, const P2PRadial& rad, int cap, double* f_near,
+                       cudaStream_t st);
+std::size_t m2l_local_smem(int Kp);
+void launch_m2l_local(const double* exp, double* loc, const long long* level_off, const double* factors,
+                      const M2LOp* ops, const int2* op_of, const int4* tiles, int n_tiles, int Kp, int periodic,
+                      cudaStream_t st);
+void launch_periodic_local(const double* root, const double* to_equi, const double* gen, int order,
+                           double* loc_root, cudaStream_t st);
+void launch_l2l(const double* loc_parent, double* loc_child, int parent_level, int order, const double* m2m,
+                cudaStream_t st);
+void launch_l2p(const double* part, const unsigned* leaf_off, int depth, int order, double rb, const double* hd4,
+                const double* loc_leaf, double* f_far, cudaStream_t st);
+void launch_force_out(const double* f_near, const double* f_far, const unsigned* sorted, std::size_t n,
+                      double* out, cudaStream_t st);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);
 

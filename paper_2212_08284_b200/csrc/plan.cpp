@@ -698,6 +698,7 @@ void Plan::build_periodic() {
   const int eb = 2 * L - 1;
   const std::size_t m = static_cast<std::size_t>(eb) * eb * eb;
   double* d_gen = static_cast<double*>(dalloc(m * sizeof(double)));
+  d_gen_ = d_gen;  // kept: the forces' periodic term applies the operator directly
   launch_periodic_gen(d_gen, L, rb, cfg.xi, cfg.p, stream_);
   ANKH_CUDA(cudaGetLastError());
   std::vector<double> gen(m);
@@ -1467,6 +1468,81 @@ void Plan::result(ankh_report_v1* out) {
     out->t_total += precompute_seconds;  // the plan build is part of the first call
     precompute_reported = true;
   }
+}
+
+// Force buffers and tables (first forces() call): per-cell dE/dM in the
+// expansion layout, near / far / output force arrays, H D^n for n = 0..3,
+// the (level, offset) -> operator table and the dE/dM tiles (level, parity
+// class, first class index, count <= 32) of k_m2l_local.
+void Plan::force_setup() {
+  if (force_init_) return;
+  const std::size_t nn = std::max<std::size_t>(n, 1);
+  d_loc_ = static_cast<double*>(dalloc(level_off_[depth + 1] * sizeof(double)));
+  d_fnear_ = static_cast<double*>(dalloc(nn * 3 * sizeof(double)));
+  d_ffar_ = static_cast<double*>(dalloc(nn * 3 * sizeof(double)));
+  d_fout_ = static_cast<double*>(dalloc(nn * 3 * sizeof(double)));
+  const auto hd = diff_operator(L);
+  std::vector<double> hd4;
+  for (const auto& m : hd) hd4.insert(hd4.end(), m.begin(), m.end());
+  const std::vector<double> d3 = diff_operator_hd3(L);
+  hd4.insert(hd4.end(), d3.begin(), d3.end());
+  d_hd4_ = static_cast<double*>(dalloc(hd4.size() * sizeof(double)));
+  ANKH_CUDA(cudaMemcpyAsync(d_hd4_, hd4.data(), hd4.size() * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  std::vector<int2> op_of(static_cast<std::size_t>(depth + 1) * 343, make_int2(-1, 0));
+  for (int level = 1; level <= depth; ++level)
+    for (int ox = -3; ox <= 3; ++ox)
+      for (int oy = -3; oy <= 3; ++oy)
+        for (int oz = -3; oz <= 3; ++oz) {
+          auto it = op_info_.find({level, offset_key({ox, oy, oz})});
+          if (it == op_info_.end()) continue;
+          op_of[level * 343 + ((ox + 3) * 7 + (oy + 3)) * 7 + (oz + 3)] =
+              make_int2(it->second.first_op, it->second.n_blocks);
+        }
+  d_op_of_ = static_cast<int2*>(dalloc(op_of.size() * sizeof(int2)));
+  ANKH_CUDA(cudaMemcpyAsync(d_op_of_, op_of.data(), op_of.size() * sizeof(int2), cudaMemcpyHostToDevice, stream_));
+  std::vector<int4> tiles;
+  for (int level = 1; level <= depth; ++level) {
+    const int per_class = 1 << (3 * (level - 1));
+    for (int cls = 0; cls < 8; ++cls)
+      for (int j0 = 0; j0 < per_class; j0 += 32) tiles.push_back(make_int4(level, cls, j0, std::min(32, per_class - j0)));
+  }
+  n_loc_tiles_ = static_cast<int>(tiles.size());
+  d_loc_tiles_ = static_cast<int4*>(dalloc(std::max<std::size_t>(tiles.size(), 1) * sizeof(int4)));
+  if (!tiles.empty())
+    ANKH_CUDA(cudaMemcpyAsync(d_loc_tiles_, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                              stream_));
+  const double per_leaf = static_cast<double>(n) / n_leaves;
+  force_cap_ = static_cast<int>(std::ceil(27.0 * per_leaf * 1.3 / 32.0)) * 32;
+  force_cap_ = std::max(256, std::min(force_cap_, force_max_cap()));
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+  force_init_ = true;
+}
+
+void Plan::forces(const double* h_pos, const double* h_src, double* h_forces, ankh_report_v1* out) {
+  if (cfg.world > 1) throw AnkhError(ANKH_RUNTIME_ERROR, "forces: sharded plans (world > 1) are not supported");
+  if (n == 0 || pending_code_ != 0 || csr_only_) {
+    enqueue_host(h_pos, h_src, nullptr);
+    result(out);  // raises the deferred error, if any
+    return;
+  }
+  ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  enqueue(d_pos_, d_src_, stream_);  // energies, records, leaf CSR, expansions of every level
+  force_setup();
+  cudaStream_t st = stream_;
+  ANKH_CUDA(cudaMemsetAsync(d_loc_, 0, level_off_[depth + 1] * sizeof(double), st));
+  launch_force_near(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, force_cap_,
+                    d_fnear_, st);
+  launch_m2l_local(d_exp_, d_loc_, d_level_off_, d_factors_, d_ops_, d_op_of_, d_loc_tiles_, n_loc_tiles_, Kp,
+                   periodic ? 1 : 0, st);
+  if (periodic) launch_periodic_local(d_exp_, d_to_equi_, d_gen_, L, d_loc_, st);
+  for (int l = 0; l < depth; ++l) launch_l2l(d_loc_ + level_off_[l], d_loc_ + level_off_[l + 1], l, L, d_m2m_, st);
+  launch_l2p(d_part_, d_off_, depth, L, rb, d_hd4_, d_loc_ + level_off_[depth], d_ffar_, st);
+  launch_force_out(d_fnear_, d_ffar_, d_idx2_, n, d_fout_, st);
+  ANKH_CUDA(cudaGetLastError());
+  ANKH_CUDA(cudaMemcpyAsync(h_forces, d_fout_, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  last_stream_ = st;
+  result(out);
 }
 
 void Plan::expansions(double* out, std::size_t count) {

@@ -106,6 +106,9 @@ class Plan {
   void enqueue_sources(const double* h_src, cudaStream_t st);
   /// Wait for the last evaluation and fill the report (throws on validation errors).
   void result(ankh_report_v1* out);
+  /// Energy evaluation plus the forces F = -dE/dx (n x 3, the caller's particle
+  /// order) into host memory (one GPU).
+  void forces(const double* h_pos, const double* h_src, double* h_forces, ankh_report_v1* out);
 
   void expansions(double* out, std::size_t count);
   void m2l_factors(int level, const int* offset, double* lmat, double* rmat, int max_rank,
@@ -280,6 +283,14 @@ class Plan {
   P2PRadial radial_{};  // near-field radial polynomials (fit_radial)
   int p2p_cap_ = 512;
   std::uint32_t launches_ = 0;
+  // forces (allocated on the first forces() call)
+  void force_setup();
+  bool force_init_ = false;
+  double *d_loc_ = nullptr, *d_fnear_ = nullptr, *d_ffar_ = nullptr, *d_fout_ = nullptr, *d_hd4_ = nullptr;
+  double* d_gen_ = nullptr;  // periodic generator (build_periodic)
+  int2* d_op_of_ = nullptr;
+  int4* d_loc_tiles_ = nullptr;
+  int n_loc_tiles_ = 0, force_cap_ = 960;
   // timing
   cudaEvent_t ev_[8] = {};
   bool evaluated_ = false;

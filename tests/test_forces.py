@@ -1,0 +1,115 @@
+"""Forces: F = -dE/dx of the FMM energy, moments fixed.
+
+The reference computes energies only, so the checker is the reference's own
+energy: central differences of ankh::fmm_energy (oracle/_ref) at a few
+particles, on small systems covering periodic / open boundaries, charges only
+and full multipoles, orders 3..6 (L = 6 takes the reference's randomized SVD
+path).  Displaced particles stay inside their leaves (the FMM energy is smooth
+there).  At full size: central differences of the engine's own energy, the
+near-field share against the numpy pair gradient, bitwise determinism.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2212_08284_b200 as ankh
+from paper_2212_08284_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _inside_leaf(pos, rb, depth, margin):
+    """Particles at least `margin` away from every leaf face (and the box)."""
+    n = 1 << depth
+    side = 2.0 * rb / n
+    u = (pos + rb) / side
+    frac = u - np.floor(u)
+    return np.where(((frac * side > margin) & ((1 - frac) * side > margin)).all(axis=1))[0]
+
+
+def _fd_reference(ref, pos, src, rb, kw, idx, h):
+    out = np.zeros((len(idx), 3))
+    for a, i in enumerate(idx):
+        for d in range(3):
+            p1, p2 = pos.copy(), pos.copy()
+            p1[i, d] += h
+            p2[i, d] -= h
+            e1 = ref.fmm_energy(p1, src, rb, threads=os.cpu_count(), **kw)["e_total"]
+            e2 = ref.fmm_energy(p2, src, rb, threads=os.cpu_count(), **kw)["e_total"]
+            out[a, d] = -(e1 - e2) / (2 * h)
+    return out
+
+
+CASES = {
+    "mp_L4_E2_periodic": (300, 5.0, 1, True, dict(order_cheb=4, order_equi=4, depth=2, p=15)),
+    "mp_L3_E2_open": (300, 5.0, 2, True, dict(order_cheb=3, order_equi=3, depth=2, p=0)),
+    "q_L5_E1_p2": (500, 7.0, 3, False, dict(order_cheb=5, order_equi=5, depth=1, p=2)),
+    "mp_L5_E3_periodic": (1500, 8.0, 4, True, dict(order_cheb=5, order_equi=5, depth=3, p=15)),
+    "mp_L6_E2_periodic": (400, 5.0, 5, True, dict(order_cheb=6, order_equi=6, depth=2, p=15)),
+    "mp_L4_E2_xi0.3": (400, 5.0, 6, True, dict(order_cheb=4, order_equi=4, depth=2, p=15, xi=0.3)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_forces_match_reference_energy_differences(cuda, ref, name):
+    n, rb, seed, mp, kw = CASES[name]
+    pos, src = inputs.random_system(n, rb, seed=seed, multipoles=mp)
+    rep, f = ankh.fmm_forces(ankh.ParticleSystem(pos, src, rb), ankh.EwaldConfig(**kw))
+    want = ref.fmm_energy(pos, src, rb, threads=os.cpu_count(), **kw)
+    assert abs(rep.e_total - want["e_total"]) <= 1e-10 * abs(want["e_total"]) + 1e-12
+    assert f.shape == (n, 3) and np.isfinite(f).all()
+    h = 1e-5
+    cand = _inside_leaf(pos, rb, kw["depth"], 50 * h)
+    idx = cand[np.linspace(0, len(cand) - 1, 5).astype(int)]
+    fd = _fd_reference(ref, pos, src, rb, kw, idx, h)
+    scale = np.abs(fd).max()
+    err = np.abs(f[idx] - fd).max()
+    # central differences of the reference: truncation h^2 and its round-off
+    # (~1e-15 |E| / h) bound the agreement
+    tol = 2e-6 * scale + 1e-9 * abs(want["e_total"]) / h * 1e-3
+    assert err <= tol, (name, err, scale, f[idx], fd)
+
+
+def test_forces_near_field_matches_pair_gradient(cuda):
+    """Open boundary, one leaf level (depth 1) with the far field switched off
+    by construction (no M2L at level 1 without periodicity): the forces are
+    the near field alone -- the numpy pair gradient summed over all pairs."""
+    import ankh_oracle as O
+
+    pos, src = inputs.random_system(120, 3.0, seed=7, multipoles=True)
+    kw = dict(order_cheb=3, order_equi=3, depth=1, p=0)
+    rep, f = ankh.fmm_forces(ankh.ParticleSystem(pos, src, 3.0), ankh.EwaldConfig(**kw))
+    n = pos.shape[0]
+    want = np.zeros((n, 3))
+    for i in range(n):
+        others = np.array([j for j in range(n) if j != i])
+        g = O.pair_gradient(np.repeat(pos[i:i + 1], n - 1, 0), np.repeat(src[i:i + 1], n - 1, 0),
+                            pos[others], src[others], 0.01)
+        want[i] = -g.sum(axis=0)
+    assert np.abs(f - want).max() <= 1e-11 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("config", [1, 3])
+def test_forces_at_scale_match_own_energy_differences(cuda, config):
+    """BASELINE configs 1 and 3: forces against central differences of the
+    engine's own energy at a few particles, and bitwise run-to-run equality."""
+    pos, src, rb, cfg = inputs.make_config(config)
+    L = cfg.orders[0]
+    ec = ankh.EwaldConfig(order_cheb=L, order_equi=L)
+    plan = ankh.Plan(pos.shape[0], rb, ec)
+    rep, f = plan.forces(pos, src)
+    rep2, f2 = plan.forces(pos, src)
+    assert np.array_equal(f, f2) and rep.e_total == rep2.e_total
+    depth = plan.info()["depth"]
+    h = 1e-4
+    cand = _inside_leaf(pos, rb, depth, 50 * h)
+    idx = cand[np.linspace(0, len(cand) - 1, 4).astype(int)]
+    for i in idx:
+        for d in range(3):
+            p1, p2 = pos.copy(), pos.copy()
+            p1[i, d] += h
+            p2[i, d] -= h
+            fd = -(plan.energy(p1, src).e_total - plan.energy(p2, src).e_total) / (2 * h)
+            assert abs(f[i, d] - fd) <= 1e-5 * np.abs(f[idx]).max() + 2e-13 * abs(rep.e_total) / h, (i, d, f[i, d], fd)
+    plan.close()

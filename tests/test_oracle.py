@@ -47,6 +47,27 @@ def test_pair_interaction_matches_finite_difference():
     assert rel(e, fd) < 1e-6
 
 
+@pytest.mark.parametrize("xi,seed", [(0.01, 1), (0.3, 2), (0.6, 3)])
+def test_pair_gradient_matches_reference_finite_differences(ref, xi, seed):
+    """The forces' pair gradient (oracle pair_gradient, the restatement the
+    GPU's pair_grad_mp follows) against central differences of the
+    reference's own pair_interaction (kernel.cpp:157-204), for full q/mu/Theta
+    pairs and the charge-only / dipole-only special cases."""
+    rng = np.random.default_rng(seed)
+    for kind in ("full", "q", "mu"):
+        xa, xb = rng.normal(size=3) * 2.0, rng.normal(size=3) * 2.0
+        sa, sb = rng.normal(size=10), rng.normal(size=10)
+        if kind == "q":
+            sa[1:] = sb[1:] = 0.0
+        if kind == "mu":
+            sa[4:] = sb[4:] = 0.0
+        g = O.pair_gradient(xa, sa, xb, sb, xi)[0]
+        h = 1e-5
+        fd = np.array([(ref.pair_interaction(xa + h * e, sa, xb, sb, xi)
+                        - ref.pair_interaction(xa - h * e, sa, xb, sb, xi)) / (2 * h) for e in np.eye(3)])
+        assert np.abs(g - fd).max() <= 1e-8 * np.abs(fd).max(), (kind, g, fd)
+
+
 def test_pair_interaction_symmetry():
     rng = np.random.default_rng(3)
     for _ in range(20):
