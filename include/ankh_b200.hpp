@@ -172,6 +172,21 @@ class Plan {
             err);
     return from_c<Report>(r);
   }
+  /// Energy plus forces F = -dE/dx (moments fixed): `forces`
+  /// receives n x 3 doubles (any 24-byte Vec3-like element type).
+  template <class P, class S, class F>
+  Report forces(const std::vector<P>& positions, const std::vector<S>& sources, std::vector<F>& forces) {
+    static_assert(sizeof(F) == 3 * sizeof(double), "force element layout");
+    check(positions.size(), sources.size());
+    forces.resize(n_);
+    ankh_report_v1 r;
+    char err[512];
+    rethrow(ankh_plan_forces_v1(plan_, reinterpret_cast<const double*>(positions.data()),
+                                reinterpret_cast<const double*>(sources.data()),
+                                reinterpret_cast<double*>(forces.data()), &r, err, sizeof(err)),
+            err);
+    return from_c<Report>(r);
+  }
   /// Bind positions once (copied, validated, binned) ...
   template <class P>
   void set_positions(const std::vector<P>& positions) {

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) k_scatter(const unsigned* __restrict__ ke
                                                  std::size_t n, unsigned* __restrict__ unsorted) {
   const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
   if (i >= n || slots[i] == ~0u) return;  // ~0u: a leaf this shard does not read
+  ANKH_DASSERT(offsets[keys[i]] + slots[i] < offsets[keys[i] + 1]);
   unsorted[offsets[keys[i]] + slots[i]] = static_cast<unsigned>(i);
 }
 
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
   if (need && !need[leaf]) return;  // another shard's leaf
   const unsigned base = offsets[leaf];
   const int c = static_cast<int>(offsets[leaf + 1] - base);
+  ANKH_DASSERT(offsets[leaf + 1] >= base);
   if (c == 0) {
     if (part && leaf_mp && threadIdx.x == 0) leaf_mp[leaf] = 0u;
     return;
@@ -268,6 +270,7 @@ __global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ sr
   const std::size_t i = (static_cast<std::size_t>(block0) + blockIdx.x) * 256 + threadIdx.x;
   bool mp = false;
   if (i < n) {
+    ANKH_DASSERT(!inv || inv[i] < n);
     if (inv) write_record(pos, src, static_cast<unsigned>(i), part + static_cast<std::size_t>(inv[i]) * kRec);
     mp = check_moments(src + 10 * i, i, res);
   }

@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __rest
     double grad[3] = {0.0, 0.0, 0.0};
     for (int c0 = 0; c0 < total; c0 += cap) {
       const int cn = min(cap, total - c0);
+      ANKH_DASSERT(cn > 0 && cn <= cap);
       __syncthreads();
       for (int q = tid; q < cn; q += kForceTPB) {
         const int g = c0 + q;
@@ -264,6 +265,8 @@ __global__ void __launch_bounds__(kLocWarps * 32) k_m2l_local(
             const int sx = pass == 0 ? ox : -ox, sy = pass == 0 ? oy : -oy, sz = pass == 0 ? oz : -oz;
             const int2 opr = op_of[level * 343 + ((sx + 3) * 7 + (sy + 3)) * 7 + (sz + 3)];
             const bool mine = valid && (pass == 0 ? canon : !canon);
+            // every pair the energy counts has its operator (a missing one would drop terms)
+            ANKH_DASSERT(!mine || (opr.x >= 0 && opr.y > 0));
             for (int blk = 0; blk < opr.y; ++blk) {
               const M2LOp op = ops[opr.x + blk];
               const double* Lg = factors + op.factor_off;
@@ -626,7 +629,7 @@ void launch_m2l_local(const double* exp, double* loc, const long long* level_off
   if (n_tiles <= 0) return;
   const std::size_t smem = m2l_local_smem(Kp);
   static std::atomic<unsigned long long> attr{0};
-  smem_opt_in(attr, k_m2l_local, m2l_local_smem(1024));
+  smem_opt_in(attr, k_m2l_local, 227 * 1024);  // the device maximum: plans of any order
   k_m2l_local<<<n_tiles, kLocWarps * 32, smem, st>>>(exp, loc, level_off, factors, ops, op_of, tiles, Kp,
                                                      periodic);
 }
@@ -636,7 +639,7 @@ void launch_periodic_local(const double* root, const double* to_equi, const doub
   const int K = order * order * order;
   const std::size_t smem = sizeof(double) * 3 * K;
   static std::atomic<unsigned long long> attr{0};
-  smem_opt_in(attr, k_periodic_local, sizeof(double) * 3 * 1000);
+  smem_opt_in(attr, k_periodic_local, sizeof(double) * 3 * 1000);  // L <= 10
   k_periodic_local<<<1, kPerLocThreads, smem, st>>>(root, to_equi, gen, order, loc_root);
 }
 

@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(kM2LTile * 4 / NTW) k_m2l(const double* __rest
   const double* E = exp + level_off[tile.level];  // rows of Kp doubles, zero tail
   for (int q = tid; q < kM2LTile; q += kThr) {
     const uint2 ts = q < tile.count ? inst[tile.begin + q] : make_uint2(0u, 0u);
+    ANKH_DASSERT(tile.count <= kM2LTile && ts.x < (1u << (3 * tile.level)) && ts.y < (1u << (3 * tile.level)));
+    ANKH_DASSERT(op.kp == kp);
     s_row[q] = E + static_cast<long long>(ts.x) * Kp;
     s_row[kM2LTile + q] = E + static_cast<long long>(ts.y) * Kp;
   }

@@ -14,9 +14,31 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace ankh_b200 {
+
+/// Device-side bounds checks of the checked build (make checked:
+/// -DANKH_CHECKED, variants/libankh_b200_checked.so).  compute-sanitizer is
+/// not available on the GPU pool, so the checked library is this engine's
+/// own memcheck: every staged shared-memory index and scattered global index
+/// on the hot path is asserted, and plan allocations carry guard zones
+/// verified after each evaluation (plan.cpp).  Compiled out otherwise.
+#ifdef ANKH_CHECKED
+#define ANKH_DASSERT(cond)                                                                  \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("ANKH_DASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                  \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define ANKH_DASSERT(cond) \
+  do {                     \
+  } while (0)
+#endif
 
 /// Dynamic shared-memory opt-in above 48 KB.  CUDA keeps the attribute per
 /// device and per kernel, so a launcher records, per kernel instantiation,

@@ -206,10 +206,31 @@ void* Plan::dalloc(std::size_t bytes) {
   }
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
+#ifdef ANKH_CHECKED
+  // guard zone after every plan buffer, verified after each evaluation
+  ANKH_CUDA(cudaMallocAsync(&p, bytes + kGuardBytes, stream_));
+  ANKH_CUDA(cudaMemsetAsync(static_cast<char*>(p) + bytes, kGuardByte, kGuardBytes, stream_));
+  guards_.emplace_back(p, bytes);
+#else
   ANKH_CUDA(cudaMallocAsync(&p, bytes, stream_));
+#endif
   allocs_.push_back(p);
   device_bytes += bytes;
   return p;
+}
+
+void Plan::check_guards() {
+#ifdef ANKH_CHECKED
+  std::vector<unsigned char> g(kGuardBytes);
+  for (std::size_t k = 0; k < guards_.size(); ++k) {
+    ANKH_CUDA(cudaMemcpy(g.data(), static_cast<char*>(guards_[k].first) + guards_[k].second, kGuardBytes,
+                         cudaMemcpyDeviceToHost));
+    for (unsigned char b : g)
+      if (b != kGuardByte)
+        throw AnkhError(ANKH_CUDA_ERROR, "checked build: guard zone after plan buffer #" + std::to_string(k) +
+                                             " (" + std::to_string(guards_[k].second) + " bytes) was overwritten");
+  }
+#endif
 }
 
 void Plan::build_geometry() {
@@ -1410,6 +1431,7 @@ void Plan::result(ankh_report_v1* out) {
     return;
   }
   ANKH_CUDA(cudaStreamSynchronize(last_stream_));
+  check_guards();
   const DevResult& r = *h_res_;
   // validate_system precedence: first per-particle violation, then duplicates
   if (r.min_nonfinite != ~0ull || r.min_outside != ~0ull) {

@@ -156,6 +156,11 @@ class Plan {
   void build_periodic();
   void allocate();
   void* dalloc(std::size_t bytes);
+  // checked build (-DANKH_CHECKED): guard zones after the plan buffers
+  void check_guards();
+  static constexpr std::size_t kGuardBytes = 256;
+  static constexpr unsigned char kGuardByte = 0xA5;
+  std::vector<std::pair<void*, std::size_t>> guards_;
   /// mode 0: whole evaluation; 1: up to this shard's P2M; 2: from M2M on.
   // mode 0: full evaluation; 1 / 2: halves around a caller-driven shard
   // exchange; 3: moments only (positions bound by set_positions)

@@ -74,6 +74,10 @@ int main(int argc, char** argv) {
     }
     const ankh::EnergyReport b = plan.energy_sources(half);
     std::printf("plan %.17g %.17g\n", a.e_total, b.e_total);
+    // forces into the caller's own Vec3 vector
+    std::vector<ankh::Vec3> f;
+    const ankh::EnergyReport c = plan.forces(sys.positions, sys.sources, f);
+    std::printf("forces %.17g %.17g %.17g %.17g\n", c.e_total, f[0].x, f[0].y, f[n - 1].z);
   }
   try {
     ankh::EwaldConfig bad = cfg;

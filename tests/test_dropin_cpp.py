@@ -54,3 +54,7 @@ def test_dropin_runs_and_matches_python(cuda, tmp_path):
     full, quarter = float(line[1]), float(line[2])
     assert full == r.e_total
     assert abs(quarter - 0.25 * r.e_total) <= 1e-12 * abs(r.e_total)
+    line = [l for l in out.splitlines() if l.startswith("forces ")][0].split()
+    rf, f = ankh.fmm_forces(ankh.ParticleSystem(pos, src, 5.0),
+                            ankh.EwaldConfig(order_cheb=4, order_equi=4, depth=2, p=15))
+    assert [float(v) for v in line[1:]] == [rf.e_total, f[0, 0], f[0, 1], f[-1, 2]]
