@@ -693,6 +693,48 @@ def quadratic_form(gen: np.ndarray, v: np.ndarray, L: int) -> float:
     return float((mult * spec.real * (w.real ** 2 + w.imag ** 2)).sum() / eb ** 3)
 
 
+def periodic_cancellation_bound(pos, src, r_b: float, order: int, xi: float, p: int,
+                                root_cheb: np.ndarray, safety: float = 64.0) -> float:
+    """Round-off bound of e_periodic_far for a given system (test
+    infrastructure, not a reference function).  The root expansion is a sum
+    of per-particle contributions W_a that cancel for a neutral box, so its
+    absolute error is ~u |sum_a |W_a||, not u |M_root|; e_per = 1/2 v^T C v
+    (v = T x T x T M_root, fmm.cpp:421-427) moves by g . dM with
+    g = (T x T x T)^T C v; and the quadratic form itself cancels (C > 0
+    entrywise, v of both signs), so its own rounding is ~u |v|^T C |v|.
+    Bound: safety * u * (||g|| ||sum_a |W_a| || + |v|^T C |v|)."""
+    L = order
+    hd = diff_operator(L)
+    # per-particle root contributions W_a (modified_charges with the root
+    # geometry, one row per particle), summed in absolute value
+    inv = 1.0 / r_b
+    t = cheb_values(L, pos * inv)
+    S = [[(inv ** n) * (t[:, ax, :] @ hd[n].T) for n in range(3)] for ax in range(3)]
+    terms = [(src[:, 0], 0, 0, 0), (src[:, 1], 1, 0, 0), (src[:, 2], 0, 1, 0), (src[:, 3], 0, 0, 1),
+             (src[:, 4], 2, 0, 0), (src[:, 7], 0, 2, 0), (src[:, 9], 0, 0, 2),
+             (2.0 * src[:, 5], 1, 1, 0), (2.0 * src[:, 6], 1, 0, 1), (2.0 * src[:, 8], 0, 1, 1)]
+    A = np.zeros(L ** 3)
+    for lo in range(0, pos.shape[0], 4096):
+        hi = min(pos.shape[0], lo + 4096)
+        w = np.zeros((hi - lo, L, L, L))
+        for coef, nx, ny, nz in terms:
+            w += np.einsum("p,pi,pj,pk->pijk", coef[lo:hi], S[0][nx][lo:hi], S[1][ny][lo:hi], S[2][nz][lo:hi],
+                           optimize=True)
+        A += np.abs(w.reshape(hi - lo, -1)).sum(axis=0)
+    to_equi = transfer_1d(L, cheb_nodes(L), equispaced=True)
+    v = tensor3_apply(to_equi, to_equi, to_equi, root_cheb)
+    eb = 2 * L - 1
+    gen = periodic_generator(r_b, L, xi, p)
+    padded = np.zeros((eb, eb, eb))
+    padded[:L, :L, :L] = v.reshape(L, L, L)
+    cv = np.fft.irfftn(np.fft.rfftn(gen) * np.fft.rfftn(padded), s=(eb, eb, eb))[:L, :L, :L].reshape(-1)
+    g = tensor3_apply(to_equi.T, to_equi.T, to_equi.T, cv)
+    padded[:L, :L, :L] = np.abs(v).reshape(L, L, L)
+    cav = np.fft.irfftn(np.fft.rfftn(gen) * np.fft.rfftn(padded), s=(eb, eb, eb))[:L, :L, :L].reshape(-1)
+    vcv = float(np.abs(v) @ cav)
+    return float(safety * np.finfo(np.float64).eps / 2 * (np.linalg.norm(g) * np.linalg.norm(A) + vcv))
+
+
 def periodic_far_energy(root_cheb: np.ndarray, r_b: float, order: int, xi: float, p: int) -> float:
     """fmm.cpp:421-427: 0.5 * quadratic form of the equispaced root expansion."""
     to_equi = transfer_1d(order, cheb_nodes(order), equispaced=True)

@@ -5,11 +5,14 @@ Checkers: golden vectors produced by the reference itself
 (tests/golden/make_golden.py -> oracle/_ref), the reference library directly
 when it is present, and the numpy restatement (oracle/ankh_oracle.py).
 
-Tolerances (north star): e_total within 1e-10 relative; leaf assignment and
-order bit-exact.  Components are checked at 1e-11 relative (e_near, e_far,
-e_self) -- e_periodic_far is cancellation-limited (the root expansion of a
-neutral box sums to ~0 against a nearly constant generator), so it is checked
-at 1e-8 relative to itself and 1e-12 relative to e_total.
+Tolerances (north star): e_total within 1e-10 relative on every case; leaf
+assignment and order bit-exact.  Components are checked at 1e-11 relative
+(e_near, e_far, e_self, e_periodic_far); where e_periodic_far misses 1e-11 the
+test proves the miss is the case's own cancellation floor: the root expansion
+of a neutral box is a sum of cancelling per-particle terms and the quadratic
+form cancels again, so the gate adds the per-case round-off bound
+(oracle periodic_cancellation_bound, measured errors 0.001-0.11 of it on the
+golden cases).
 """
 import hashlib
 import json
@@ -30,15 +33,38 @@ def rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
-def check_energies(got, want, scale_total=True, tol_total=1e-10):
+def check_energies(got, want, system=None, tol_total=1e-10):
+    """e_total within tol_total of |e_total| on every case; e_near, e_far,
+    e_self within 1e-11 relative (+1e-14 of the component sum, for exact
+    zeros); e_periodic_far within 1e-11 relative, or -- when that fails and
+    the system (pos, src, r_B, config) is given -- within its per-case
+    round-off bound (oracle periodic_cancellation_bound): the root expansion
+    of a neutral box is a sum of cancelling per-particle terms and the
+    quadratic form cancels again, so its absolute error scales with those
+    summands, not with e_periodic_far itself."""
     w = {k: float(v) for k, v in want.items() if k.startswith("e_")}
     comps = abs(w["e_near"]) + abs(w["e_far"]) + abs(w["e_self"]) + abs(w["e_periodic_far"])
-    denom = abs(w["e_total"]) if scale_total else comps
-    assert abs(got.e_total - w["e_total"]) <= tol_total * denom, (got.e_total, w["e_total"])
+    assert abs(got.e_total - w["e_total"]) <= tol_total * abs(w["e_total"]) + 1e-14 * comps, \
+        (got.e_total, w["e_total"])
     for k in ("e_near", "e_far", "e_self"):
         assert abs(getattr(got, k) - w[k]) <= 1e-11 * max(abs(w[k]), 1e-300) + 1e-14 * comps, k
     dp = abs(got.e_periodic_far - w["e_periodic_far"])
-    assert dp <= 1e-8 * abs(w["e_periodic_far"]) + 1e-12 * comps, (got.e_periodic_far, w["e_periodic_far"])
+    if dp <= 1e-11 * abs(w["e_periodic_far"]):
+        return
+    assert system is not None, ("e_periodic_far beyond 1e-11 and no system for its bound",
+                                got.e_periodic_far, w["e_periodic_far"])
+    bound = _periodic_bound(*system)
+    assert dp <= 1e-11 * abs(w["e_periodic_far"]) + bound, (got.e_periodic_far, w["e_periodic_far"], bound)
+
+
+def _periodic_bound(pos, src, rb, kw):
+    import ankh_oracle as O  # checker only
+    import ref as R
+
+    L = kw["order_cheb"]
+    depth = kw.get("depth") or O.default_depth(pos.shape[0])
+    root = R.expansions(pos, src, rb, depth, L)[0][0]
+    return O.periodic_cancellation_bound(pos, src, rb, L, kw.get("xi", 0.01), kw.get("p", 15), root)
 
 
 def _load(name):
@@ -67,8 +93,7 @@ def test_golden_small(cuda, case):
     pos, src = _system(case)
     kw = dict(case["config"])
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, case["box_radius"]), ankh.EwaldConfig(**kw))
-    # random test systems have strongly cancelling components; water boxes do not
-    check_energies(rep, case["energies"], scale_total=case["kind"] != "random")
+    check_energies(rep, case["energies"], (pos, src, case["box_radius"], kw))
     offs, idx = ankh.build_tree_csr(pos, case["box_radius"], rep.depth)
     assert hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest() == case["leaf_csr_sha256"]
 
@@ -80,7 +105,7 @@ def test_golden_high_orders(cuda, case):
     pos, src = _system(case)
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, case["box_radius"]),
                           ankh.EwaldConfig(**case["config"]))
-    check_energies(rep, case["energies"], scale_total=False)
+    check_energies(rep, case["energies"], (pos, src, case["box_radius"], case["config"]))
     offs, idx = ankh.build_tree_csr(pos, case["box_radius"], rep.depth)
     assert hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest() == case["leaf_csr_sha256"]
 
@@ -92,7 +117,7 @@ def test_golden_configs(cuda, case):
     pos, src = _system(case)
     kw = dict(case["config"])
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, case["box_radius"]), ankh.EwaldConfig(**kw))
-    check_energies(rep, case["energies"])
+    check_energies(rep, case["energies"], (pos, src, case["box_radius"], kw))
     offs, idx = ankh.build_tree_csr(pos, case["box_radius"], rep.depth)
     assert hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest() == case["leaf_csr_sha256"]
 
@@ -109,7 +134,7 @@ def test_oracle_random(cuda, ref, kw, n, rb, mp):
     pos, src = inputs.random_system(n, rb, seed=n + kw["order_cheb"], multipoles=mp)
     want = ref.fmm_energy(pos, src, rb, threads=os.cpu_count(), **kw)
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, rb), ankh.EwaldConfig(**kw))
-    check_energies(rep, want, scale_total=False)
+    check_energies(rep, want, (pos, src, rb, kw))
 
 
 def test_mixed_moment_orders(cuda, ref):
@@ -120,7 +145,7 @@ def test_mixed_moment_orders(cuda, ref):
     kw = dict(order_cheb=4, order_equi=4, depth=2, p=15)
     want = ref.fmm_energy(pos, src, 5.0, threads=os.cpu_count(), **kw)
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 5.0), ankh.EwaldConfig(**kw))
-    check_energies(rep, want, scale_total=False)
+    check_energies(rep, want, (pos, src, 5.0, kw))
 
 
 def test_large_leaves_chunking(cuda, ref):
@@ -129,7 +154,7 @@ def test_large_leaves_chunking(cuda, ref):
     kw = dict(order_cheb=3, order_equi=3, depth=1, p=2)
     want = ref.fmm_energy(pos, src, 10.0, threads=os.cpu_count(), **kw)
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 10.0), ankh.EwaldConfig(**kw))
-    check_energies(rep, want, scale_total=False)
+    check_energies(rep, want, (pos, src, 10.0, kw))
 
 
 def test_own_leaf_larger_than_a_chunk(cuda, ref):
@@ -140,7 +165,7 @@ def test_own_leaf_larger_than_a_chunk(cuda, ref):
     kw = dict(order_cheb=3, order_equi=3, depth=1, p=2)
     want = ref.fmm_energy(pos, src, 10.0, threads=os.cpu_count(), **kw)
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, 10.0), ankh.EwaldConfig(**kw))
-    check_energies(rep, want, scale_total=False)
+    check_energies(rep, want, (pos, src, 10.0, kw))
 
 
 def test_leaf_csr_bit_exact(cuda, ref):
@@ -357,7 +382,7 @@ def test_config4_style_rescaled_dipoles(cuda, ref):
         s = src.copy()
         s[:, 1:4] *= f
         want = ref.fmm_energy(pos, s, 6.0, threads=os.cpu_count(), **kw)
-        check_energies(plan.energy(pos, s), want, scale_total=False)
+        check_energies(plan.energy(pos, s), want, (pos, s, 6.0, kw))
 
 
 # ------------------------------------------------------------ error semantics
@@ -418,7 +443,7 @@ def test_golden_headline_configs(cuda, name):
         src[:, 1:4] *= case["dipole_scale"]
     assert hashlib.sha256(pos.tobytes() + src.tobytes()).hexdigest() == case["sha256"]
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, rb), ankh.EwaldConfig(**case["config"]))
-    check_energies(rep, case["energies"])
+    check_energies(rep, case["energies"], (pos, src, rb, case["config"]))
 
 
 def test_config4_series(cuda):
@@ -731,7 +756,7 @@ def test_config4_series_all_evaluations_vs_reference(cuda):
         src = src0.copy()
         src[:, 1:4] *= ev["dipole_scale"]
         rep = plan.energy_sources(src)
-        check_energies(rep, ev["energies"])
+        check_energies(rep, ev["energies"], (pos, src, rb, want["config"]))
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("ANKH_RANDOM_CASES", "12"))))
@@ -756,7 +781,7 @@ def test_randomized_configurations_vs_reference(cuda, ref, seed):
     kw = dict(order_cheb=L, order_equi=L, depth=depth, p=p, xi=xi)
     want = ref.fmm_energy(pos, src, rb, threads=os.cpu_count(), **kw)
     rep = ankh.fmm_energy(ankh.ParticleSystem(pos, src, rb), ankh.EwaldConfig(**kw))
-    check_energies(rep, want, scale_total=False)
+    check_energies(rep, want, (pos, src, rb, kw))
     offs, idx = ankh.build_tree_csr(pos, rb, depth)
     o2, i2 = ref.leaf_csr(pos, rb, depth)
     assert np.array_equal(offs, o2) and np.array_equal(idx, i2)
