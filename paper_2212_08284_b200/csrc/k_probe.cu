@@ -1,7 +1,10 @@
 // FP64 pipe peak probe (roofline denominator).  MEASURED_PEAKS.json carries
 // HBM and bf16 figures only, so bench.py measures the DFMA peak in-process,
-// right before its timed region, with this kernel: 8 independent FMA chains
-// per thread, 4 CTAs x 256 threads per SM, timed with CUDA events.
+// right before its timed region: the best of a few DFMA-chain shapes (8 / 16
+// / 32 independent chains per thread, 2 / 4 / 8 CTAs of 256 threads per SM),
+// timed with CUDA events.
+#include <algorithm>
+
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -9,20 +12,21 @@
 namespace ankh_b200 {
 
 namespace {
+template <int CH>
 __global__ void __launch_bounds__(256) k_dfma(double* out, int iters, double b, double c) {
-  double a[8];
+  double a[CH];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3 + k;
+  for (int k = 0; k < CH; ++k) a[k] = threadIdx.x * 1e-3 + k;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+    for (int r = 0; r < 128 / CH; ++r) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+      for (int k = 0; k < CH; ++k) a[k] = fma(a[k], b, c);
     }
   }
   double s = 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) s += a[k];
+  for (int k = 0; k < CH; ++k) s += a[k];
   if (s == 12345.678) out[0] = s;  // keep the chains live
 }
 
@@ -185,19 +189,30 @@ double probe_fp64_tflops(int iters) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int blocks = sms * 4;
-  k_dfma<<<blocks, 256>>>(d, iters / 4 + 1, 0.999999, 1e-7);  // warm-up / clock ramp
-  cudaEventRecord(e0);
-  k_dfma<<<blocks, 256>>>(d, iters, 0.999999, 1e-7);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
+  // the best of a few shapes (independent chains per thread x resident CTAs
+  // per SM): 128 FMA per thread per iteration in every case
+  double best = 0.0;
+  auto run = [&](auto kernel, int per_sm) {
+    const int blocks = sms * per_sm;
+    kernel<<<blocks, 256>>>(d, iters / 4 + 1, 0.999999, 1e-7);  // warm-up / clock ramp
+    cudaEventRecord(e0);
+    kernel<<<blocks, 256>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 128 * static_cast<double>(iters) * blocks * 256;
+    if (ms > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  };
+  run(k_dfma<8>, 4);
+  run(k_dfma<8>, 8);
+  run(k_dfma<16>, 4);
+  run(k_dfma<16>, 2);
+  run(k_dfma<32>, 2);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(d);
-  const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * 256;
-  return ms > 0 ? flops / (ms * 1e-3) / 1e12 : 0.0;
+  return best;
 }
 
 }  // namespace ankh_b200
