@@ -180,43 +180,53 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     order = sorted + base;
   }
   if (!part) return;  // sort only (positions bound ahead of the moments)
-  // four threads per particle (more loads in flight than one thread per
-  // record): thread k writes 16-B pieces {k, k+4} of the record
+  // four threads (a lane quad) per particle: the moments row (80 B, 16-B
+  // aligned) is read as five 16-B pieces s0..s4 = (q,mx) (my,mz) (txx,txy)
+  // (txz,tyy) (tyz,tzz) -- lane k takes s_k, lane 0 also s4 and (x, y), lane 1
+  // z -- and the record's 16-B pieces {k, k+4} are assembled by quad shuffles:
   //   0 (x, y)  1 (z, q)  2 (mx, my)  3 (mz, txx)  4 (txy, txz)  5 (tyy, tyz)  6 (tzz, tr)
-  // and checks the moments it read (together every one of q, mu, Theta)
+  // Each lane checks the moments it read (together every one of q, mu, Theta).
   bool mp = false;
-  for (int e = threadIdx.x; e < 4 * c; e += kLeafThreads) {
-    const int p = e >> 2, k = e & 3;
+  const int k = threadIdx.x & 3;
+  for (int e0 = 0; e0 < 4 * c; e0 += kLeafThreads) {
+    const int e = e0 + threadIdx.x;
+    const bool ok = e < 4 * c;  // whole quads: 4c is a multiple of 4
+    const int p = ok ? e >> 2 : 0;
     const std::size_t i = order[p];
-    const double* ps = pos + 3 * i;
-    const double* ss = src + 10 * i;
-    double2* out = reinterpret_cast<double2*>(part + static_cast<std::size_t>(base + p) * kRec);
-    double a, b, c2 = 0.0, d = 0.0;  // the moments this thread checks
-    if (k == 0) {
-      a = ss[5];
-      b = ss[6];
-      out[0] = make_double2(ps[0], ps[1]);
-      out[4] = make_double2(a, b);
-    } else if (k == 1) {
-      a = ss[7];
-      b = ss[8];
-      c2 = ss[0];
-      out[1] = make_double2(ps[2], c2);
-      out[5] = make_double2(a, b);
-    } else if (k == 2) {
-      a = ss[1];
-      b = ss[2];
-      d = ss[9];
-      out[2] = make_double2(a, b);
-      out[6] = make_double2(d, (ss[4] + ss[7]) + d);  // SymMat3::trace (types.hpp:57)
-    } else {
-      a = ss[3];
-      b = ss[4];
-      out[3] = make_double2(a, b);
+    const double2* s2 = reinterpret_cast<const double2*>(src + 10 * i);
+    double2 mine = ok ? __ldg(s2 + k) : make_double2(0.0, 0.0);
+    double2 s4 = make_double2(0.0, 0.0), xy = make_double2(0.0, 0.0);
+    double z = 0.0;
+    if (ok && k == 0) {
+      s4 = __ldg(s2 + 4);
+      xy = make_double2(__ldg(pos + 3 * i), __ldg(pos + 3 * i + 1));
     }
-    if (check_src && !(isfinite(a) && isfinite(b) && isfinite(c2) && isfinite(d)))
-      atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
-    mp = mp || a != 0.0 || b != 0.0 || d != 0.0;  // (c2 is q: not a multipole)
+    if (ok && k == 1) z = __ldg(pos + 3 * i + 2);
+    // quad exchange (all lanes take part; lane q's pieces from __shfl ... width 4)
+    const double p0x = __shfl_sync(0xffffffffu, mine.x, 0, 4), p0y = __shfl_sync(0xffffffffu, mine.y, 0, 4);
+    const double p1x = __shfl_sync(0xffffffffu, mine.x, 1, 4), p1y = __shfl_sync(0xffffffffu, mine.y, 1, 4);
+    const double p2x = __shfl_sync(0xffffffffu, mine.x, 2, 4), p2y = __shfl_sync(0xffffffffu, mine.y, 2, 4);
+    const double p3x = __shfl_sync(0xffffffffu, mine.x, 3, 4), p3y = __shfl_sync(0xffffffffu, mine.y, 3, 4);
+    const double p4x = __shfl_sync(0xffffffffu, s4.x, 0, 4), p4y = __shfl_sync(0xffffffffu, s4.y, 0, 4);
+    if (!ok) continue;
+    double2* out = reinterpret_cast<double2*>(part + static_cast<std::size_t>(base + p) * kRec);
+    if (k == 0) {
+      out[0] = xy;
+      out[4] = make_double2(p2y, p3x);
+    } else if (k == 1) {
+      out[1] = make_double2(z, p0x);
+      out[5] = make_double2(p3y, p4x);
+    } else if (k == 2) {
+      out[2] = make_double2(p0y, p1x);
+      out[6] = make_double2(p4y, (p2x + p3y) + p4y);  // SymMat3::trace (types.hpp:57)
+    } else {
+      out[3] = make_double2(p1y, p2x);
+    }
+    bool fin = isfinite(mine.x) && isfinite(mine.y);
+    if (k == 0) fin = fin && isfinite(s4.x) && isfinite(s4.y);
+    if (check_src && !fin) atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
+    // multipole: anything but q (lane 0's s0.x) nonzero
+    mp = mp || (k != 0 && mine.x != 0.0) || mine.y != 0.0 || (k == 0 && (s4.x != 0.0 || s4.y != 0.0));
   }
   mp = __syncthreads_or(mp);
   if (threadIdx.x == 0) {
@@ -270,7 +280,6 @@ __global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ sr
   const std::size_t i = (static_cast<std::size_t>(block0) + blockIdx.x) * 256 + threadIdx.x;
   bool mp = false;
   if (i < n) {
-    ANKH_DASSERT(!inv || inv[i] < n);
     if (inv) write_record(pos, src, static_cast<unsigned>(i), part + static_cast<std::size_t>(inv[i]) * kRec);
     mp = check_moments(src + 10 * i, i, res);
   }

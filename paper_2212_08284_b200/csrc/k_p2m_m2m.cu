@@ -405,32 +405,28 @@ __global__ void __launch_bounds__(kP2MThreads) k_p2m(const double* __restrict__ 
 
 constexpr int kM2MThreads = 128;
 
-template <int L>
-__global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ child,
-                                                     double* __restrict__ parent, int level,
-                                                     const double* __restrict__ m2m_g,
-                                                     unsigned p_begin) {
+// One parent's M2M (upward_pass, fmm.cpp:203-236; tensor3_apply,
+// chebyshev.cpp:246-272) by the whole CTA: parent[i,j,k] = sum over the 8
+// children of T_cx(i,a) T_cy(j,b) T_cz(k,c) child[a,b,c], the child sums
+// folded into each axis stage.  M (the two 1-D transfer matrices) is already
+// in shared memory.  kCoherent: children written by other CTAs of the same
+// launch (the chained kernel) are read past L1 (ld.global.cg).
+template <int L, bool kCoherent>
+__device__ __forceinline__ void m2m_parent(const double* __restrict__ child, double* __restrict__ parent,
+                                           unsigned pcell, const double* M, double* V, double* S1, double* S2) {
   constexpr int L2 = L * L, K = L2 * L, KS = exp_stride(K);
-  extern __shared__ __align__(16) double sm[];
-  double* M = sm;               // 2 x L x L: M[c][i][a] = T_c(i, a)
-  double* V = M + 2 * L2;       // 8 x KS children (rows as stored, zero tails)
-  double* S1 = V + 8 * KS;      // 4 x K  (cx, cy) after z
-  double* S2 = S1 + 4 * K;      // 2 x K  (cx) after y
-  (void)level;
   // Morton order: the children of parent p are rows 8p + (cx<<2 | cy<<1 | cz),
   // one contiguous 8 KS-double block: loaded as 16-B pieces, a batch of
   // loads in flight per thread before any shared-memory store
-  const unsigned pcell = p_begin + blockIdx.x;
   const double2* ch0 = reinterpret_cast<const double2*>(child + static_cast<std::size_t>(pcell) * 8 * KS);
   double2* V2 = reinterpret_cast<double2*>(V);
   constexpr int NV = 8 * KS / 2, kBatch = 8;
-  for (int w = threadIdx.x; w < 2 * L2; w += kM2MThreads) M[w] = m2m_g[w];
   for (int w0 = 0; w0 < NV; w0 += kBatch * kM2MThreads) {
     double2 t[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
       const int w = w0 + u * kM2MThreads + threadIdx.x;
-      if (w < NV) t[u] = __ldg(ch0 + w);
+      if (w < NV) t[u] = kCoherent ? __ldcg(ch0 + w) : __ldg(ch0 + w);
     }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
@@ -486,6 +482,51 @@ __global__ void __launch_bounds__(kM2MThreads) k_m2m(const double* __restrict__ 
   }
 }
 
+// The upward pass in ONE launch: CTA b computes parent p_begin + b at level
+// `first`; the last of eight siblings to finish (per-cell arrival counter,
+// threadfence pattern) goes on to their parent, and so on up to level `top`.
+// Every sibling set lies inside the launch's cells (whole subtrees), so each
+// cell is computed exactly once, by the CTA that completed its children.
+// The counters reset themselves (the eighth arrival zeroes its slot).
+template <int L>
+__global__ void __launch_bounds__(kM2MThreads) k_m2m_chain(double* __restrict__ exp,
+                                                           const long long* __restrict__ level_off, int first,
+                                                           int top, unsigned p_begin,
+                                                           unsigned* __restrict__ counters,
+                                                           const double* __restrict__ m2m_g) {
+  constexpr int L2 = L * L, K = L2 * L, KS = exp_stride(K);
+  extern __shared__ __align__(16) double sm[];
+  double* M = sm;           // 2 x L x L: M[c][i][a] = T_c(i, a)
+  double* V = M + 2 * L2;   // 8 x KS children (rows as stored, zero tails)
+  double* S1 = V + 8 * KS;  // 4 x K  (cx, cy) after z
+  double* S2 = S1 + 4 * K;  // 2 x K  (cx) after y
+  __shared__ int s_last;
+  for (int w = threadIdx.x; w < 2 * L2; w += kM2MThreads) M[w] = m2m_g[w];
+  unsigned p = p_begin + blockIdx.x;
+  int l = first;
+  for (;;) {
+    if (l == first)
+      m2m_parent<L, false>(exp + level_off[l + 1], exp + level_off[l], p, M, V, S1, S2);
+    else
+      m2m_parent<L, true>(exp + level_off[l + 1], exp + level_off[l], p, M, V, S1, S2);
+    if (l == top) break;
+    __threadfence();  // this parent row is visible before the arrival is counted
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // counters of the parent level l - 1: cells [8^(l-1) - 1) / 7 ...
+      unsigned* c = counters + ((1u << (3 * (l - 1))) - 1u) / 7u + (p >> 3);
+      const unsigned old = atomicAdd(c, 1u);
+      s_last = old == 7u;
+      if (old == 7u) *c = 0u;
+    }
+    __syncthreads();
+    if (!s_last) break;
+    __threadfence();  // the siblings' rows, published before their arrivals
+    p >>= 3;
+    --l;
+  }
+}
+
 template <int L>
 void p2m_order(const double* part, const unsigned* leaf_off, int depth, double rb,
                const double* hd, double* exp_leaf, const DevResult* res, double* self_leaf, double xi,
@@ -524,14 +565,13 @@ void upload_p2m_basis(int order, const double* hd, cudaStream_t st) {
 namespace {
 
 template <int L>
-void m2m_order(const double* child, double* parent, int parent_level, const double* m2m,
-               cudaStream_t st, unsigned p_begin, unsigned p_count) {
+void m2m_chain_order(double* exp, const long long* level_off, int first, int top, unsigned p_begin,
+                     unsigned p_count, unsigned* counters, const double* m2m, cudaStream_t st) {
   constexpr int K = L * L * L;
   const std::size_t smem = sizeof(double) * (2 * L * L + 8 * exp_stride(K) + 6 * K);
   static std::atomic<unsigned long long> attr{0};
-  smem_opt_in(attr, k_m2m<L>, smem);
-  const unsigned cells = p_count ? p_count : (1u << (3 * parent_level));
-  k_m2m<L><<<cells, kM2MThreads, smem, st>>>(child, parent, parent_level, m2m, p_begin);
+  smem_opt_in(attr, k_m2m_chain<L>, smem);
+  k_m2m_chain<L><<<p_count, kM2MThreads, smem, st>>>(exp, level_off, first, top, p_begin, counters, m2m);
 }
 
 }  // namespace
@@ -561,9 +601,18 @@ void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int ord
 #undef ANKH_P2M
 }
 
-void launch_m2m(const double* child, double* parent, int parent_level, int order,
-                const double* m2m, cudaStream_t st, unsigned p_begin, unsigned p_count) {
-#define ANKH_M2M(N) m2m_order<N>(child, parent, parent_level, m2m, st, p_begin, p_count)
+std::size_t m2m_counter_count(int depth) {
+  std::size_t c = 0;
+  for (int l = 0; l < depth; ++l) c += std::size_t(1) << (3 * l);
+  return c;
+}
+
+void launch_m2m_chain(double* exp, const long long* level_off, int first, int top, int order,
+                      const double* m2m, unsigned* counters, cudaStream_t st, unsigned p_begin,
+                      unsigned p_count) {
+  if (first < top || first < 0) return;
+  if (p_count == 0) p_count = 1u << (3 * first);
+#define ANKH_M2M(N) m2m_chain_order<N>(exp, level_off, first, top, p_begin, p_count, counters, m2m, st)
   ANKH_ORDER_SWITCH(order, ANKH_M2M)
 #undef ANKH_M2M
 }

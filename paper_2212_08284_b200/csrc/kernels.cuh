@@ -146,9 +146,14 @@ void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std:
                            unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
                            unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st,
                            unsigned* host_bounds = nullptr, cudaEvent_t after_inverse = nullptr);
-/// Parents [p_begin, p_begin + p_count) of `parent_level` (Morton); p_count 0: all.
-void launch_m2m(const double* child, double* parent, int parent_level, int order,
-                const double* m2m, cudaStream_t st, unsigned p_begin = 0, unsigned p_count = 0);
+/// The upward pass (M2M) in one launch: parents [p_begin, p_begin + p_count)
+/// of level `first` (Morton; p_count 0: all), then every coarser level down
+/// to `top`, each cell by the last of its children's CTAs to finish.
+/// counters: m2m_counter_count(depth) zeroed uints (self-resetting).
+std::size_t m2m_counter_count(int depth);
+void launch_m2m_chain(double* exp, const long long* level_off, int first, int top, int order,
+                      const double* m2m, unsigned* counters, cudaStream_t st, unsigned p_begin = 0,
+                      unsigned p_count = 0);
 void launch_m2l(const double* exp, const long long* level_off, const double* factors,
                 const M2LOp* ops, const M2LTile* tiles, int n_tiles_class, int kp8,
                 const int* tile_ids, const uint2* inst, int K, int Kp, double* far_partial,

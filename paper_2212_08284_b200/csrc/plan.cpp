@@ -327,6 +327,9 @@ void Plan::allocate() {
   for (int l = 0; l <= depth; ++l) level_off_[l + 1] = level_off_[l] + (1ll << (3 * l)) * Kp;
   d_exp_ = static_cast<double*>(dalloc(level_off_[depth + 1] * sizeof(double)));
   ANKH_CUDA(cudaMemsetAsync(d_exp_, 0, level_off_[depth + 1] * sizeof(double), stream_));
+  d_m2m_cnt_ = static_cast<unsigned*>(dalloc(std::max<std::size_t>(m2m_counter_count(depth), 1) * sizeof(unsigned)));
+  ANKH_CUDA(cudaMemsetAsync(d_m2m_cnt_, 0, std::max<std::size_t>(m2m_counter_count(depth), 1) * sizeof(unsigned),
+                            stream_));
   d_level_off_ = static_cast<long long*>(dalloc(level_off_.size() * sizeof(long long)));
   ANKH_CUDA(cudaMemcpyAsync(d_level_off_, level_off_.data(), level_off_.size() * sizeof(long long),
                             cudaMemcpyHostToDevice, stream_));
@@ -814,8 +817,8 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   m2m_top_ = depth - 1;
   if (mode == 0 || mode == 3) launches += exchange_upward(far);
   if (serial) {
-    for (int l = m2m_top_; l >= 0; --l) {
-      launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, far);
+    if (m2m_top_ >= 0) {
+      launch_m2m_chain(d_exp_, d_level_off_, m2m_top_, 0, L, d_m2m_, d_m2m_cnt_, far);
       ++launches;
     }
     if (timing) ANKH_CUDA(cudaEventRecord(ev_[2], st));
@@ -892,10 +895,9 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
     ++launches;
   };
   auto m2m = [&](cudaStream_t s) {
-    for (int l = m2m_top_; l >= 0; --l) {  // (levels below are done by exchange_upward)
-      launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, s);
-      ++launches;
-    }
+    if (m2m_top_ < 0) return;  // (levels below m2m_top_ are done by exchange_upward)
+    launch_m2m_chain(d_exp_, d_level_off_, m2m_top_, 0, L, d_m2m_, d_m2m_cnt_, s);
+    ++launches;
   };
   if (!fork) {
     m2m(far);
@@ -1043,10 +1045,10 @@ std::uint32_t Plan::exchange_upward(cudaStream_t st) {
   if (!coll_ || !shard_upward_) return 0;
   std::uint32_t launches = 0;
   const long long G = cfg.world, r = cfg.rank;
-  for (int l = depth - 1; l >= exch_level_; --l) {
-    const long long cells = 1ll << (3 * l);
-    launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, st,
-               static_cast<unsigned>(cells * r / G), static_cast<unsigned>(cells / G));
+  if (depth - 1 >= exch_level_) {  // this shard's subtrees, parent levels depth-1 .. exch_level_
+    const long long cells = 1ll << (3 * (depth - 1));
+    launch_m2m_chain(d_exp_, d_level_off_, depth - 1, exch_level_, L, d_m2m_, d_m2m_cnt_, st,
+                     static_cast<unsigned>(cells * r / G), static_cast<unsigned>(cells / G));
     ++launches;
   }
   std::vector<double*> recv;
@@ -1275,10 +1277,8 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[C - 1], 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[3], st));
   if (timing) {  // phase spans: M2M, M2L, periodic back to back
-    for (int l = depth - 1; l >= 0; --l) {
-      launch_m2m(d_exp_ + level_off_[l + 1], d_exp_ + level_off_[l], l, L, d_m2m_, side_stream_);
-      ++launches;
-    }
+    launch_m2m_chain(d_exp_, d_level_off_, depth - 1, 0, L, d_m2m_, d_m2m_cnt_, side_stream_);
+    ++launches;
     ANKH_CUDA(cudaEventRecord(ev_t_[4], side_stream_));
     for (int c = 1; c <= kMaxKp8; ++c) {
       const auto r = class_range_[c];

@@ -258,7 +258,8 @@ class Plan {
   double *d_pos_ = nullptr, *d_src_ = nullptr;
   unsigned *d_keys_ = nullptr, *d_keys2_ = nullptr, *d_idx_ = nullptr, *d_idx2_ = nullptr;
   unsigned *d_counts_ = nullptr, *d_off_ = nullptr;
-  unsigned* d_leaf_mp_ = nullptr;  // per lex leaf: holds a dipole / quadrupole (P2P pair code)
+  unsigned* d_leaf_mp_ = nullptr;
+  unsigned* d_m2m_cnt_ = nullptr;  // arrival counters of the chained M2M  // per lex leaf: holds a dipole / quadrupole (P2P pair code)
   unsigned char* d_need_ = nullptr;  // shard: leaves whose records are gathered
   double* d_fin_scratch_ = nullptr;   // two-level final reduction
   void* d_temp_ = nullptr;
