@@ -40,15 +40,38 @@ __device__ __forceinline__ bool check_moments(const double* __restrict__ s, std:
   return finite && mp;
 }
 
+// Lanes of a warp with the same key take consecutive slots of one counter
+// with a single atomic (consecutive particles mostly share a leaf, so
+// per-lane atomics would serialise on a handful of addresses); the leader
+// also raises the leaf's largest index (the streamed path's readiness).
+// key == ~0u: lane inactive.  Returns the lane's slot.
+__device__ __forceinline__ unsigned warp_count(unsigned key, unsigned* counts, unsigned* leafmax, unsigned i) {
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  unsigned base = 0;
+  if (lane == leader && key != ~0u) {
+    base = atomicAdd(&counts[key], static_cast<unsigned>(__popc(peers)));
+    // indices ascend with the lane: the highest peer holds the largest
+    if (leafmax) atomicMax(&leafmax[key], i + static_cast<unsigned>((31 - __clz(peers)) - lane));
+  }
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + static_cast<unsigned>(__popc(peers & ((1u << lane) - 1u)));
+}
+
+// particles [256 block0, n): one range of the positions (the streamed path
+// bins each arrived chunk) or all of them (block0 = 0)
 __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
                                              const double* __restrict__ src, std::size_t n,
                                              double rb, double inv_side, int nax,
                                              unsigned* __restrict__ keys,
                                              unsigned* __restrict__ idx,
                                              unsigned* __restrict__ counts,
-                                             const unsigned char* __restrict__ need, DevResult* res) {
-  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+                                             const unsigned char* __restrict__ need, DevResult* res,
+                                             unsigned block0, unsigned* __restrict__ leafmax) {
+  const std::size_t i = (static_cast<std::size_t>(block0) + blockIdx.x) * 256 + threadIdx.x;
   bool mp = false;
+  unsigned key = 0;
+  bool counted = false;
   if (i < n) {
     const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
     bool finite = isfinite(x) && isfinite(y) && isfinite(z);
@@ -60,7 +83,6 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
       for (int k = 0; k < 10; ++k) finite = finite && isfinite(s[k]);
       mp = finite && check_moments(s, i, res);
     }
-    unsigned key = 0;
     if (!finite) {
       atomicMin(&res->min_nonfinite, static_cast<unsigned long long>(i));
     } else {
@@ -72,17 +94,110 @@ __global__ void __launch_bounds__(256) k_bin(const double* __restrict__ pos,
       key = static_cast<unsigned>((ix * nax + iy) * nax + iz);
     }
     keys[i] = key;
-    // counting sort: idx receives the particle's arrival slot in its leaf
-    // (ascending order inside the leaf is restored by k_leaf_gather);
-    // without counts (validation path) idx is the identity for the radix sort.
-    // A shard (need != nullptr) sorts only the leaves it reads: the others
-    // stay empty in its CSR (every particle is still validated above).
+    // without counts (validation path) idx is the identity for the radix sort;
+    // a shard (need != nullptr) sorts only the leaves it reads: the others
+    // stay empty in its CSR (every particle is still validated above)
     if (!counts)
       idx[i] = static_cast<unsigned>(i);
+    else if (need && !need[key])
+      idx[i] = ~0u;
     else
-      idx[i] = (need && !need[key]) ? ~0u : atomicAdd(&counts[key], 1u);
+      counted = true;
+  }
+  // counting sort: idx receives the particle's arrival slot in its leaf
+  // (ascending order inside the leaf is restored by k_leaf_gather)
+  if (counts) {  // uniform across the grid: every lane takes part
+    const unsigned slot = warp_count(counted ? key : ~0u, counts, leafmax, static_cast<unsigned>(i));
+    if (counted) idx[i] = slot;
   }
   if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
+}
+
+// Exclusive scan of n uints in one pass (the leaf histogram -> the CSR
+// offsets): tiles of 4096 taken in ticket order, each publishes its
+// aggregate and then its inclusive prefix (decoupled look-back over the
+// predecessors' status words: flag in bits 62-63, value below).  The state
+// (status[tiles], ticket, done) resets itself: the last tile to finish
+// zeroes it for the next launch (zero-initialised once by the plan).
+constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kScanAgg = 1ull << 62, kScanIncl = 2ull << 62, kScanVal = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(const unsigned* __restrict__ in, unsigned* __restrict__ out,
+                                                       unsigned n, unsigned long long* status, unsigned* ctr) {
+  __shared__ unsigned s_tile, s_prefix, s_last, s_warp[kScanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(&ctr[0], 1u);
+  __syncthreads();
+  const unsigned tile = s_tile;
+  const std::size_t base = static_cast<std::size_t>(tile) * kScanTile + static_cast<std::size_t>(tid) * kScanItems;
+  unsigned v[kScanItems];
+  if (base + kScanItems <= n) {
+    const uint4* p = reinterpret_cast<const uint4*>(in + base);
+#pragma unroll
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      const uint4 w = p[q];
+      v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = base + k < n ? in[base + k] : 0u;
+  }
+  unsigned tsum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) tsum += v[k];
+  unsigned incl = tsum;  // warp-inclusive scan of the thread sums
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned agg = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+      const unsigned t = s_warp[w];
+      s_warp[w] = agg;
+      agg += t;
+    }
+    volatile unsigned long long* st = status;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      st[0] = kScanIncl | agg;
+    } else {
+      st[tile] = kScanAgg | agg;
+      for (int j = static_cast<int>(tile) - 1; j >= 0;) {
+        const unsigned long long w = st[j];
+        if ((w & ~kScanVal) == 0) continue;  // predecessor not published yet
+        excl += w & kScanVal;
+        if ((w & ~kScanVal) == kScanIncl) break;
+        --j;
+      }
+      st[tile] = kScanIncl | (excl + agg);
+    }
+    s_prefix = static_cast<unsigned>(excl);
+  }
+  __syncthreads();
+  unsigned run = s_prefix + s_warp[warp] + (incl - tsum);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+  // self-reset: the last tile to finish clears the state for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(&ctr[1], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (unsigned j = tid; j < gridDim.x; j += kScanThreads) status[j] = 0ull;
+    if (tid == 0) {
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+    }
+  }
 }
 
 // Counting-sort scatter: particle i goes to offsets[key] + slot (leaf order is
@@ -131,7 +246,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
     const unsigned* __restrict__ offsets, unsigned* __restrict__ unsorted,
     unsigned* __restrict__ scratch, unsigned* __restrict__ sorted,
     const unsigned char* __restrict__ need, double* __restrict__ part, bool check_src,
-    DevResult* res, unsigned* __restrict__ leaf_mp) {
+    DevResult* res, unsigned* __restrict__ leaf_mp, unsigned* __restrict__ inv) {
   __shared__ unsigned a[kLeafSmem], b[kLeafSmem];
   const unsigned leaf = blockIdx.x;
   if (need && !need[leaf]) return;  // another shard's leaf
@@ -152,6 +267,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
       for (int j = 0; j < c; ++j) rank += a[j] < v;
       b[rank] = v;
       sorted[base + rank] = v;
+      if (inv) inv[v] = base + rank;  // the sorted slot of particle v
     }
     __syncthreads();
     order = b;
@@ -175,7 +291,10 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf_gather(
       x = y;
       y = t;
     }
-    for (int p = threadIdx.x; p < c; p += kLeafThreads) sorted[base + p] = x[p];
+    for (int p = threadIdx.x; p < c; p += kLeafThreads) {
+      sorted[base + p] = x[p];
+      if (inv) inv[x[p]] = base + p;
+    }
     __syncthreads();
     order = sorted + base;
   }
@@ -287,27 +406,28 @@ __global__ void __launch_bounds__(256) k_src_check(const double* __restrict__ sr
   if (__syncthreads_or(mp) && threadIdx.x == 0) atomicOr(&res->any_multipole, 1);
 }
 
-// inv[sorted[j]] = j: the sorted slot of every particle
-__global__ void k_inverse(const unsigned* __restrict__ sorted, std::size_t n, unsigned* __restrict__ inv) {
-  const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (j < n) inv[sorted[j]] = static_cast<unsigned>(j);
-}
-
 // Streamed host path, per Morton leaf m: the chunk after which its records
-// are complete (its largest particle index -- leaves hold ascending indices)
+// are complete (the chunk of its largest particle index, leafmax from k_bin)
 // and the chunk after which its 13 half-shell neighbours are too (P2P's
 // source set, k_p2p); counts per chunk in cnt[0..C) (P2M) / cnt[C..2C) (P2P).
-__device__ __forceinline__ void stream_ready_leaf(unsigned m, const unsigned* __restrict__ offsets,
-                                                  const unsigned* __restrict__ sorted, int depth, int periodic,
-                                                  unsigned chunk, int n_chunks, unsigned char* __restrict__ ready,
-                                                  unsigned* key_p2m, unsigned* key_p2p) {
+__device__ __forceinline__ int chunk_of(unsigned i, const StreamChunks& ch) {
+  int lo = 0, hi = ch.n - 1;  // the last c with start[c] <= i
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ch.start[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void stream_ready_leaf(unsigned m, const unsigned* __restrict__ leafmax, int depth,
+                                                  int periodic, const StreamChunks& ch,
+                                                  unsigned char* __restrict__ ready, unsigned* key_p2m,
+                                                  unsigned* key_p2p) {
   const int n = 1 << depth;
   const int ax = static_cast<int>(morton_compact3(m >> 2)), ay = static_cast<int>(morton_compact3(m >> 1)),
             az = static_cast<int>(morton_compact3(m));
   auto leaf_ready = [&](int x, int y, int z) -> int {
-    const unsigned b = static_cast<unsigned>((x * n + y) * n + z);
-    const unsigned e = offsets[b + 1];
-    return e > offsets[b] ? static_cast<int>(sorted[e - 1] / chunk) : 0;
+    return chunk_of(leafmax[static_cast<unsigned>((x * n + y) * n + z)], ch);  // empty: 0
   };
   const int r = leaf_ready(ax, ay, az);
   int p = r;
@@ -328,7 +448,7 @@ __device__ __forceinline__ void stream_ready_leaf(unsigned m, const unsigned* __
   ready[2 * m] = static_cast<unsigned char>(r);
   ready[2 * m + 1] = static_cast<unsigned char>(p);
   *key_p2m = static_cast<unsigned>(r);
-  *key_p2p = static_cast<unsigned>(n_chunks + p);
+  *key_p2p = static_cast<unsigned>(ch.n + p);
 }
 
 // Warp-aggregated slot in a shared-memory counter per key: the lanes with
@@ -344,9 +464,9 @@ __device__ __forceinline__ unsigned warp_slot(unsigned key, unsigned* s_cnt) {
   return base + static_cast<unsigned>(__popc(peers & ((1u << lane) - 1u)));
 }
 
-__global__ void __launch_bounds__(256) k_stream_ready(const unsigned* __restrict__ offsets,
-                                                      const unsigned* __restrict__ sorted, int depth,
-                                                      int periodic, unsigned chunk, int n_chunks,
+// cnt[0 .. 2C) and cursor[0 .. 2C) zeroed by the caller (one memset)
+__global__ void __launch_bounds__(256) k_stream_ready(const unsigned* __restrict__ leafmax, int depth,
+                                                      int periodic, StreamChunks ch,
                                                       unsigned char* __restrict__ ready,
                                                       unsigned* __restrict__ cnt) {
   __shared__ unsigned s_cnt[2 * kMaxStreamChunks];
@@ -354,53 +474,45 @@ __global__ void __launch_bounds__(256) k_stream_ready(const unsigned* __restrict
   __syncthreads();
   const unsigned m = blockIdx.x * 256 + threadIdx.x;
   unsigned k0 = ~0u, k1 = ~0u;
-  if (m < (1u << (3 * depth))) stream_ready_leaf(m, offsets, sorted, depth, periodic, chunk, n_chunks, ready, &k0, &k1);
+  if (m < (1u << (3 * depth))) stream_ready_leaf(m, leafmax, depth, periodic, ch, ready, &k0, &k1);
   warp_slot(k0, s_cnt);
   warp_slot(k1, s_cnt);
   __syncthreads();
-  if (threadIdx.x < 2 * n_chunks && s_cnt[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], s_cnt[threadIdx.x]);
+  if (threadIdx.x < 2 * ch.n && s_cnt[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], s_cnt[threadIdx.x]);
 }
 
-// bounds[0..C] / bounds[C+1..2C+1]: exclusive scans of the two count sets;
-// cursors reset to the bucket starts
-// (bounds also stored to host_bounds -- mapped page-locked memory the host
-// reads after the kernel: no device-to-host copy queued behind the moment
-// chunks' host-to-device copies)
-__global__ void k_stream_scan(const unsigned* __restrict__ cnt, int n_chunks, unsigned* __restrict__ bounds,
-                              unsigned* __restrict__ cursor, unsigned* host_bounds) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int s = 0; s < 2; ++s) {
-    unsigned acc = 0;
-    for (int c = 0; c < n_chunks; ++c) {
-      bounds[s * (n_chunks + 1) + c] = acc;
-      if (host_bounds) host_bounds[s * (n_chunks + 1) + c] = acc;
-      cursor[s * n_chunks + c] = acc;
-      acc += cnt[s * n_chunks + c];
-    }
-    bounds[s * (n_chunks + 1) + n_chunks] = acc;
-    if (host_bounds) host_bounds[s * (n_chunks + 1) + n_chunks] = acc;
-  }
-  __threadfence_system();
-}
-
-// Per-chunk leaf lists: each block reserves one contiguous range per key in
-// the global buckets, its leaves take warp-aggregated slots inside it.
+// Per-chunk leaf lists: bucket starts = exclusive scans of the two count
+// sets (every block computes them; block 0 also stores the bounds the chunk
+// kernels read: bounds[0..C] P2M, bounds[C+1..2C+1] P2P); each block
+// reserves one contiguous range per key inside the buckets, its leaves take
+// warp-aggregated slots inside it.
 __global__ void __launch_bounds__(256) k_stream_lists(const unsigned char* __restrict__ ready, unsigned n_leaves,
-                                                      int n_chunks, unsigned* __restrict__ cursor,
+                                                      int n_chunks, const unsigned* __restrict__ cnt,
+                                                      unsigned* __restrict__ cursor, unsigned* __restrict__ bounds,
                                                       unsigned* __restrict__ list_p2m,
                                                       unsigned* __restrict__ list_p2p) {
   __shared__ unsigned s_cnt[2 * kMaxStreamChunks], s_base[2 * kMaxStreamChunks];
-  if (threadIdx.x < 2 * kMaxStreamChunks) s_cnt[threadIdx.x] = 0;
+  const int tid = threadIdx.x;
+  if (tid < 2 * kMaxStreamChunks) s_cnt[tid] = 0;
+  if (tid < 2 * n_chunks) {
+    const int set = tid / n_chunks, c = tid - set * n_chunks;
+    unsigned start = 0;
+    for (int j = 0; j < c; ++j) start += cnt[set * n_chunks + j];
+    s_base[tid] = start;
+    if (blockIdx.x == 0) {
+      bounds[set * (n_chunks + 1) + c] = start;
+      if (c == n_chunks - 1) bounds[set * (n_chunks + 1) + n_chunks] = start + cnt[tid];
+    }
+  }
   __syncthreads();
-  const unsigned m = blockIdx.x * 256 + threadIdx.x;
+  const unsigned m = blockIdx.x * 256 + tid;
   const bool ok = m < n_leaves;
   const unsigned k0 = ok ? ready[2 * m] : ~0u;
   const unsigned k1 = ok ? n_chunks + ready[2 * m + 1] : ~0u;
   const unsigned s0 = warp_slot(k0, s_cnt);
   const unsigned s1 = warp_slot(k1, s_cnt);
   __syncthreads();
-  if (threadIdx.x < 2 * n_chunks)
-    s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]) : 0u;
+  if (tid < 2 * n_chunks && s_cnt[tid]) s_base[tid] += atomicAdd(&cursor[tid], s_cnt[tid]);
   __syncthreads();
   if (!ok) return;
   list_p2m[s_base[k0] + s0] = m;
@@ -456,25 +568,35 @@ void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, c
 
 void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
                 double inv_side, int n_axis, unsigned* keys, unsigned* idx, unsigned* counts,
-                DevResult* res, cudaStream_t st, const unsigned char* need) {
-  if (n == 0) return;
-  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
-  k_bin<<<blocks, 256, 0, st>>>(pos, src, n, box_radius, inv_side, n_axis, keys, idx, counts, need, res);
+                DevResult* res, cudaStream_t st, const unsigned char* need, std::size_t i0, std::size_t i1,
+                unsigned* leafmax) {
+  i1 = std::min(i1, n);
+  if (i1 <= i0) return;  // i0: a multiple of 256
+  const unsigned blocks = static_cast<unsigned>((i1 - i0 + 255) / 256);
+  k_bin<<<blocks, 256, 0, st>>>(pos, src, i1, box_radius, inv_side, n_axis, keys, idx, counts, need, res,
+                                static_cast<unsigned>(i0 / 256), leafmax);
 }
 
-void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
+std::size_t scan_tiles(std::size_t n) { return (n + kScanTile - 1) / kScanTile; }
+
+void launch_scan(const unsigned* in, unsigned* out, std::size_t n, ScanWork w, cudaStream_t st) {
+  if (n == 0) return;
+  k_scan<<<static_cast<unsigned>(scan_tiles(n)), kScanThreads, 0, st>>>(in, out, static_cast<unsigned>(n),
+                                                                         w.status, w.ctr);
+}
+
+void launch_bucket_gather(ScanWork scan, const double* pos, const double* src,
                           const unsigned* keys, const unsigned* slots, const unsigned* counts,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
                           unsigned* sorted, std::size_t n, int n_leaves,
                           const unsigned char* need, double* part, cudaStream_t st,
-                          bool check_src, DevResult* res, unsigned* leaf_mp) {
-  std::size_t bytes = temp_bytes;
-  cub::DeviceScan::ExclusiveSum(temp, bytes, counts, offsets, n_leaves + 1, st);
+                          bool check_src, DevResult* res, unsigned* leaf_mp, unsigned* inv) {
+  launch_scan(counts, offsets, static_cast<std::size_t>(n_leaves) + 1, scan, st);
   if (n == 0) return;
   k_scatter<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, slots, offsets, n,
                                                                     unsorted);
   k_leaf_gather<<<static_cast<unsigned>(n_leaves), kLeafThreads, 0, st>>>(
-      pos, src, offsets, unsorted, scratch, sorted, need, part, check_src && part != nullptr, res, leaf_mp);
+      pos, src, offsets, unsorted, scratch, sorted, need, part, check_src && part != nullptr, res, leaf_mp, inv);
 }
 
 void launch_src_gather(const double* pos, const double* src, const unsigned* sorted,
@@ -495,45 +617,33 @@ void launch_src_chunk(const double* pos, const double* src, const unsigned* inv,
                                       leaf_mp);
 }
 
-void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,
-                           int periodic, unsigned chunk, int n_chunks, unsigned* inv,
-                           unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
-                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st, unsigned* host_bounds,
-                           cudaEvent_t after_inverse) {
+void launch_stream_lists(const unsigned* leafmax, int depth, int periodic, const StreamChunks& ch,
+                         unsigned char* ready, unsigned* cnt_cursor, unsigned* bounds, unsigned* list_p2m,
+                         unsigned* list_p2p, cudaStream_t st) {
   const unsigned n_leaves = 1u << (3 * depth);
-  if (n > 0) k_inverse<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(sorted, n, inv);
-  if (after_inverse) cudaEventRecord(after_inverse, st);  // the chunk gathers need only `inv`
-  cudaMemsetAsync(cnt, 0, 2 * n_chunks * sizeof(unsigned), st);
-  k_stream_ready<<<(n_leaves + 255) / 256, 256, 0, st>>>(offsets, sorted, depth, periodic, chunk,
-                                                        n_chunks, ready, cnt);
-  k_stream_scan<<<1, 32, 0, st>>>(cnt, n_chunks, bounds, cursor, host_bounds);
-  k_stream_lists<<<(n_leaves + 255) / 256, 256, 0, st>>>(ready, n_leaves, n_chunks, cursor, list_p2m,
+  cudaMemsetAsync(cnt_cursor, 0, 4 * kMaxStreamChunks * sizeof(unsigned), st);
+  k_stream_ready<<<(n_leaves + 255) / 256, 256, 0, st>>>(leafmax, depth, periodic, ch, ready, cnt_cursor);
+  k_stream_lists<<<(n_leaves + 255) / 256, 256, 0, st>>>(ready, n_leaves, ch.n, cnt_cursor,
+                                                        cnt_cursor + 2 * kMaxStreamChunks, bounds, list_p2m,
                                                         list_p2p);
 }
 
-std::size_t sort_temp_bytes(std::size_t n, int n_leaves) {
-  std::size_t a = 0, b = 0;
+std::size_t sort_temp_bytes(std::size_t n) {
+  std::size_t a = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const unsigned*>(nullptr),
                                   static_cast<unsigned*>(nullptr),
                                   static_cast<const unsigned*>(nullptr),
                                   static_cast<unsigned*>(nullptr), static_cast<int>(n), 0, 32);
-  cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const unsigned*>(nullptr),
-                                static_cast<unsigned*>(nullptr), n_leaves + 1);
-  return (a > b ? a : b) + 256;
+  return a + 256;
 }
 
+// validation path only (validate_only: no tree, duplicates by a radix sort)
 void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
-                 const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
-                 const unsigned* counts, unsigned* offsets, int n_leaves, cudaStream_t st) {
-  if (n > 0) {
-    std::size_t bytes = temp_bytes;
-    cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out, idx_in, idx_out,
-                                    static_cast<int>(n), 0, end_bit > 0 ? end_bit : 1, st);
-  }
-  if (counts) {
-    std::size_t bytes = temp_bytes;
-    cub::DeviceScan::ExclusiveSum(temp, bytes, counts, offsets, n_leaves + 1, st);
-  }
+                 const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit, cudaStream_t st) {
+  if (n == 0) return;
+  std::size_t bytes = temp_bytes;
+  cub::DeviceRadixSort::SortPairs(temp, bytes, keys_in, keys_out, idx_in, idx_out, static_cast<int>(n), 0,
+                                  end_bit > 0 ? end_bit : 1, st);
 }
 
 }  // namespace ankh_b200

@@ -597,6 +597,11 @@ void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int ord
 #define ANKH_P2M(N) \
   p2m_order<N>(part, leaf_off, depth, box_radius, hd, exp_leaf, res, self_leaf, xi, m_begin, m_end, list, \
                bounds, list_count, st)
+  if (order > 10) {  // runtime-order kernel (k_generic.cu); no list mode (streamed path is L <= 6)
+    if (!list) launch_p2m_generic(part, leaf_off, depth, order, box_radius, hd, exp_leaf, self_leaf, xi, m_begin,
+                                  m_end, st);
+    return;
+  }
   ANKH_ORDER_SWITCH(order, ANKH_P2M)
 #undef ANKH_P2M
 }

@@ -71,10 +71,12 @@ constexpr int kPerThreads = 256;
 __global__ void __launch_bounds__(kPerThreads) k_periodic_eval(const double* __restrict__ root,
                                                                const double* __restrict__ T,
                                                                const double* __restrict__ spec_re,
-                                                               int L, double* __restrict__ out) {
+                                                               int L, double* __restrict__ out,
+                                                               double* __restrict__ gbuf) {
   extern __shared__ double sm[];
   const int eb = 2 * L - 1, L2 = L * L, K = L2 * L;
-  double* v = sm;                 // K   (root, then scratch)
+  // working set in shared memory, or (large orders) in a global scratch
+  double* v = gbuf ? gbuf : sm;   // K   (root, then scratch)
   double* t1 = v + K;             // K
   double* t2 = t1 + K;            // K
   double* tw_c = t2 + K;          // eb twiddles
@@ -268,14 +270,27 @@ void launch_periodic_gen(double* gen, int order, double box_radius, double xi, i
   k_periodic_gen<<<eb * eb * eb, 256, 0, st>>>(gen, order, box_radius, xi, p);
 }
 
+namespace {
+constexpr std::size_t kPerSmemMax = 200 * 1024;
+std::size_t periodic_eval_doubles(int L) {
+  const std::size_t eb = 2 * L - 1, K = static_cast<std::size_t>(L) * L * L;
+  return 3 * K + 2 * eb + 2 * K + 2 * L * eb * L + kPerThreads;
+}
+}  // namespace
+
+std::size_t periodic_eval_scratch_doubles(int order) {
+  const std::size_t d = periodic_eval_doubles(order);
+  return d * sizeof(double) <= kPerSmemMax ? 0 : d;
+}
+
 void launch_periodic_eval(const double* root, const double* to_equi, const double* spec_re,
-                          int order, double* out, cudaStream_t st) {
-  const int L = order, eb = 2 * L - 1, K = L * L * L;
-  const std::size_t smem =
-      sizeof(double) * (3 * K + 2 * eb + 2 * K + 2 * L * eb * L + kPerThreads);
+                          int order, double* out, cudaStream_t st, double* scratch) {
+  const int L = order;
+  const bool global = periodic_eval_scratch_doubles(L) != 0;
+  const std::size_t smem = global ? 0 : sizeof(double) * periodic_eval_doubles(L);
   static std::atomic<unsigned long long> attr{0};
-  smem_opt_in(attr, k_periodic_eval, 200 * 1024);
-  k_periodic_eval<<<1, kPerThreads, smem, st>>>(root, to_equi, spec_re, L, out);
+  smem_opt_in(attr, k_periodic_eval, kPerSmemMax);
+  k_periodic_eval<<<1, kPerThreads, smem, st>>>(root, to_equi, spec_re, L, out, global ? scratch : nullptr);
 }
 
 void launch_finalize(const double* near_partial, int n_near, const unsigned long long* pair_count,

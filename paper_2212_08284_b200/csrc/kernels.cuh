@@ -92,6 +92,12 @@ enum RedSlot {
 
 // streamed host path: at most this many moment chunks (per-chunk leaf lists)
 constexpr int kMaxStreamChunks = 32;
+/// Streamed host path: chunk c holds particles [start[c], start[c + 1]),
+/// c < n; starts are multiples of 256 (k_bin's block layout).
+struct StreamChunks {
+  unsigned start[kMaxStreamChunks + 1];
+  int n;
+};
 
 struct DevResult {
   double red[kRedCount];
@@ -116,13 +122,24 @@ struct M2LOp {
 };
 
 // ---- launchers (defined in the .cu files) ----
+/// Particles [i0, min(i1, n)) (i0 a multiple of 256): keys, leaf histogram
+/// (counts) with arrival slots in idx, position flags; leafmax (optional,
+/// zeroed): each leaf's largest particle index.
 void launch_bin(const double* pos, const double* src, std::size_t n, double box_radius,
                 double inv_side, int n_axis, unsigned* keys, unsigned* idx, unsigned* counts,
-                DevResult* res, cudaStream_t st, const unsigned char* need = nullptr);
-std::size_t sort_temp_bytes(std::size_t n, int n_leaves);
+                DevResult* res, cudaStream_t st, const unsigned char* need = nullptr, std::size_t i0 = 0,
+                std::size_t i1 = ~std::size_t{0}, unsigned* leafmax = nullptr);
+/// Single-pass exclusive scan (k_bin.cu k_scan): the state -- scan_tiles(n)
+/// status words and two counters -- is zeroed once and resets itself.
+struct ScanWork {
+  unsigned long long* status;
+  unsigned* ctr;
+};
+std::size_t scan_tiles(std::size_t n);
+void launch_scan(const unsigned* in, unsigned* out, std::size_t n, ScanWork w, cudaStream_t st);
+std::size_t sort_temp_bytes(std::size_t n);
 void launch_sort(void* temp, std::size_t temp_bytes, const unsigned* keys_in, unsigned* keys_out,
-                 const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit,
-                 const unsigned* counts, unsigned* offsets, int n_leaves, cudaStream_t st);
+                 const unsigned* idx_in, unsigned* idx_out, std::size_t n, int end_bit, cudaStream_t st);
 /// hd[n] = H D^n, n = 0..2 (3 x L x L, host order) into the P2M constant bank.
 void upload_p2m_basis(int order, const double* hd, cudaStream_t st);
 // list != nullptr (L <= 6 only): the leaves list[bounds[0] .. bounds[1]),
@@ -138,14 +155,13 @@ void launch_p2m(const double* part, const unsigned* leaf_off, int depth, int ord
 void launch_src_chunk(const double* pos, const double* src, const unsigned* inv, std::size_t i0,
                       std::size_t i1, DevResult* res, double* part, cudaStream_t st,
                       const unsigned* keys = nullptr, unsigned* leaf_mp = nullptr);
-// inverse permutation, per-leaf readiness chunk (P2M: own records; P2P: + the
-// 13 half-shell neighbours), per-chunk leaf lists and their bounds
-// (bounds[0..C] P2M, bounds[C+1..2C+1] P2P)
-void launch_stream_prepare(const unsigned* offsets, const unsigned* sorted, std::size_t n, int depth,
-                           int periodic, unsigned chunk, int n_chunks, unsigned* inv,
-                           unsigned char* ready, unsigned* cnt, unsigned* bounds, unsigned* cursor,
-                           unsigned* list_p2m, unsigned* list_p2p, cudaStream_t st,
-                           unsigned* host_bounds = nullptr, cudaEvent_t after_inverse = nullptr);
+// per-leaf readiness chunk (P2M: own records; P2P: + the 13 half-shell
+// neighbours) from each leaf's largest particle index (launch_bin leafmax),
+// per-chunk leaf lists and their bounds (bounds[0..C] P2M, bounds[C+1..2C+1]
+// P2P); cnt_cursor: 4 kMaxStreamChunks uints of scratch
+void launch_stream_lists(const unsigned* leafmax, int depth, int periodic, const StreamChunks& ch,
+                         unsigned char* ready, unsigned* cnt_cursor, unsigned* bounds, unsigned* list_p2m,
+                         unsigned* list_p2p, cudaStream_t st);
 /// The upward pass (M2M) in one launch: parents [p_begin, p_begin + p_count)
 /// of level `first` (Morton; p_count 0: all), then every coarser level down
 /// to `top`, each cell by the last of its children's CTAs to finish.
@@ -177,12 +193,25 @@ int launch_p2p(const double* part, const unsigned* leaf_off, const unsigned* lea
                double period, double xi, const P2PRadial& rad, int cap, int leaf_begin,
                int leaf_end, double* near_partial, unsigned long long* pair_count, DevResult* res,
                cudaStream_t st, const unsigned* list = nullptr, const unsigned* bounds = nullptr,
-               int list_grid = 0);
+               int list_grid = 0, unsigned* work = nullptr);
 int p2p_max_cap();
 void launch_periodic_gen(double* gen, int order, double box_radius, double xi, int p,
                          cudaStream_t st);
+/// scratch: periodic_eval_scratch_doubles(order) doubles when nonzero (the
+/// working set past the shared-memory size)
 void launch_periodic_eval(const double* root, const double* to_equi, const double* spec_re,
-                          int order, double* out, cudaStream_t st);
+                          int order, double* out, cudaStream_t st, double* scratch = nullptr);
+std::size_t periodic_eval_scratch_doubles(int order);
+// Runtime-order P2M / M2M (k_generic.cu) for orders past the compiled ones
+constexpr unsigned kM2MGenGlobalCtas = 148;
+void launch_p2m_generic(const double* part, const unsigned* leaf_off, int depth, int order, double box_radius,
+                        const double* hd, double* exp_leaf, double* self_leaf, double xi, unsigned m_begin,
+                        unsigned m_end, cudaStream_t st);
+std::size_t m2m_generic_scratch_doubles(int order);
+/// h_level_off: the host copy of the level offsets
+void launch_m2m_generic(double* exp, const long long* h_level_off, int first, int top, int order,
+                        const double* m2m, double* scratch, cudaStream_t st, unsigned p_begin = 0,
+                        unsigned p_count = 0);
 void launch_finalize(const double* near_partial, int n_near, const unsigned long long* pair_count,
                      int n_count, const double* far_partial, int n_far, const double* self_partial,
                      int n_self, double self_scale, const double* periodic, int use_periodic,
@@ -203,12 +232,14 @@ void launch_init_result(DevResult* res, cudaStream_t st, int any_multipole = 0,
 /// (optional, per lex leaf): only those leaves are sorted and gathered;
 /// part == nullptr: sort only.  launch_bin with src == nullptr bins and
 /// validates positions only.
-void launch_bucket_gather(void* temp, std::size_t temp_bytes, const double* pos, const double* src,
+/// inv (optional): inv[sorted[j]] = j, the sorted slot of every particle.
+void launch_bucket_gather(ScanWork scan, const double* pos, const double* src,
                           const unsigned* keys, const unsigned* slots, const unsigned* counts,
                           unsigned* offsets, unsigned* unsorted, unsigned* scratch,
                           unsigned* sorted, std::size_t n, int n_leaves,
                           const unsigned char* need, double* part, cudaStream_t st,
-                          bool check_src = false, DevResult* res = nullptr, unsigned* leaf_mp = nullptr);
+                          bool check_src = false, DevResult* res = nullptr, unsigned* leaf_mp = nullptr,
+                          unsigned* inv = nullptr);
 double probe_fp64_tflops(int iters);
 /// ms of k_mix<mode> (k_probe.cu): DFMA-only, DMMA-only, or half/half warps
 double probe_fp64_mix_ms(int mode, int it_f, int it_m);

@@ -38,7 +38,8 @@ void validate_config(const ankh_config_v1& c) {
 
 namespace {
 constexpr double kInvSqrtPi = 0.5641895835477562869;
-constexpr int kMaxOrderGpu = 10;
+constexpr int kMaxOrderGpu = 64;     // L > kMaxOrderCompiled: runtime-order P2M / M2M (k_generic.cu)
+constexpr int kMaxOrderCompiled = 10;
 
 int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 
@@ -77,7 +78,7 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
     pending_msg_ = "DiffOperator: order out of range";
   } else if (L > kMaxOrderGpu) {
     pending_code_ = ANKH_RUNTIME_ERROR;
-    pending_msg_ = "order_cheb > 10 is not supported by the B200 engine";
+    pending_msg_ = "order_cheb > 64 is not supported by the B200 engine";
   }
   ANKH_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   // The far chain (P2M -> exchange -> M2M -> M2L) and the streamed path's
@@ -145,6 +146,7 @@ Plan::~Plan() {
     if (s) cudaStreamSynchronize(s);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_src_exec_) cudaGraphExecDestroy(graph_src_exec_);
+  if (sgraph_exec_) cudaGraphExecDestroy(sgraph_exec_);
   for (void* p : allocs_) cudaFreeAsync(p, stream_);  // back to the pool (kept for the next plan)
   if (stream_) cudaStreamSynchronize(stream_);
   if (h_res_) cudaFreeHost(h_res_);
@@ -166,13 +168,14 @@ Plan::~Plan() {
       cudaStreamSynchronize(s);
       cudaStreamDestroy(s);
     }
-  for (cudaEvent_t e : {ev_s_start_, ev_s_pos_, ev_s_sorted_, ev_s_inv_, ev_s_p2p2_})
+  for (cudaEvent_t e : {ev_s_start_, ev_s_binned_, ev_s_lists_, ev_s_sorted_, ev_s_inv_, ev_s_p2p2_})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_t_)
     if (e) cudaEventDestroy(e);
   for (int c = 0; c < kMaxStreamChunks; ++c) {
     if (ev_s_chunk_[c]) cudaEventDestroy(ev_s_chunk_[c]);
     if (ev_s_gath_[c]) cudaEventDestroy(ev_s_gath_[c]);
+    if (ev_s_posc_[c]) cudaEventDestroy(ev_s_posc_[c]);
   }
   if (p2p_stream2_) {
     cudaStreamSynchronize(p2p_stream2_);
@@ -279,7 +282,15 @@ void Plan::allocate() {
   d_keys2_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
   d_idx_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
   d_idx2_ = static_cast<unsigned*>(dalloc(nn * sizeof(unsigned)));
-  d_counts_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
+  // leaf histogram, then (streamed path) each leaf's largest particle index
+  d_counts_ = static_cast<unsigned*>(dalloc(2 * (n_leaves + 1) * sizeof(unsigned)));
+  d_leafmax_ = d_counts_ + (n_leaves + 1);
+  {
+    const std::size_t tiles = scan_tiles(static_cast<std::size_t>(n_leaves) + 1);
+    scan_.status = static_cast<unsigned long long*>(dalloc(tiles * sizeof(unsigned long long) + 16));
+    scan_.ctr = reinterpret_cast<unsigned*>(scan_.status + tiles);
+    ANKH_CUDA(cudaMemsetAsync(scan_.status, 0, tiles * sizeof(unsigned long long) + 16, stream_));
+  }
   d_off_ = static_cast<unsigned*>(dalloc((n_leaves + 1) * sizeof(unsigned)));
   d_leaf_mp_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
   ANKH_CUDA(cudaMemsetAsync(d_leaf_mp_, 0, static_cast<std::size_t>(n_leaves) * sizeof(unsigned), stream_));
@@ -318,7 +329,7 @@ void Plan::allocate() {
     ANKH_CUDA(cudaMemcpyAsync(d_need_, need.data(), need.size(), cudaMemcpyHostToDevice, stream_));
     ANKH_CUDA(cudaStreamSynchronize(stream_));
   }
-  temp_bytes_ = sort_temp_bytes(nn, n_leaves);
+  temp_bytes_ = sort_temp_bytes(nn);
   d_temp_ = dalloc(temp_bytes_);
   d_part_ = static_cast<double*>(dalloc(nn * kRec * sizeof(double)));
   level_off_.assign(depth + 2, 0);
@@ -338,6 +349,9 @@ void Plan::allocate() {
   d_pair_count_ = static_cast<unsigned long long*>(
       dalloc(std::max(leaf_end_ - leaf_begin_, 1) * sizeof(unsigned long long)));
   d_per_ = static_cast<double*>(dalloc(sizeof(double)));
+  if (const std::size_t ps = periodic_eval_scratch_doubles(L)) d_per_scratch_ = static_cast<double*>(dalloc(ps * sizeof(double)));
+  if (L > kMaxOrderCompiled)
+    if (const std::size_t ms = m2m_generic_scratch_doubles(L)) d_m2m_scratch_ = static_cast<double*>(dalloc(ms * sizeof(double)));
   d_res_ = static_cast<DevResult*>(dalloc(sizeof(DevResult)));
   d_res_pos_ = static_cast<DevResult*>(dalloc(sizeof(DevResult)));
   ANKH_CUDA(cudaMallocHost(&h_res_, sizeof(DevResult)));
@@ -743,11 +757,20 @@ void Plan::validate_only(const double* d_pos, const double* d_src, cudaStream_t 
   const int nax8 = 256;  // depth-8 bins keep the duplicate scan local
   const double inv_side = nax8 / (2.0 * rb);
   launch_bin(d_pos, d_src, n, rb, inv_side, nax8, d_keys_, d_idx_, nullptr, d_res_, st);
-  launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 24, nullptr, nullptr,
-              0, st);
+  launch_sort(d_temp_, temp_bytes_, d_keys_, d_keys2_, d_idx_, d_idx2_, n, 24, st);
   launch_dup_check(d_keys2_, d_idx2_, d_pos, n, d_res_, st);
   ANKH_CUDA(cudaMemcpyAsync(h_res_, d_res_, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
   launches_ = 3;
+}
+
+// the upward pass for parent levels first .. top (whole subtrees from
+// p_begin): the chained one-launch kernel for the compiled orders, per-level
+// runtime-order launches past them
+void Plan::launch_m2m(int first, int top, cudaStream_t st, unsigned p_begin, unsigned p_count) {
+  if (L <= kMaxOrderCompiled)
+    launch_m2m_chain(d_exp_, d_level_off_, first, top, L, d_m2m_, d_m2m_cnt_, st, p_begin, p_count);
+  else
+    launch_m2m_generic(d_exp_, level_off_.data(), first, top, L, d_m2m_, d_m2m_scratch_, st, p_begin, p_count);
 }
 
 void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st, int mode) {
@@ -780,7 +803,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
     }
     // counting sort by leaf: d_idx_ holds the arrival slots, d_keys2_ the
     // scattered indices, d_idx2_ the leaf CSR's ascending indices
-    launch_bucket_gather(d_temp_, temp_bytes_, d_pos, d_src, d_keys_, d_idx_, d_counts_, d_off_,
+    launch_bucket_gather(scan_, d_pos, d_src, d_keys_, d_idx_, d_counts_, d_off_,
                          d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, d_part_, st, gather_src, d_res_,
                          d_leaf_mp_);
     launches += 2;
@@ -818,7 +841,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   if (mode == 0 || mode == 3) launches += exchange_upward(far);
   if (serial) {
     if (m2m_top_ >= 0) {
-      launch_m2m_chain(d_exp_, d_level_off_, m2m_top_, 0, L, d_m2m_, d_m2m_cnt_, far);
+      launch_m2m(m2m_top_, 0, far);
       ++launches;
     }
     if (timing) ANKH_CUDA(cudaEventRecord(ev_[2], st));
@@ -844,7 +867,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
   ++launches;
   if (timing) ANKH_CUDA(cudaEventRecord(ev_[4], st));
   if (serial && do_periodic) {
-    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, st);
+    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, st, d_per_scratch_);
     ++launches;
   }
   if (!serial) ANKH_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
@@ -896,14 +919,14 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
   };
   auto m2m = [&](cudaStream_t s) {
     if (m2m_top_ < 0) return;  // (levels below m2m_top_ are done by exchange_upward)
-    launch_m2m_chain(d_exp_, d_level_off_, m2m_top_, 0, L, d_m2m_, d_m2m_cnt_, s);
+    launch_m2m(m2m_top_, 0, s);
     ++launches;
   };
   if (!fork) {
     m2m(far);
     for (int c : cls) m2l(c, class_range_[c].first, class_range_[c].second, far);
     if (with_periodic) {
-      launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, far);
+      launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, far, d_per_scratch_);
       ++launches;
     }
     return launches;
@@ -957,7 +980,7 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
   if (with_periodic) {
     const int k = pick(0);
     after(k);
-    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, lane[k]);
+    launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, lane[k], d_per_scratch_);
     ++launches;
   }
   for (int k = 1; k <= kM2LStreams; ++k)
@@ -1047,8 +1070,7 @@ std::uint32_t Plan::exchange_upward(cudaStream_t st) {
   const long long G = cfg.world, r = cfg.rank;
   if (depth - 1 >= exch_level_) {  // this shard's subtrees, parent levels depth-1 .. exch_level_
     const long long cells = 1ll << (3 * (depth - 1));
-    launch_m2m_chain(d_exp_, d_level_off_, depth - 1, exch_level_, L, d_m2m_, d_m2m_cnt_, st,
-                     static_cast<unsigned>(cells * r / G), static_cast<unsigned>(cells / G));
+    launch_m2m(depth - 1, exch_level_, st, static_cast<unsigned>(cells * r / G), static_cast<unsigned>(cells / G));
     ++launches;
   }
   std::vector<double*> recv;
@@ -1139,8 +1161,8 @@ void Plan::stream_setup() {
     stream_chunks_ = std::max(1, std::min(stream_chunks_, kMaxStreamChunks));
     d_inv_ = static_cast<unsigned*>(dalloc(n * sizeof(unsigned)));
     d_ready_ = static_cast<unsigned char*>(dalloc(2 * static_cast<std::size_t>(n_leaves)));
-    d_scnt_ = static_cast<unsigned*>(dalloc(2 * kMaxStreamChunks * sizeof(unsigned)));
-    d_scursor_ = static_cast<unsigned*>(dalloc(2 * kMaxStreamChunks * sizeof(unsigned)));
+    // list counts, list cursors, P2P work counters (kMaxStreamChunks each; 2, 2, 1)
+    d_scnt_ = static_cast<unsigned*>(dalloc(5 * kMaxStreamChunks * sizeof(unsigned)));
     d_sbounds_ = static_cast<unsigned*>(dalloc(2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
     d_list_p2m_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
     d_list_p2p_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
@@ -1148,42 +1170,139 @@ void Plan::stream_setup() {
     ANKH_CUDA(cudaStreamCreateWithFlags(&p2p_stream2_, cudaStreamNonBlocking));
     ANKH_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
     ANKH_CUDA(cudaStreamCreateWithPriority(&gather_stream_, cudaStreamNonBlocking, hi_prio_));
-    for (cudaEvent_t* e : {&ev_s_start_, &ev_s_pos_, &ev_s_sorted_, &ev_s_inv_, &ev_s_p2p2_})
+    for (cudaEvent_t* e : {&ev_s_start_, &ev_s_binned_, &ev_s_lists_, &ev_s_sorted_, &ev_s_inv_, &ev_s_p2p2_})
       ANKH_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (int c = 0; c < kMaxStreamChunks; ++c) {
       ANKH_CUDA(cudaEventCreateWithFlags(&ev_s_chunk_[c], cudaEventDisableTiming));
       ANKH_CUDA(cudaEventCreateWithFlags(&ev_s_gath_[c], cudaEventDisableTiming));
+      ANKH_CUDA(cudaEventCreateWithFlags(&ev_s_posc_[c], cudaEventDisableTiming));
     }
+    // chunk schedules in whole 256-particle blocks (k_bin's block layout):
+    // the moments' first chunk is half a regular one (the evaluation starts
+    // as soon as it lands), the rest equal; positions in equal chunks
+    if (const char* c = std::getenv("ANKH_STREAM_POS_CHUNKS")) stream_pos_chunks_ = std::atoi(c);
+    stream_pos_chunks_ = std::max(1, std::min(stream_pos_chunks_, kMaxStreamChunks));
+    const std::size_t blocks = (n + 255) / 256;
+    auto schedule = [&](int C, double first) {
+      StreamChunks ch{};
+      std::vector<std::size_t> b(1, 0);
+      const double w0 = first / (first + (C - 1));
+      if (C > 1) b.push_back(std::max<std::size_t>(1, static_cast<std::size_t>(w0 * blocks + 0.5)));
+      for (int c = static_cast<int>(b.size()); c < C; ++c) {
+        const std::size_t rest = blocks - b[1];
+        b.push_back(b[1] + (rest * (c - 1) + (C - 2)) / (C - 1));
+      }
+      b.push_back(blocks);
+      for (std::size_t c = 0; c + 1 < b.size(); ++c)
+        if (b[c + 1] > b[c]) ch.start[ch.n++] = static_cast<unsigned>(std::min(n, 256 * b[c]));
+      ch.start[ch.n] = static_cast<unsigned>(n);
+      return ch;
+    };
+    double first = 0.5;
+    if (const char* f = std::getenv("ANKH_STREAM_FIRST")) first = std::atof(f);
+    sch_ = schedule(stream_chunks_, first);
+    pch_ = schedule(stream_pos_chunks_, 1.0);
     for (auto& e : ev_t_) ANKH_CUDA(cudaEventCreate(&e));
     ANKH_CUDA(cudaStreamSynchronize(stream_));  // pool allocations complete before other streams use them
     stream_init_ = true;
   }
 }
 
-// positions half of the streamed path: validation, binning, per-leaf sort
-// (build_tree, as set_positions) and the per-chunk leaf lists; their bounds
-// stay on the device (the chunk kernels read them there); `after_inverse` is
-// recorded once the inverse permutation -- all the chunk gathers need -- is in
-void Plan::stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C,
+// positions half of the streamed path: validation and binning of each
+// positions chunk as it lands (pos_ev; nullptr: all in), then the per-leaf
+// sort (build_tree, as set_positions) with the inverse permutation on `st`,
+// and -- beside it on side_stream_ -- the per-chunk leaf lists (their bounds
+// stay on the device: the chunk kernels read them there).  `after_inverse`
+// is recorded once the inverse permutation -- all the chunk gathers need --
+// is in; on return `st` has also joined the lists.
+void Plan::stream_positions(cudaStream_t st, DevResult* res, const cudaEvent_t* pos_ev,
                             const std::function<void(const std::string&)>& mark, cudaEvent_t after_inverse) {
-  launch_init_result(res, st, 0, d_counts_, static_cast<unsigned>(n_leaves + 1));
+  launch_init_result(res, st, 0, d_counts_, static_cast<unsigned>(2 * (n_leaves + 1)));
   const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
-  launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, res, st);
+  for (int p = 0; p < pch_.n; ++p) {
+    if (pos_ev) ANKH_CUDA(cudaStreamWaitEvent(st, pos_ev[p], 0));
+    launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, res, st, nullptr, pch_.start[p],
+               pch_.start[p + 1], d_leafmax_);
+  }
   if (mark) mark("  binned");
-  launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_, d_off_, d_keys2_,
-                       d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
-  if (mark) mark("  leaf CSR");
-  launch_stream_prepare(d_off_, d_idx2_, n, depth, periodic ? 1 : 0, static_cast<unsigned>(chunk), C, d_inv_,
-                        d_ready_, d_scnt_, d_sbounds_, d_scursor_, d_list_p2m_, d_list_p2p_, st, nullptr,
-                        after_inverse);
+  ANKH_CUDA(cudaEventRecord(ev_s_binned_, st));
+  ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_binned_, 0));
+  launch_stream_lists(d_leafmax_, depth, periodic ? 1 : 0, sch_, d_ready_, d_scnt_, d_sbounds_, d_list_p2m_,
+                      d_list_p2p_, side_stream_);
+  ANKH_CUDA(cudaEventRecord(ev_s_lists_, side_stream_));
+  launch_bucket_gather(scan_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_, d_off_, d_keys2_, d_idx_, d_idx2_, n,
+                       n_leaves, nullptr, nullptr, st, false, nullptr, nullptr, d_inv_);
+  if (after_inverse) ANKH_CUDA(cudaEventRecord(after_inverse, st));
+  if (mark) mark("  leaf CSR + inverse");
+  ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_lists_, 0));
 }
 
-std::size_t Plan::stream_chunk_size() const {
-  // chunks of whole 256-particle blocks (k_bin's self-energy partial layout)
-  return ((n + stream_chunks_ - 1) / stream_chunks_ + 255) / 256 * 256;
+namespace {
+bool page_locked(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
 }
+}  // namespace
 
 void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream_t st) {
+  // Repeated calls on the same page-locked host buffers replay a graph of the
+  // whole streamed evaluation (its copies read the buffers' current
+  // contents); pageable buffers, traces and phase timing launch directly.
+  const bool graphable = !cfg.phase_timing && std::getenv("ANKH_STREAM_TRACE") == nullptr &&
+                         std::getenv("ANKH_STREAM_NO_GRAPH") == nullptr && page_locked(h_pos) &&
+                         page_locked(h_src);
+  if (!graphable) {
+    enqueue_streamed_launch(h_pos, h_src, st);
+    return;
+  }
+  auto replayed = [&]() {  // host state an evaluation leaves behind
+    last_stream_ = st;
+    evaluated_ = true;
+    if (h_pos) bound_ = stream_bound_ = false;
+    streamed_last_ = true;
+    launches_ = sgraph_launches_;
+  };
+  if (sgraph_exec_ && sgraph_pos_ == h_pos && sgraph_src_ == h_src) {
+    ANKH_CUDA(cudaGraphLaunch(sgraph_exec_, st));
+    replayed();
+    return;
+  }
+  if (sgraph_warm_ && sgraph_warm_pos_ == h_pos && sgraph_warm_src_ == h_src) {
+    if (sgraph_exec_) {
+      cudaGraphExecDestroy(sgraph_exec_);
+      sgraph_exec_ = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    ANKH_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_streamed_launch(h_pos, h_src, st);
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    ANKH_CUDA(cudaStreamEndCapture(st, &g));
+    const cudaError_t e = cudaGraphInstantiate(&sgraph_exec_, g, cudaGraphInstantiateFlagUseNodePriority);
+    cudaGraphDestroy(g);
+    ANKH_CUDA(e);
+    sgraph_pos_ = h_pos;
+    sgraph_src_ = h_src;
+    sgraph_launches_ = launches_;
+    ANKH_CUDA(cudaGraphLaunch(sgraph_exec_, st));
+    return;
+  }
+  sgraph_warm_ = true;
+  sgraph_warm_pos_ = h_pos;
+  sgraph_warm_src_ = h_src;
+  enqueue_streamed_launch(h_pos, h_src, st);
+}
+
+void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cudaStream_t st) {
   // ANKH_STREAM_TRACE=1: stage timestamps (ms after the call) on stderr
   const bool trace = std::getenv("ANKH_STREAM_TRACE") != nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
@@ -1203,28 +1322,32 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   streamed_last_ = true;
   const bool timing = cfg.phase_timing != 0;
   stream_setup();
-  const std::size_t chunk = stream_chunk_size();
-  const int C = static_cast<int>((n + chunk - 1) / chunk);
+  const int C = sch_.n;
   // copies: positions, then the moment chunks (after the previous evaluation)
   ANKH_CUDA(cudaEventRecord(ev_s_start_, st));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[0], st));
+  unsigned* p2p_work = std::getenv("ANKH_P2P_STATIC") ? nullptr : d_scnt_ + 4 * kMaxStreamChunks;
+  if (p2p_work) ANKH_CUDA(cudaMemsetAsync(p2p_work, 0, kMaxStreamChunks * sizeof(unsigned), st));
   mark("start", st);
   ANKH_CUDA(cudaStreamWaitEvent(copy_stream_, ev_s_start_, 0));
   if (!bound_pos) {
-    ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, copy_stream_));
-    ANKH_CUDA(cudaEventRecord(ev_s_pos_, copy_stream_));
+    for (int p = 0; p < pch_.n; ++p) {
+      const std::size_t i0 = pch_.start[p], i1 = pch_.start[p + 1];
+      ANKH_CUDA(cudaMemcpyAsync(d_pos_ + 3 * i0, h_pos + 3 * i0, (i1 - i0) * 3 * sizeof(double),
+                                cudaMemcpyHostToDevice, copy_stream_));
+      ANKH_CUDA(cudaEventRecord(ev_s_posc_[p], copy_stream_));
+    }
     mark("copy positions done", copy_stream_);
   }
   for (int c = 0; c < C; ++c) {
-    const std::size_t i0 = c * chunk, i1 = std::min(n, i0 + chunk);
+    const std::size_t i0 = sch_.start[c], i1 = sch_.start[c + 1];
     ANKH_CUDA(cudaMemcpyAsync(d_src_ + 10 * i0, h_src + 10 * i0, (i1 - i0) * 10 * sizeof(double),
                               cudaMemcpyHostToDevice, copy_stream_));
     ANKH_CUDA(cudaEventRecord(ev_s_chunk_[c], copy_stream_));
     mark("copy chunk " + std::to_string(c), copy_stream_);
   }
   if (!bound_pos) {
-    ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_pos_, 0));
-    stream_positions(st, d_res_, chunk, C,
+    stream_positions(st, d_res_, ev_s_posc_,
                      trace ? std::function<void(const std::string&)>([&](const std::string& w) { mark(w, st); })
                            : std::function<void(const std::string&)>(),
                      ev_s_inv_);
@@ -1248,11 +1371,12 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_sorted_, 0));
   ANKH_CUDA(cudaStreamWaitEvent(p2p_stream2_, ev_s_sorted_, 0));
   const unsigned p2m_cap = static_cast<unsigned>(std::min<long long>(n_leaves, 32ll * sm_count_));
-  const int p2p_grid = static_cast<int>(std::min<long long>(n_leaves, 6ll * sm_count_));
+  // a work-counter launch is one resident wave (3 CTAs per SM); static strides 2 waves
+  const int p2p_grid = static_cast<int>(std::min<long long>(n_leaves, (p2p_work ? 3ll : 6ll) * sm_count_));
   const bool do_periodic = periodic && include_self_;
   int n_near_parts = leaf_end_ - leaf_begin_;
   for (int c = 0; c < C; ++c) {
-    const std::size_t i0 = c * chunk, i1 = std::min(n, i0 + chunk);
+    const std::size_t i0 = sch_.start[c], i1 = sch_.start[c + 1];
     ANKH_CUDA(cudaStreamWaitEvent(gather_stream_, ev_s_chunk_[c], 0));
     launch_src_chunk(d_pos_, d_src_, d_inv_, i0, i1, d_res_, d_part_, gather_stream_, d_keys_, d_leaf_mp_);
     ANKH_CUDA(cudaEventRecord(ev_s_gath_[c], gather_stream_));
@@ -1266,7 +1390,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
     if (timing && c == 0) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
     n_near_parts = launch_p2p(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
                               p2p_cap_, leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, ps,
-                              d_list_p2p_, d_sbounds_ + (C + 1) + c, p2p_grid);
+                              d_list_p2p_, d_sbounds_ + (C + 1) + c, p2p_grid, p2p_work ? p2p_work + c : nullptr);
     mark("p2p " + std::to_string(c), ps);
     launches += 3;
   }
@@ -1277,7 +1401,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
   ANKH_CUDA(cudaStreamWaitEvent(st, ev_s_gath_[C - 1], 0));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[3], st));
   if (timing) {  // phase spans: M2M, M2L, periodic back to back
-    launch_m2m_chain(d_exp_, d_level_off_, depth - 1, 0, L, d_m2m_, d_m2m_cnt_, side_stream_);
+    launch_m2m(depth - 1, 0, side_stream_);
     ++launches;
     ANKH_CUDA(cudaEventRecord(ev_t_[4], side_stream_));
     for (int c = 1; c <= kMaxKp8; ++c) {
@@ -1289,7 +1413,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
     }
     ANKH_CUDA(cudaEventRecord(ev_t_[5], side_stream_));
     if (do_periodic) {
-      launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, side_stream_);
+      launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, side_stream_, d_per_scratch_);
       ++launches;
     }
     ANKH_CUDA(cudaEventRecord(ev_t_[6], side_stream_));
@@ -1355,9 +1479,8 @@ void Plan::set_positions(const double* h_pos, cudaStream_t st) {
   }
   if (stream_eligible()) {  // energy_sources will stream the moments chunk by chunk
     stream_setup();
-    const std::size_t chunk = stream_chunk_size();
     ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
-    stream_positions(st, d_res_pos_, chunk, static_cast<int>((n + chunk - 1) / chunk));
+    stream_positions(st, d_res_pos_, nullptr);
     ANKH_CUDA(cudaStreamSynchronize(st));
     bound_ = stream_bound_ = true;
     return;
@@ -1367,7 +1490,7 @@ void Plan::set_positions(const double* h_pos, cudaStream_t st) {
     launch_init_result(d_res_pos_, st, 0, d_counts_, static_cast<unsigned>(n_leaves + 1));
     const double inv_side = nax / (2.0 * rb);  // octree.cpp:35
     launch_bin(d_pos_, nullptr, n, rb, inv_side, nax, d_keys_, d_idx_, d_counts_, d_res_pos_, st, d_need_);
-    launch_bucket_gather(d_temp_, temp_bytes_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_,
+    launch_bucket_gather(scan_, d_pos_, nullptr, d_keys_, d_idx_, d_counts_,
                          d_off_, d_keys2_, d_idx_, d_idx2_, n, n_leaves, d_need_, nullptr, st);
   }
   ANKH_CUDA(cudaGetLastError());
@@ -1542,6 +1665,8 @@ void Plan::force_setup() {
 
 void Plan::forces(const double* h_pos, const double* h_src, double* h_forces, ankh_report_v1* out) {
   if (cfg.world > 1) throw AnkhError(ANKH_RUNTIME_ERROR, "forces: sharded plans (world > 1) are not supported");
+  if (L > kMaxOrderCompiled && pending_code_ == 0)
+    throw AnkhError(ANKH_RUNTIME_ERROR, "forces: order_cheb > 10 is not supported (energy only)");
   if (n == 0 || pending_code_ != 0 || csr_only_) {
     enqueue_host(h_pos, h_src, nullptr);
     result(out);  // raises the deferred error, if any

@@ -172,23 +172,39 @@ class Plan {
   // so the PCIe copy overlaps the evaluation.  Bit-identical to enqueue().
   bool stream_eligible() const;
   void stream_setup();
-  std::size_t stream_chunk_size() const;
-  void stream_positions(cudaStream_t st, DevResult* res, std::size_t chunk, int C,
+  // positions chunks pos_ev[0..pch_.n) (nullptr: already in d_pos_) are
+  // binned as they land; the leaf lists run beside the sort on side_stream_
+  void stream_positions(cudaStream_t st, DevResult* res, const cudaEvent_t* pos_ev,
                         const std::function<void(const std::string&)>& mark = {},
                         cudaEvent_t after_inverse = nullptr);
   void enqueue_streamed(const double* h_pos, const double* h_src, cudaStream_t st);
+  void enqueue_streamed_launch(const double* h_pos, const double* h_src, cudaStream_t st);
+  // CUDA-graph replay of the streamed path for repeated page-locked host
+  // buffers (h_pos == nullptr: bound positions): copies and kernels of one
+  // evaluation in one graph launch, captured on the second such call
+  cudaGraphExec_t sgraph_exec_ = nullptr;
+  const double *sgraph_pos_ = nullptr, *sgraph_src_ = nullptr;
+  const double *sgraph_warm_pos_ = nullptr, *sgraph_warm_src_ = nullptr;
+  bool sgraph_warm_ = false;
+  std::uint32_t sgraph_launches_ = 0;
   bool stream_bound_ = false;  // set_positions built the streamed path's lists
   static constexpr int kMaxStreamChunks = ankh_b200::kMaxStreamChunks;
   int stream_chunks_ = 8;
   bool stream_init_ = false;
-  unsigned *d_inv_ = nullptr, *d_scnt_ = nullptr, *d_sbounds_ = nullptr, *d_scursor_ = nullptr;
+  // moment chunks (the first one small: compute starts early) and
+  // positions chunks (binned as they land)
+  StreamChunks sch_{}, pch_{};
+  int stream_pos_chunks_ = 4;
+  unsigned *d_inv_ = nullptr, *d_scnt_ = nullptr, *d_sbounds_ = nullptr;
+  unsigned* d_leafmax_ = nullptr;  // = d_counts_ + n_leaves + 1 (zeroed with the histogram)
   unsigned *d_list_p2m_ = nullptr, *d_list_p2p_ = nullptr;
   int sm_count_ = 148;
   cudaStream_t p2p_stream2_ = nullptr;  // odd chunks' P2P (tails overlap the next chunk's start)
   unsigned char* d_ready_ = nullptr;
   cudaStream_t copy_stream_ = nullptr, gather_stream_ = nullptr;
-  cudaEvent_t ev_s_start_ = nullptr, ev_s_pos_ = nullptr, ev_s_sorted_ = nullptr, ev_s_inv_ = nullptr,
-              ev_s_p2p2_ = nullptr;
+  cudaEvent_t ev_s_start_ = nullptr, ev_s_binned_ = nullptr, ev_s_lists_ = nullptr, ev_s_sorted_ = nullptr,
+              ev_s_inv_ = nullptr, ev_s_p2p2_ = nullptr;
+  cudaEvent_t ev_s_posc_[kMaxStreamChunks] = {};
   cudaEvent_t ev_s_chunk_[kMaxStreamChunks] = {}, ev_s_gath_[kMaxStreamChunks] = {};
   // phase spans of a streamed evaluation (phases overlap: start/end per phase)
   cudaEvent_t ev_t_[9] = {};
@@ -224,6 +240,9 @@ class Plan {
   cudaEvent_t ev_m2l_fork_ = nullptr, ev_m2m_done_ = nullptr, ev_m2l_join_[kM2LStreams] = {};
   std::vector<int> class_leaf_;  // leading leaf-level tiles of each class's range
   std::uint32_t launch_far_chain(cudaStream_t far, bool fork, bool with_periodic);
+  void launch_m2m(int first, int top, cudaStream_t st, unsigned p_begin = 0, unsigned p_count = 0);
+  double* d_m2m_scratch_ = nullptr;  // runtime-order M2M past the shared-memory size
+  double* d_per_scratch_ = nullptr;  // periodic term past the shared-memory size
   // CUDA-graph replay of launch_all for repeated inputs
   cudaGraphExec_t graph_exec_ = nullptr;
   const double *graph_pos_ = nullptr, *graph_src_ = nullptr;
@@ -262,8 +281,9 @@ class Plan {
   unsigned* d_m2m_cnt_ = nullptr;  // arrival counters of the chained M2M  // per lex leaf: holds a dipole / quadrupole (P2P pair code)
   unsigned char* d_need_ = nullptr;  // shard: leaves whose records are gathered
   double* d_fin_scratch_ = nullptr;   // two-level final reduction
-  void* d_temp_ = nullptr;
+  void* d_temp_ = nullptr;  // radix sort of the validation path
   std::size_t temp_bytes_ = 0;
+  ScanWork scan_{};  // the CSR offsets' single-pass scan
   double* d_part_ = nullptr;
   // expansions
   double* d_exp_ = nullptr;

@@ -8,7 +8,8 @@ generator drift is detected instead of silently comparing different systems.
     python tests/golden/make_golden.py [--big | --high | --config 3|4]
 
 --big adds configs 1 and 2 (L = 3..6), which take minutes on the CPU;
---high writes the order 8-10 random systems (golden_high.json).
+--high writes the order 8-10 random systems (golden_high.json), --higher the
+order 11-16 ones (golden_higher.json).
 """
 from __future__ import annotations
 
@@ -48,6 +49,16 @@ HIGH_CASES = [
     ("rand_mp_L9_E2_p15", 500, 5.0, 22, True, dict(order_cheb=9, order_equi=9, depth=2, p=15)),
     ("rand_mp_L10_E1_p2", 300, 4.0, 23, True, dict(order_cheb=10, order_equi=10, depth=1, p=2)),
     ("rand_mp_L8_E2_open", 600, 5.0, 24, True, dict(order_cheb=8, order_equi=8, depth=2, p=0)),
+]
+
+
+# orders past the compiled kernels (11 .. 64: runtime-order P2M / M2M, host
+# randomized SVD, the periodic term in a global scratch from L = 15)
+HIGHER_CASES = [
+    ("rand_mp_L11_E2_p15", 300, 5.0, 31, True, dict(order_cheb=11, order_equi=11, depth=2, p=15)),
+    ("rand_mp_L12_E1_p2", 250, 4.0, 32, True, dict(order_cheb=12, order_equi=12, depth=1, p=2)),
+    ("rand_q_L13_E2_open", 400, 5.0, 33, False, dict(order_cheb=13, order_equi=13, depth=2, p=0)),
+    ("rand_mp_L16_E1_p15", 200, 4.0, 34, True, dict(order_cheb=16, order_equi=16, depth=1, p=15)),
 ]
 
 
@@ -103,6 +114,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--high", action="store_true", help="orders 8-10 only -> golden_high.json")
+    ap.add_argument("--higher", action="store_true", help="orders 11-16 only -> golden_higher.json")
     ap.add_argument("--series", action="store_true",
                     help="with --config 4: all evaluations of the rescale series -> golden_c4_series.json")
     ap.add_argument("--config", type=int, default=None,
@@ -150,10 +162,11 @@ def main():
         return
     doc = {"generator": "tests/golden/make_golden.py", "reference": "oracle/_ref/libankh_ref.so",
            "kats": kats(), "systems": []}
-    if args.high:
-        doc = {"generator": "tests/golden/make_golden.py --high",
+    if args.high or args.higher:
+        doc = {"generator": "tests/golden/make_golden.py --high" + ("er" if args.higher else ""),
                "reference": "oracle/_ref/libankh_ref.so", "systems": []}
-    for name, n, rb, seed, mp, kw in (HIGH_CASES if args.high else SMALL_CASES):
+    cases = HIGHER_CASES if args.higher else (HIGH_CASES if args.high else SMALL_CASES)
+    for name, n, rb, seed, mp, kw in cases:
         pos, src = inputs.random_system(n, rb, seed=seed, multipoles=mp)
         rep = R.fmm_energy(pos, src, rb, threads=threads, **kw)
         depth = kw["depth"]
@@ -164,7 +177,7 @@ def main():
             "leaf_csr_sha256": hashlib.sha256(offs.tobytes() + idx.tobytes()).hexdigest(),
         })
         print(name, doc["systems"][-1]["energies"]["e_total"], flush=True)
-    cfgs = [] if args.high else [(0, 4)]
+    cfgs = [] if (args.high or args.higher) else [(0, 4)]
     if args.big:
         cfgs += [(1, 4), (2, 3), (2, 4), (2, 5), (2, 6)]
     for ci, L in cfgs:
@@ -180,7 +193,8 @@ def main():
             "ref_wall_times": rep["wall_times"], "ref_threads": threads,
         })
         print(c.name, L, doc["systems"][-1]["energies"]["e_total"], rep["wall_times"]["total"], flush=True)
-    name = "golden_high.json" if args.high else ("golden_big.json" if args.big else "golden.json")
+    name = ("golden_higher.json" if args.higher else "golden_high.json" if args.high else
+            ("golden_big.json" if args.big else "golden.json"))
     with open(os.path.join(HERE, name), "w") as f:
         json.dump(doc, f, indent=1)
     print("wrote", name)
