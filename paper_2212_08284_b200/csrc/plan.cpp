@@ -150,6 +150,7 @@ Plan::~Plan() {
   for (void* p : allocs_) cudaFreeAsync(p, stream_);  // back to the pool (kept for the next plan)
   if (stream_) cudaStreamSynchronize(stream_);
   if (h_res_) cudaFreeHost(h_res_);
+  if (h_sbounds_) cudaFreeHost(h_sbounds_);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
@@ -1161,9 +1162,9 @@ void Plan::stream_setup() {
     stream_chunks_ = std::max(1, std::min(stream_chunks_, kMaxStreamChunks));
     d_inv_ = static_cast<unsigned*>(dalloc(n * sizeof(unsigned)));
     d_ready_ = static_cast<unsigned char*>(dalloc(2 * static_cast<std::size_t>(n_leaves)));
-    // list counts, list cursors, P2P work counters (kMaxStreamChunks each; 2, 2, 1)
-    d_scnt_ = static_cast<unsigned*>(dalloc(5 * kMaxStreamChunks * sizeof(unsigned)));
+    d_scnt_ = static_cast<unsigned*>(dalloc(4 * kMaxStreamChunks * sizeof(unsigned)));  // list counts, cursors
     d_sbounds_ = static_cast<unsigned*>(dalloc(2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
+    ANKH_CUDA(cudaMallocHost(&h_sbounds_, 2 * (kMaxStreamChunks + 1) * sizeof(unsigned)));
     d_list_p2m_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
     d_list_p2p_ = static_cast<unsigned*>(dalloc(static_cast<std::size_t>(n_leaves) * sizeof(unsigned)));
     ANKH_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device_));
@@ -1326,8 +1327,6 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
   // copies: positions, then the moment chunks (after the previous evaluation)
   ANKH_CUDA(cudaEventRecord(ev_s_start_, st));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[0], st));
-  unsigned* p2p_work = std::getenv("ANKH_P2P_STATIC") ? nullptr : d_scnt_ + 4 * kMaxStreamChunks;
-  if (p2p_work) ANKH_CUDA(cudaMemsetAsync(p2p_work, 0, kMaxStreamChunks * sizeof(unsigned), st));
   mark("start", st);
   ANKH_CUDA(cudaStreamWaitEvent(copy_stream_, ev_s_start_, 0));
   if (!bound_pos) {
@@ -1357,6 +1356,9 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
   }
   ANKH_CUDA(cudaEventRecord(ev_s_sorted_, st));
   if (timing) ANKH_CUDA(cudaEventRecord(ev_t_[1], st));
+  // this evaluation's list bounds for the next one's grids (D2H engine; read
+  // by the host only after the caller's synchronisation)
+  ANKH_CUDA(cudaMemcpyAsync(h_sbounds_, d_sbounds_, 2 * (C + 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
   mark("sorted + lists", st);
   ANKH_CUDA(cudaGetLastError());
   // No host wait: the chunk kernels read their leaf-list bounds on the device,
@@ -1370,9 +1372,24 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
   ANKH_CUDA(cudaMemsetAsync(d_leaf_mp_, 0, static_cast<std::size_t>(n_leaves) * sizeof(unsigned), gather_stream_));
   ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_sorted_, 0));
   ANKH_CUDA(cudaStreamWaitEvent(p2p_stream2_, ev_s_sorted_, 0));
-  const unsigned p2m_cap = static_cast<unsigned>(std::min<long long>(n_leaves, 32ll * sm_count_));
-  // a work-counter launch is one resident wave (3 CTAs per SM); static strides 2 waves
-  const int p2p_grid = static_cast<int>(std::min<long long>(n_leaves, (p2p_work ? 3ll : 6ll) * sm_count_));
+  // P2P chunk grids: one CTA per listed leaf, sized from the previous
+  // evaluation's list (the block scheduler balances short-lived CTAs, and the
+  // far chain's higher-priority CTAs interleave as they exit); the first
+  // evaluation strides two waves over each list.  (A persistent work-counter
+  // variant kept P2P's CTAs resident and pushed M2L behind it: 6.28 vs 6.16
+  // ms per streamed call at config 3.)
+  const bool sized = h_sbounds_valid_ && std::getenv("ANKH_P2P_STRIDE") == nullptr;
+  auto p2p_grid = [&](int c) {
+    if (!sized) return static_cast<int>(std::min<long long>(n_leaves, 6ll * sm_count_));
+    const long long cnt = static_cast<long long>(h_sbounds_[C + 1 + c + 1]) - h_sbounds_[C + 1 + c];
+    return static_cast<int>(std::max(1ll, std::min<long long>(n_leaves, cnt + cnt / 16 + 8)));
+  };
+  // P2M: one warp per listed leaf, sized the same way (else 32 warps per SM striding)
+  auto p2m_cap = [&](int c) {
+    if (!sized) return static_cast<unsigned>(std::min<long long>(n_leaves, 32ll * sm_count_));
+    const long long cnt = static_cast<long long>(h_sbounds_[c + 1]) - h_sbounds_[c];
+    return static_cast<unsigned>(std::max(1ll, std::min<long long>(n_leaves, cnt + cnt / 16 + 8)));
+  };
   const bool do_periodic = periodic && include_self_;
   int n_near_parts = leaf_end_ - leaf_begin_;
   for (int c = 0; c < C; ++c) {
@@ -1383,14 +1400,14 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
     mark("gather " + std::to_string(c), gather_stream_);
     ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[c], 0));
     launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, d_self_leaf_, cfg.xi, 0u,
-               0u, side_stream_, d_list_p2m_, d_sbounds_ + c, p2m_cap);
+               0u, side_stream_, d_list_p2m_, d_sbounds_ + c, p2m_cap(c));
     mark("p2m " + std::to_string(c), side_stream_);
     cudaStream_t ps = (c & 1) ? p2p_stream2_ : st;
     ANKH_CUDA(cudaStreamWaitEvent(ps, ev_s_gath_[c], 0));
     if (timing && c == 0) ANKH_CUDA(cudaEventRecord(ev_t_[2], st));
     n_near_parts = launch_p2p(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
                               p2p_cap_, leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, ps,
-                              d_list_p2p_, d_sbounds_ + (C + 1) + c, p2p_grid, p2p_work ? p2p_work + c : nullptr);
+                              d_list_p2p_, d_sbounds_ + (C + 1) + c, p2p_grid(c));
     mark("p2p " + std::to_string(c), ps);
     launches += 3;
   }
@@ -1434,6 +1451,7 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
   mark("finalize + result copy", st);
   ANKH_CUDA(cudaGetLastError());
   launches_ = launches;
+  h_sbounds_valid_ = true;
   if (trace) {
     ANKH_CUDA(cudaStreamSynchronize(st));
     for (auto& m : marks) {

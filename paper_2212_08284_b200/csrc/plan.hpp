@@ -189,7 +189,7 @@ class Plan {
   std::uint32_t sgraph_launches_ = 0;
   bool stream_bound_ = false;  // set_positions built the streamed path's lists
   static constexpr int kMaxStreamChunks = ankh_b200::kMaxStreamChunks;
-  int stream_chunks_ = 8;
+  int stream_chunks_ = 16;
   bool stream_init_ = false;
   // moment chunks (the first one small: compute starts early) and
   // positions chunks (binned as they land)
@@ -197,6 +197,10 @@ class Plan {
   int stream_pos_chunks_ = 4;
   unsigned *d_inv_ = nullptr, *d_scnt_ = nullptr, *d_sbounds_ = nullptr;
   unsigned* d_leafmax_ = nullptr;  // = d_counts_ + n_leaves + 1 (zeroed with the histogram)
+  // the previous evaluation's chunk-list bounds (page-locked copy): P2P chunk
+  // grids of one CTA per listed leaf (striding covers a larger list)
+  unsigned* h_sbounds_ = nullptr;
+  bool h_sbounds_valid_ = false;
   unsigned *d_list_p2m_ = nullptr, *d_list_p2p_ = nullptr;
   int sm_count_ = 148;
   cudaStream_t p2p_stream2_ = nullptr;  // odd chunks' P2P (tails overlap the next chunk's start)

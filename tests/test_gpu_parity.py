@@ -384,6 +384,24 @@ def test_streamed_host_path_bitwise(cuda, case, monkeypatch):
         for w, s_ in zip(want, (src, src2, src)):
             assert key(sp.energy_sources(s_)) == key(w), (case, chunks, "bound")
         sp.close()
+    # page-locked buffers: the streamed evaluation is captured into a CUDA
+    # graph on the second call and replayed; the replays read the buffers'
+    # current contents (moments changed in place between calls)
+    import torch
+
+    monkeypatch.setenv("ANKH_STREAM_CHUNKS", "8")
+    hp = torch.from_numpy(pos.copy()).pin_memory().numpy()
+    hs = torch.from_numpy(src.copy()).pin_memory().numpy()
+    sp = ankh.Plan(n, rb, cfg)
+    for k in range(4):
+        assert key(sp.energy(hp, hs)) == key(want[0]), (case, "graph", k)
+    hs[:] = src2
+    assert key(sp.energy(hp, hs)) == key(want[1]), (case, "graph, moments changed in place")
+    sp.set_positions(hp)
+    for k in range(3):
+        hs[:] = (src, src2, src)[k]
+        assert key(sp.energy_sources(hs)) == key(want[k % 2]), (case, "graph, bound", k)
+    sp.close()
 
 
 def test_streamed_host_path_errors(cuda, monkeypatch):
