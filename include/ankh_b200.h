@@ -109,6 +109,16 @@ int ankh_fmm_forces_v1(size_t n, const double* positions, const double* sources,
                        size_t errlen);
 int ankh_plan_forces_v1(ankh_plan_v1* plan, const double* positions, const double* sources, double* forces,
                         ankh_report_v1* out, char* err, size_t errlen);
+/* Forces (optional, n x 3) and the derivative of the energy with respect to
+ * every particle's 10 stored moments (optional, n x 10: dE/dq = the
+ * potential, dE/dmu = minus the field, dE/dTheta per stored component --
+ * an off-diagonal Theta_ij counts for both matrix entries), moments and
+ * positions as in ankh_fmm_energy_v1.  The energy is bilinear in the
+ * moments, so dsrc is exact for the reference's energy (central differences
+ * of fmm_energy reproduce it).  The induced-dipole solve iterates on
+ * -dE/dmu (api.induced_dipoles).  At least one output is required. */
+int ankh_plan_derivatives_v1(ankh_plan_v1* plan, const double* positions, const double* sources, double* forces,
+                             double* dsrc, ankh_report_v1* out, char* err, size_t errlen);
 
 /* The call-level checks of fmm_energy in the reference's order, for wrappers
  * whose containers carry separate position / source lengths:

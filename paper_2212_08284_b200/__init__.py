@@ -21,6 +21,8 @@ from .api import (  # noqa: F401
     exchange_leaf_levels,
     fmm_energy,
     fmm_forces,
+    InducedDipoles,
+    induced_dipoles,
     nccl_unique_id,
 )
 from ._lib import LIB_PATH, build, lib  # noqa: F401

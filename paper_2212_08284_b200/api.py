@@ -37,6 +37,8 @@ __all__ = [
     "CudaError",
     "fmm_energy",
     "fmm_forces",
+    "InducedDipoles",
+    "induced_dipoles",
     "default_depth",
     "build_tree_csr",
     "Plan",
@@ -240,6 +242,62 @@ def fmm_forces(system: ParticleSystem, config: Optional[EwaldConfig] = None,
     return EnergyReport._from_c(rep), forces
 
 
+@dataclasses.dataclass
+class InducedDipoles:
+    dipoles: np.ndarray      # n x 3 induced dipoles (e.A)
+    iterations: int          # conjugate-gradient iterations (one field evaluation each)
+    residual: float          # |mu / alpha - E(s + mu)| / |F0|, from a fresh evaluation
+    field: np.ndarray        # n x 3 total field at the solution (permanent + induced)
+
+
+def induced_dipoles(plan: "Plan", positions, sources, polarizability, tol: float = 1e-10,
+                    max_iter: int = 100) -> InducedDipoles:
+    """Self-consistent induced dipoles mu = alpha E(s + mu) (point
+    polarizabilities, the field of the same periodic FMM energy, Ewald self
+    term included) -- the solve the paper's perspective and BASELINE config 4
+    ("induced-dipole-style repeated solve") refer to.  E is affine in mu:
+    E(s + mu) = F0 + J mu with F0 = the field of the permanent moments and
+    J mu = the field of the dipoles mu alone, so (alpha^-1 - J) mu = F0 is
+    solved by conjugate gradients (J is symmetric: minus the energy's Hessian
+    in the dipoles); every product J p is one GPU field evaluation.
+    polarizability: scalar or length-n array (A^3)."""
+    pos = _as_host(positions, 3)
+    src = _as_host(sources, 10)
+    n = pos.shape[0]
+    alpha = np.broadcast_to(np.asarray(polarizability, dtype=np.float64), (n,)).reshape(n, 1)
+    if np.any(alpha <= 0):
+        raise InvalidArgument("induced_dipoles: polarizabilities must be positive")
+    inv_a = 1.0 / alpha
+    f0 = plan.field(pos, src)
+    probe = np.zeros_like(src)
+
+    def jmul(v):
+        probe[:, 1:4] = v
+        return plan.field(pos, probe)
+
+    x = alpha * f0  # the first (direct-field) guess
+    r = f0 - (inv_a * x - jmul(x))
+    p = r.copy()
+    rr = float(np.vdot(r, r))
+    bn = max(float(np.sqrt(np.vdot(f0, f0))), 1e-300)
+    it = 0
+    while np.sqrt(rr) / bn > tol and it < max_iter:
+        ap = inv_a * p - jmul(p)
+        it += 1
+        step = rr / float(np.vdot(p, ap))
+        x += step * p
+        r -= step * ap
+        rr_new = float(np.vdot(r, r))
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    # the residual from a fresh evaluation at the total moments: mu = alpha E(s + mu)
+    total = src.copy()
+    total[:, 1:4] += x
+    ftot = plan.field(pos, total)
+    res = float(np.sqrt(np.vdot(inv_a * x - ftot, inv_a * x - ftot))) / bn
+    return InducedDipoles(dipoles=x, iterations=it, residual=res, field=ftot)
+
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id (rank 0 creates it; broadcast to the other shards)."""
     buf = ctypes.create_string_buffer(128)
@@ -352,6 +410,27 @@ class Plan:
         _check(lib().ankh_plan_forces_v1(self._h, _ptr(pos), _ptr(src), _ptr(forces), ctypes.byref(rep), err,
                                          512), err)
         return EnergyReport._from_c(rep), forces
+
+    def derivatives(self, positions, sources, forces: bool = True):
+        """Energy, forces F = -dE/dx (n x 3, or None with ``forces=False``) and
+        the moment gradient dE/ds (n x 10, the stored moment layout: dE/dq is
+        the potential, dE/dmu minus the field, dE/dTheta per stored component)
+        of host arrays: (EnergyReport, forces, dsrc)."""
+        pos = _as_host(positions, 3)
+        src = _as_host(sources, 10)
+        self._check_n(pos, src)
+        rep = _Report()
+        err = ctypes.create_string_buffer(512)
+        f = np.zeros((pos.shape[0], 3), dtype=np.float64) if forces else None
+        dsrc = np.zeros((pos.shape[0], 10), dtype=np.float64)
+        _check(lib().ankh_plan_derivatives_v1(self._h, _ptr(pos), _ptr(src), _ptr(f) if f is not None else None,
+                                              _ptr(dsrc), ctypes.byref(rep), err, 512), err)
+        return EnergyReport._from_c(rep), f, dsrc
+
+    def field(self, positions, sources) -> np.ndarray:
+        """The electric field at every particle, -dE/dmu (n x 3): the quantity
+        an induced-dipole solve iterates on (``induced_dipoles``)."""
+        return -self.derivatives(positions, sources, forces=False)[2][:, 1:4]
 
     def set_positions(self, positions) -> None:
         """Bind host positions (copied, validated, binned and sorted once) for

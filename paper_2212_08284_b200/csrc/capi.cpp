@@ -191,6 +191,18 @@ int ankh_plan_forces_v1(ankh_plan_v1* plan, const double* positions, const doubl
   });
 }
 
+int ankh_plan_derivatives_v1(ankh_plan_v1* plan, const double* positions, const double* sources, double* forces,
+                             double* dsrc, ankh_report_v1* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!out) throw AnkhError(ANKH_INVALID_ARGUMENT, "null report");
+    on_plan(plan, [&](Plan& p) {
+      if (p.n > 0 && (!positions || !sources || (!forces && !dsrc)))
+        throw AnkhError(ANKH_INVALID_ARGUMENT, "null input buffer");
+      p.derivatives(positions, sources, forces, dsrc, out);
+    });
+  });
+}
+
 int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg, ankh_plan_v1** plan,
                         char* err, size_t errlen) {
   return guarded(err, errlen, [&] {

@@ -53,13 +53,16 @@ __device__ __forceinline__ void split_extf(int ext, int n, int& in_box, int& ima
 // ---------------------------------------------------------------- near field
 constexpr int kForceTPB = 256;
 
-template <int NT>
+// kDsrc: also the derivative of the pair energies with respect to the
+// target's 10 moments (pair_dsrc) into d_near[10 j] (sorted order)
+template <int NT, bool kDsrc>
 __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __restrict__ part,
                                                              const unsigned* __restrict__ leaf_off,
                                                              const unsigned* __restrict__ leaf_mp, int depth,
                                                              int periodic, double period,
                                                              const __grid_constant__ P2PParams pp, int cap,
-                                                             double* __restrict__ f_near) {
+                                                             double* __restrict__ f_near,
+                                                             double* __restrict__ d_near) {
   extern __shared__ __align__(16) double sm[];  // cap x kRec staged sources
   __shared__ int seg_begin[27], seg_prefix[28], seg_n, any_mp;
   __shared__ double seg_shift[27][3];
@@ -135,6 +138,7 @@ __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __rest
     const int il = t0 + (active ? tid % nt : 0), sl = active ? tid / nt : 0;
     const Target tg = load_target(part + static_cast<std::size_t>(a_begin + il) * kRec);
     double grad[3] = {0.0, 0.0, 0.0};
+    double ds[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int c0 = 0; c0 < total; c0 += cap) {
       const int cn = min(cap, total - c0);
       ANKH_DASSERT(cn > 0 && cn <= cap);
@@ -160,10 +164,16 @@ __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __rest
       const int skip = il - c0;  // the target itself (own leaf = virtual [0, na))
       if (mp) {
         for (int j = sl; j < cn; j += S)
-          if (j != skip) pair_grad_mp<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
+          if (j != skip) {
+            pair_grad_mp<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
+            if (kDsrc) pair_dsrc<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, ds);
+          }
       } else {
         for (int j = sl; j < cn; j += S)
-          if (j != skip) pair_grad_q<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
+          if (j != skip) {
+            pair_grad_q<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
+            if (kDsrc) pair_dsrc<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, ds);
+          }
       }
     }
     // fixed-order sum over the target's slices; F = -grad
@@ -179,6 +189,21 @@ __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __rest
       double* out = f_near + 3 * static_cast<std::size_t>(a_begin + t0 + tid);
 #pragma unroll
       for (int d = 0; d < 3; ++d) out[d] = -f[d];
+    }
+    if (kDsrc) {  // the same fixed-order slice sum, staged in the (finished) source buffer
+      __syncthreads();
+#pragma unroll
+      for (int d = 0; d < 10; ++d) sm[10 * tid + d] = ds[d];
+      __syncthreads();
+      if (tid < nt) {
+        double v[10] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int s_ = 0; s_ < S; ++s_)
+#pragma unroll
+          for (int d = 0; d < 10; ++d) v[d] += sm[10 * (s_ * nt + tid) + d];
+        double* out = d_near + 10 * static_cast<std::size_t>(a_begin + t0 + tid);
+#pragma unroll
+        for (int d = 0; d < 10; ++d) out[d] = v[d];
+      }
     }
   }
 }
@@ -461,7 +486,7 @@ __global__ void __launch_bounds__(kL2PThreads) k_l2p(const double* __restrict__ 
                                                      const unsigned* __restrict__ leaf_off, int depth,
                                                      double rb, const double* __restrict__ hd4,
                                                      const double* __restrict__ loc_leaf,
-                                                     double* __restrict__ f_far) {
+                                                     double* __restrict__ f_far, double* __restrict__ d_far) {
   constexpr int L2 = L * L, K = L2 * L, KS = exp_stride(K);
   __shared__ double lam[K];
   __shared__ double hd[4 * L2];  // H D^n, n = 0..3
@@ -560,7 +585,37 @@ __global__ void __launch_bounds__(kL2PThreads) k_l2p(const double* __restrict__ 
     out[0] = -g[0];
     out[1] = -g[1];
     out[2] = -g[2];
+    if (d_far) {  // dE_far/ds_a: the terms' own basis products (no extra derivative)
+      double* o = d_far + 10 * static_cast<std::size_t>(begin + pi);
+      o[0] = W[0][0][0];
+      o[1] = W[1][0][0];
+      o[2] = W[0][1][0];
+      o[3] = W[0][0][1];
+      o[4] = W[2][0][0];
+      o[5] = 2.0 * W[1][1][0];
+      o[6] = 2.0 * W[1][0][1];
+      o[7] = W[0][2][0];
+      o[8] = 2.0 * W[0][1][1];
+      o[9] = W[0][0][2];
+    }
   }
+}
+
+// dE/ds[idx[j]] = near[j] + far[j] + the self energy's derivative
+// (kernel.cpp:206-213: -xi/sqrt(pi) (q^2 + c_mu |mu|^2 + c_th Theta:Theta),
+// Theta:Theta with the off-diagonals twice)
+__global__ void k_dsrc_out(const double* __restrict__ d_near, const double* __restrict__ d_far,
+                           const double* __restrict__ part, const unsigned* __restrict__ sorted, std::size_t n,
+                           double self_scale, double c_mu, double c_th, double* __restrict__ out) {
+  const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (j >= n) return;
+  const double* r = part + j * kRec;  // x y z q mx my mz txx txy txz tyy tyz tzz tr
+  const double self[10] = {2.0 * r[3],        2.0 * c_mu * r[4], 2.0 * c_mu * r[5], 2.0 * c_mu * r[6],
+                           2.0 * c_th * r[7], 4.0 * c_th * r[8], 4.0 * c_th * r[9], 2.0 * c_th * r[10],
+                           4.0 * c_th * r[11], 2.0 * c_th * r[12]};
+  double* o = out + 10 * static_cast<std::size_t>(sorted[j]);
+#pragma unroll
+  for (int d = 0; d < 10; ++d) o[d] = (d_near[10 * j + d] + d_far[10 * j + d]) + self_scale * self[d];
 }
 
 // forces[idx[j]] = near[j] + far[j]: back to the caller's particle order
@@ -591,12 +646,19 @@ P2PParams make_force_params(double xi, const P2PRadial& rad) {
 template <int NT>
 void launch_force_near_t(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth,
                          int periodic, double period, const P2PParams& pp, int cap, double* f_near,
-                         cudaStream_t st) {
+                         double* d_near, cudaStream_t st) {
   const std::size_t smem = sizeof(double) * static_cast<std::size_t>(cap) * kRec;
-  static std::atomic<unsigned long long> attr{0};
-  smem_opt_in(attr, k_p2p_force<NT>, sizeof(double) * force_max_cap() * kRec);
-  k_p2p_force<NT><<<1u << (3 * depth), kForceTPB, smem, st>>>(part, leaf_off, leaf_mp, depth, periodic, period,
-                                                               pp, cap, f_near);
+  if (d_near) {
+    static std::atomic<unsigned long long> attr{0};
+    smem_opt_in(attr, k_p2p_force<NT, true>, sizeof(double) * force_max_cap() * kRec);
+    k_p2p_force<NT, true><<<1u << (3 * depth), kForceTPB, smem, st>>>(part, leaf_off, leaf_mp, depth, periodic,
+                                                                      period, pp, cap, f_near, d_near);
+  } else {
+    static std::atomic<unsigned long long> attr{0};
+    smem_opt_in(attr, k_p2p_force<NT, false>, sizeof(double) * force_max_cap() * kRec);
+    k_p2p_force<NT, false><<<1u << (3 * depth), kForceTPB, smem, st>>>(part, leaf_off, leaf_mp, depth, periodic,
+                                                                       period, pp, cap, f_near, nullptr);
+  }
 }
 
 }  // namespace
@@ -605,10 +667,12 @@ int force_max_cap() { return 960; }  // 960 x 112 B = 105 KB: two CTAs per SM
 
 void launch_force_near(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth,
                        int periodic, double period, double xi, const P2PRadial& rad, int cap, double* f_near,
-                       cudaStream_t st) {
+                       cudaStream_t st, double* d_near) {
   cap = cap < 64 ? 64 : (cap > force_max_cap() ? force_max_cap() : cap);
+  if (d_near && cap < kForceTPB) cap = kForceTPB;  // the moment sums are staged in the source buffer
   const P2PParams pp = make_force_params(xi, rad);
-#define ANKH_F_NT(N) launch_force_near_t<N>(part, leaf_off, leaf_mp, depth, periodic, period, pp, cap, f_near, st)
+#define ANKH_F_NT(N) \
+  launch_force_near_t<N>(part, leaf_off, leaf_mp, depth, periodic, period, pp, cap, f_near, d_near, st)
   switch (rad.nterms) {
     case 6: ANKH_F_NT(6); break;
     case 7: ANKH_F_NT(7); break;
@@ -672,9 +736,9 @@ void launch_l2l(const double* loc_parent, double* loc_child, int parent_level, i
 }
 
 void launch_l2p(const double* part, const unsigned* leaf_off, int depth, int order, double rb, const double* hd4,
-                const double* loc_leaf, double* f_far, cudaStream_t st) {
+                const double* loc_leaf, double* f_far, cudaStream_t st, double* d_far) {
   const unsigned leaves = 1u << (3 * depth);
-#define ANKH_L2P(N) k_l2p<N><<<leaves, kL2PThreads, 0, st>>>(part, leaf_off, depth, rb, hd4, loc_leaf, f_far)
+#define ANKH_L2P(N) k_l2p<N><<<leaves, kL2PThreads, 0, st>>>(part, leaf_off, depth, rb, hd4, loc_leaf, f_far, d_far)
   ANKH_FORCE_ORDERS(ANKH_L2P)
 #undef ANKH_L2P
 }
@@ -683,6 +747,16 @@ void launch_force_out(const double* f_near, const double* f_far, const unsigned*
                       double* out, cudaStream_t st) {
   if (n == 0) return;
   k_force_out<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(f_near, f_far, sorted, n, out);
+}
+
+void launch_dsrc_out(const double* d_near, const double* d_far, const double* part, const unsigned* sorted,
+                     std::size_t n, double xi, int include_self, double* out, cudaStream_t st) {
+  if (n == 0) return;
+  constexpr double kInvSqrtPiD = 0.56418958354775628695;
+  const double self_scale = include_self ? -xi * kInvSqrtPiD : 0.0;
+  const double c_mu = 2.0 * xi * xi / 3.0, c_th = 8.0 * xi * xi * xi * xi / 5.0;  // kernel.cpp:209-210
+  k_dsrc_out<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(d_near, d_far, part, sorted, n, self_scale,
+                                                                     c_mu, c_th, out);
 }
 
 }  // namespace ankh_b200

@@ -283,7 +283,7 @@ void launch_halo_rows(double* exp, const long long* row_off, long long n_rows, i
 int force_max_cap();
 void launch_force_near(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth,
                        int periodic, double period, double xi, const P2PRadial& rad, int cap, double* f_near,
-                       cudaStream_t st);
+                       cudaStream_t st, double* d_near = nullptr);
 std::size_t m2l_local_smem(int Kp);
 void launch_m2l_local(const double* exp, double* loc, const long long* level_off, const double* factors,
                       const M2LOp* ops, const int2* op_of, const int4* tiles, int n_tiles, int Kp, int periodic,
@@ -293,7 +293,11 @@ void launch_periodic_local(const double* root, const double* to_equi, const doub
 void launch_l2l(const double* loc_parent, double* loc_child, int parent_level, int order, const double* m2m,
                 cudaStream_t st);
 void launch_l2p(const double* part, const unsigned* leaf_off, int depth, int order, double rb, const double* hd4,
-                const double* loc_leaf, double* f_far, cudaStream_t st);
+                const double* loc_leaf, double* f_far, cudaStream_t st, double* d_far = nullptr);
+/// dE/ds (n x 10, the caller's order) = near + far (sorted order) + the
+/// self energy's derivative (include_self)
+void launch_dsrc_out(const double* d_near, const double* d_far, const double* part, const unsigned* sorted,
+                     std::size_t n, double xi, int include_self, double* out, cudaStream_t st);
 void launch_force_out(const double* f_near, const double* f_far, const unsigned* sorted, std::size_t n,
                       double* out, cudaStream_t st);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,

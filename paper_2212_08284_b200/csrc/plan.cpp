@@ -1682,6 +1682,11 @@ void Plan::force_setup() {
 }
 
 void Plan::forces(const double* h_pos, const double* h_src, double* h_forces, ankh_report_v1* out) {
+  derivatives(h_pos, h_src, h_forces, nullptr, out);
+}
+
+void Plan::derivatives(const double* h_pos, const double* h_src, double* h_forces, double* h_dsrc,
+                       ankh_report_v1* out) {
   if (cfg.world > 1) throw AnkhError(ANKH_RUNTIME_ERROR, "forces: sharded plans (world > 1) are not supported");
   if (L > kMaxOrderCompiled && pending_code_ == 0)
     throw AnkhError(ANKH_RUNTIME_ERROR, "forces: order_cheb > 10 is not supported (energy only)");
@@ -1696,16 +1701,30 @@ void Plan::forces(const double* h_pos, const double* h_src, double* h_forces, an
   force_setup();
   cudaStream_t st = stream_;
   ANKH_CUDA(cudaMemsetAsync(d_loc_, 0, level_off_[depth + 1] * sizeof(double), st));
+  const bool dsrc = h_dsrc != nullptr;
+  if (dsrc && !d_dnear_) {
+    const std::size_t nn = std::max<std::size_t>(n, 1);
+    d_dnear_ = static_cast<double*>(dalloc(nn * 10 * sizeof(double)));
+    d_dfar_ = static_cast<double*>(dalloc(nn * 10 * sizeof(double)));
+    d_dout_ = static_cast<double*>(dalloc(nn * 10 * sizeof(double)));
+  }
   launch_force_near(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, force_cap_,
-                    d_fnear_, st);
+                    d_fnear_, st, dsrc ? d_dnear_ : nullptr);
   launch_m2l_local(d_exp_, d_loc_, d_level_off_, d_factors_, d_ops_, d_op_of_, d_loc_tiles_, n_loc_tiles_, Kp,
                    periodic ? 1 : 0, st);
   if (periodic) launch_periodic_local(d_exp_, d_to_equi_, d_gen_, L, d_loc_, st);
   for (int l = 0; l < depth; ++l) launch_l2l(d_loc_ + level_off_[l], d_loc_ + level_off_[l + 1], l, L, d_m2m_, st);
-  launch_l2p(d_part_, d_off_, depth, L, rb, d_hd4_, d_loc_ + level_off_[depth], d_ffar_, st);
-  launch_force_out(d_fnear_, d_ffar_, d_idx2_, n, d_fout_, st);
+  launch_l2p(d_part_, d_off_, depth, L, rb, d_hd4_, d_loc_ + level_off_[depth], d_ffar_, st,
+             dsrc ? d_dfar_ : nullptr);
+  if (h_forces) {
+    launch_force_out(d_fnear_, d_ffar_, d_idx2_, n, d_fout_, st);
+    ANKH_CUDA(cudaMemcpyAsync(h_forces, d_fout_, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  if (dsrc) {
+    launch_dsrc_out(d_dnear_, d_dfar_, d_part_, d_idx2_, n, cfg.xi, include_self_ ? 1 : 0, d_dout_, st);
+    ANKH_CUDA(cudaMemcpyAsync(h_dsrc, d_dout_, n * 10 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
   ANKH_CUDA(cudaGetLastError());
-  ANKH_CUDA(cudaMemcpyAsync(h_forces, d_fout_, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   last_stream_ = st;
   result(out);
 }

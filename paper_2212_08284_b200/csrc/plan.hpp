@@ -109,6 +109,12 @@ class Plan {
   /// Energy evaluation plus the forces F = -dE/dx (n x 3, the caller's particle
   /// order) into host memory (one GPU).
   void forces(const double* h_pos, const double* h_src, double* h_forces, ankh_report_v1* out);
+  /// Forces (h_forces, n x 3, optional) and the derivative of the energy with
+  /// respect to every particle's 10 moments (h_dsrc, n x 10, optional: the
+  /// potential dE/dq, minus the field -dE/dmu, the field gradient dE/dTheta
+  /// per stored component) -- the induced-dipole machinery.
+  void derivatives(const double* h_pos, const double* h_src, double* h_forces, double* h_dsrc,
+                   ankh_report_v1* out);
 
   void expansions(double* out, std::size_t count);
   void m2l_factors(int level, const int* offset, double* lmat, double* rmat, int max_rank,
@@ -317,6 +323,7 @@ class Plan {
   void force_setup();
   bool force_init_ = false;
   double *d_loc_ = nullptr, *d_fnear_ = nullptr, *d_ffar_ = nullptr, *d_fout_ = nullptr, *d_hd4_ = nullptr;
+  double *d_dnear_ = nullptr, *d_dfar_ = nullptr, *d_dout_ = nullptr;  // moment derivatives (first use)
   double* d_gen_ = nullptr;  // periodic generator (build_periodic)
   int2* d_op_of_ = nullptr;
   int4* d_loc_tiles_ = nullptr;

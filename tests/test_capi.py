@@ -169,3 +169,36 @@ def test_radial_fit_is_roundoff_accurate(s_max, want_nt):
             h = h * s + ld(coef[k])
         assert float(np.max(np.abs((h - ref) / ref))) < 2.5e-16
     assert err.value < 2.5e-16
+
+
+def test_induced_dipole_solver_logic_on_a_linear_mock():
+    """Host logic of api.induced_dipoles (conjugate gradients on
+    (alpha^-1 - J) mu = F0, one field evaluation per product) against a dense
+    solve, with a mock plan whose field is linear in the moments."""
+    import paper_2212_08284_b200 as ankh
+
+    rng = np.random.default_rng(3)
+    n = 40
+    B = rng.normal(0, 0.2, (3 * n, 3 * n))
+    J = 0.5 * (B + B.T) / np.sqrt(3 * n)
+    Gq = rng.normal(0, 1.0, (3 * n, n))
+
+    class Mock:
+        calls = 0
+
+        def field(self, pos, s):
+            Mock.calls += 1
+            return (Gq @ s[:, 0] + J @ s[:, 1:4].reshape(-1)).reshape(n, 3)
+
+    pos = np.zeros((n, 3))
+    src = rng.normal(0, 1.0, (n, 10))
+    alpha = rng.uniform(0.2, 0.5, n)
+    sol = ankh.induced_dipoles(Mock(), pos, src, alpha, tol=1e-13, max_iter=500)
+    f0 = (Gq @ src[:, 0] + J @ src[:, 1:4].reshape(-1))
+    A = np.diag(np.repeat(1.0 / alpha, 3)) - J
+    want = np.linalg.solve(A, f0).reshape(n, 3)
+    assert np.abs(sol.dipoles - want).max() <= 1e-10 * np.abs(want).max()
+    assert sol.residual <= 1e-11 and sol.iterations <= 3 * n
+    assert Mock.calls == sol.iterations + 3  # F0, the first product, one per iteration, the check
+    with pytest.raises(ankh.InvalidArgument):
+        ankh.induced_dipoles(Mock(), pos, src, 0.0)

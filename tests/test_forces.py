@@ -115,3 +115,65 @@ def test_forces_at_scale_match_own_energy_differences(cuda, config):
             assert abs(f[i, d] - fd) <= 1e-6 * np.abs(f[idx]).max() + 2e-14 * abs(rep.e_total) / h, \
                 (i, d, f[i, d], fd)
     plan.close()
+
+
+# ---------------------------------------------------------------- moment gradient
+def _fd_moments(ref, pos, src, rb, kw, pairs, h):
+    """Central differences of the reference energy in single stored moments:
+    exact up to round-off, since the energy is a quadratic form in them."""
+    out = np.zeros(len(pairs))
+    for a, (i, k) in enumerate(pairs):
+        s1, s2 = src.copy(), src.copy()
+        s1[i, k] += h
+        s2[i, k] -= h
+        e1 = ref.fmm_energy(pos, s1, rb, threads=os.cpu_count(), **kw)["e_total"]
+        e2 = ref.fmm_energy(pos, s2, rb, threads=os.cpu_count(), **kw)["e_total"]
+        out[a] = (e1 - e2) / (2 * h)
+    return out
+
+
+@pytest.mark.parametrize("name", ["mp_L4_E2_periodic", "mp_L3_E2_open", "q_L5_E1_p2", "mp_L4_E2_xi0.3"])
+def test_moment_gradient_matches_reference_energy_differences(cuda, ref, name):
+    """dE/ds (potential, minus field, field gradient per stored moment) against
+    central differences of the reference's own energy in each moment -- every
+    component, including moments that are zero in the input (charges-only
+    case: the field of charges) and the off-diagonal quadrupole convention."""
+    n, rb, seed, mp, kw = CASES[name]
+    pos, src = inputs.random_system(n, rb, seed=seed, multipoles=mp)
+    plan = ankh.Plan(n, rb, ankh.EwaldConfig(**kw))
+    try:
+        rep, f, ds = plan.derivatives(pos, src)
+        rep2, f2 = plan.forces(pos, src)
+    finally:
+        plan.close()
+    assert ds.shape == (n, 10) and np.isfinite(ds).all()
+    # the forces of the same pass (the kernel variant differs in its schedule)
+    assert np.abs(f - f2).max() <= 1e-12 * np.abs(f2).max() and rep.e_total == rep2.e_total
+    pairs = [(i, k) for i in (0, n // 3, n - 1) for k in range(10)]
+    fd = _fd_moments(ref, pos, src, rb, kw, pairs, 0.5)
+    got = np.array([ds[i, k] for i, k in pairs])
+    scale = np.abs(fd).max()
+    tol = 1e-10 * scale + 1e-14 * abs(rep.e_total) / 0.5
+    assert np.abs(got - fd).max() <= tol, (name, np.abs(got - fd).max(), tol, got, fd)
+
+
+def test_induced_dipoles_self_consistent(cuda, ref):
+    """The conjugate-gradient induced-dipole solve on the water-like config 0
+    (point polarizabilities 0.1 A^3): mu = alpha E(s + mu) to 1e-10, checked
+    with a fresh field evaluation and, at a few particles, with central
+    differences of the reference energy at the total moments."""
+    pos, src, rb, c = inputs.make_config(0)
+    kw = dict(order_cheb=4, order_equi=4)
+    plan = ankh.Plan(pos.shape[0], rb, ankh.EwaldConfig(**kw))
+    try:
+        sol = ankh.induced_dipoles(plan, pos, src, 0.1, tol=1e-11, max_iter=60)
+    finally:
+        plan.close()
+    assert sol.iterations < 60 and sol.residual <= 1e-9, (sol.iterations, sol.residual)
+    assert np.abs(sol.dipoles - 0.1 * sol.field).max() <= 1e-9 * np.abs(sol.dipoles).max()
+    total = src.copy()
+    total[:, 1:4] += sol.dipoles
+    pairs = [(i, k) for i in (5, 1700) for k in (1, 2, 3)]
+    fd = _fd_moments(ref, pos, total, rb, kw, pairs, 0.05)
+    field = np.array([sol.field[i, k - 1] for i, k in pairs])
+    assert np.abs(field + fd).max() <= 1e-9 * np.abs(fd).max() + 1e-12, (field, -fd)
