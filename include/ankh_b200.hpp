@@ -187,6 +187,22 @@ class Plan {
             err);
     return from_c<Report>(r);
   }
+  /// Energy plus the moment gradient dE/ds (n x 10 doubles in the
+  /// MultipoleSource layout: potential, minus the field, field gradient per
+  /// stored component) -- the induced-dipole machinery; any 80-byte element.
+  template <class P, class S, class G>
+  Report moment_gradient(const std::vector<P>& positions, const std::vector<S>& sources, std::vector<G>& dsrc) {
+    static_assert(sizeof(G) == 10 * sizeof(double), "moment-gradient element layout");
+    check(positions.size(), sources.size());
+    dsrc.resize(n_);
+    ankh_report_v1 r;
+    char err[512];
+    rethrow(ankh_plan_derivatives_v1(plan_, reinterpret_cast<const double*>(positions.data()),
+                                     reinterpret_cast<const double*>(sources.data()), nullptr,
+                                     reinterpret_cast<double*>(dsrc.data()), &r, err, sizeof(err)),
+            err);
+    return from_c<Report>(r);
+  }
   /// Bind positions once (copied, validated, binned) ...
   template <class P>
   void set_positions(const std::vector<P>& positions) {

@@ -78,6 +78,11 @@ int main(int argc, char** argv) {
     std::vector<ankh::Vec3> f;
     const ankh::EnergyReport c = plan.forces(sys.positions, sys.sources, f);
     std::printf("forces %.17g %.17g %.17g %.17g\n", c.e_total, f[0].x, f[0].y, f[n - 1].z);
+    // the moment gradient (potential, -field, field gradient) into the
+    // caller's own MultipoleSource vector (same 10-double layout)
+    std::vector<ankh::MultipoleSource> g;
+    const ankh::EnergyReport d = plan.moment_gradient(sys.positions, sys.sources, g);
+    std::printf("mgrad %.17g %.17g %.17g %.17g\n", d.e_total, g[0].q, g[0].mu.x, g[n - 1].theta.m[1]);
   }
   try {
     ankh::EwaldConfig bad = cfg;

@@ -58,3 +58,12 @@ def test_dropin_runs_and_matches_python(cuda, tmp_path):
     rf, f = ankh.fmm_forces(ankh.ParticleSystem(pos, src, 5.0),
                             ankh.EwaldConfig(order_cheb=4, order_equi=4, depth=2, p=15))
     assert [float(v) for v in line[1:]] == [rf.e_total, f[0, 0], f[0, 1], f[-1, 2]]
+    line = [l for l in out.splitlines() if l.startswith("mgrad ")][0].split()
+    plan = ankh.Plan(pos.shape[0], 5.0, ankh.EwaldConfig(order_cheb=4, order_equi=4, depth=2, p=15))
+    try:
+        rg, _, ds = plan.derivatives(pos, src, forces=False)
+    finally:
+        plan.close()
+    got = [float(v) for v in line[1:]]
+    want = [rg.e_total, ds[0, 0], ds[0, 1], ds[-1, 5]]
+    assert np.allclose(got, want, rtol=1e-13, atol=0.0), (got, want)
