@@ -447,16 +447,47 @@ std::vector<double> gaussian_rowmajor(int rows, int cols, std::uint64_t seed) {
   return m;
 }
 
-// c (m x k) = a (m x n) * b (n x k), row-major
+// c (m x k) = a (m x n) * b (n x k), row-major.  Every c_ij accumulates its
+// n products in increasing l, one multiply-add at a time (the arithmetic of
+// the plain triple loop, bit for bit); the loops are blocked so a (l, j)
+// block of b stays cache-resident across all rows of a, and four rows of c
+// share each load of b.
 std::vector<double> matmul(const std::vector<double>& a, const std::vector<double>& b, int m, int n,
                            int k) {
   std::vector<double> c(static_cast<std::size_t>(m) * k, 0.0);
-  for (int i = 0; i < m; ++i) {
-    double* ci = c.data() + static_cast<std::size_t>(i) * k;
-    for (int l = 0; l < n; ++l) {
-      const double x = a[static_cast<std::size_t>(i) * n + l];
-      const double* bl = b.data() + static_cast<std::size_t>(l) * k;
-      for (int j = 0; j < k; ++j) ci[j] += x * bl[j];
+  constexpr int JB = 256, LB = 128;
+  for (int j0 = 0; j0 < k; j0 += JB) {
+    const int jn = std::min(JB, k - j0);
+    for (int l0 = 0; l0 < n; l0 += LB) {
+      const int l1 = std::min(n, l0 + LB);
+      int i = 0;
+      for (; i + 4 <= m; i += 4) {
+        double* __restrict__ c0 = c.data() + static_cast<std::size_t>(i) * k + j0;
+        double* __restrict__ c1 = c0 + k;
+        double* __restrict__ c2 = c1 + k;
+        double* __restrict__ c3 = c2 + k;
+        const double* a0 = a.data() + static_cast<std::size_t>(i) * n;
+        for (int l = l0; l < l1; ++l) {
+          const double x0 = a0[l], x1 = a0[n + l], x2 = a0[2 * static_cast<std::size_t>(n) + l],
+                       x3 = a0[3 * static_cast<std::size_t>(n) + l];
+          const double* __restrict__ bl = b.data() + static_cast<std::size_t>(l) * k + j0;
+          for (int j = 0; j < jn; ++j) {
+            const double bv = bl[j];
+            c0[j] += x0 * bv;
+            c1[j] += x1 * bv;
+            c2[j] += x2 * bv;
+            c3[j] += x3 * bv;
+          }
+        }
+      }
+      for (; i < m; ++i) {
+        double* __restrict__ ci = c.data() + static_cast<std::size_t>(i) * k + j0;
+        for (int l = l0; l < l1; ++l) {
+          const double x = a[static_cast<std::size_t>(i) * n + l];
+          const double* __restrict__ bl = b.data() + static_cast<std::size_t>(l) * k + j0;
+          for (int j = 0; j < jn; ++j) ci[j] += x * bl[j];
+        }
+      }
     }
   }
   return c;
