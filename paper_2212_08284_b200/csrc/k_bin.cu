@@ -153,29 +153,42 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const unsigned* __restric
   }
   if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
-  if (tid == 0) {
-    unsigned agg = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) {
-      const unsigned t = s_warp[w];
-      s_warp[w] = agg;
-      agg += t;
+  if (warp == 0) {
+    // block aggregate and the warps' exclusive offsets
+    const unsigned wv = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+    unsigned wi = wv;
+#pragma unroll
+    for (int o = 1; o < kScanThreads / 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
     }
+    const unsigned agg = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - wv;
     volatile unsigned long long* st = status;
     unsigned long long excl = 0;
     if (tile == 0) {
-      st[0] = kScanIncl | agg;
+      if (lane == 0) st[0] = kScanIncl | agg;
     } else {
-      st[tile] = kScanAgg | agg;
-      for (int j = static_cast<int>(tile) - 1; j >= 0;) {
-        const unsigned long long w = st[j];
-        if ((w & ~kScanVal) == 0) continue;  // predecessor not published yet
-        excl += w & kScanVal;
-        if ((w & ~kScanVal) == kScanIncl) break;
-        --j;
+      if (lane == 0) st[tile] = kScanAgg | agg;
+      // warp-wide look-back: 32 predecessors per round trip, nearest first;
+      // stop at the nearest one that published its inclusive prefix
+      for (long long j = static_cast<long long>(tile) - 1; j >= 0; j -= 32) {
+        const long long idx = j - lane;
+        unsigned long long w = kScanIncl + 0ull;  // before tile 0: inclusive 0
+        if (idx >= 0) w = st[idx];
+        while (__any_sync(0xffffffffu, (w & ~kScanVal) == 0))
+          if ((w & ~kScanVal) == 0) w = st[idx];
+        const unsigned incl_mask = __ballot_sync(0xffffffffu, (w & ~kScanVal) == kScanIncl);
+        const int stop = incl_mask ? __ffs(incl_mask) - 1 : 31;  // lanes 0..stop contribute
+        unsigned long long v = lane <= stop ? (w & kScanVal) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        excl += __shfl_sync(0xffffffffu, v, 0);
+        if (incl_mask) break;
       }
-      st[tile] = kScanIncl | (excl + agg);
+      if (lane == 0) st[tile] = kScanIncl | (excl + agg);
     }
-    s_prefix = static_cast<unsigned>(excl);
+    if (lane == 0) s_prefix = static_cast<unsigned>(excl);
   }
   __syncthreads();
   unsigned run = s_prefix + s_warp[warp] + (incl - tsum);
