@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const unsigned* __restric
   if (tid == 0) s_tile = atomicAdd(&ctr[0], 1u);
   __syncthreads();
   const unsigned tile = s_tile;
+  ANKH_DASSERT(tile < gridDim.x);  // tickets: one per block (the state was reset by the last launch)
   const std::size_t base = static_cast<std::size_t>(tile) * kScanTile + static_cast<std::size_t>(tid) * kScanItems;
   unsigned v[kScanItems];
   if (base + kScanItems <= n) {

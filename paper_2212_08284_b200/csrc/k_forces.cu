@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __rest
       for (int d = 0; d < 3; ++d) out[d] = -f[d];
     }
     if (kDsrc) {  // the same fixed-order slice sum, staged in the (finished) source buffer
+      ANKH_DASSERT(cap * kRec >= 10 * kForceTPB);
       __syncthreads();
 #pragma unroll
       for (int d = 0; d < 10; ++d) sm[10 * tid + d] = ds[d];

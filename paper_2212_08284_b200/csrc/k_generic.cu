@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kGenThreads) k_p2m_gen(const double* __restric
   const unsigned leaf = (static_cast<unsigned>(ci[0]) * n + ci[1]) * n + ci[2];
   const unsigned begin = leaf_off[leaf];
   const int cnt = static_cast<int>(leaf_off[leaf + 1] - begin);
+  ANKH_DASSERT(leaf_off[leaf + 1] >= begin && PB >= 1 && PB <= kGenThreads);
   double* out = exp_leaf + static_cast<std::size_t>(m) * KS;
   if (cnt == 0) {  // fmm.cpp:190-193
     for (int o = tid; o < K; o += kGenThreads) out[o] = 0.0;
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(kGenThreads) k_m2m_gen(const double* __restric
   double* A = S2 + K;
   for (unsigned pi = blockIdx.x; pi < p_count; pi += gridDim.x) {
     const unsigned p = p_begin + pi;
+    ANKH_DASSERT(gbuf || 3 * K * sizeof(double) <= 200 * 1024);
     for (int c = 0; c < 8; ++c) {  // Morton children 8p + (cx<<2 | cy<<1 | cz)
       const int cx = c >> 2, cy = (c >> 1) & 1, cz = c & 1;
       const double* v = child + (8ull * p + c) * KS;
