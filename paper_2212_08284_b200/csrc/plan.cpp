@@ -1268,6 +1268,22 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
     streamed_last_ = true;
     launches_ = sgraph_launches_;
   };
+  // the graph's chunk grids were sized from the lists of the evaluation
+  // before its capture: when the last replay's lists (h_sbounds_) outgrow
+  // them or shrink to under half (new positions), capture again
+  if (sgraph_exec_ && sgraph_pos_ == h_pos && sgraph_src_ == h_src) {
+    const int C = sch_.n;
+    for (int k = 0; k < 2 * C; ++k) {
+      const int set = k / C, c = k - set * C;
+      const long long cnt = static_cast<long long>(h_sbounds_[set * (C + 1) + c + 1]) - h_sbounds_[set * (C + 1) + c];
+      const long long g = sgraph_grid_[k];
+      if (cnt > g || 2 * cnt + 16 < g) {
+        cudaGraphExecDestroy(sgraph_exec_);
+        sgraph_exec_ = nullptr;
+        break;
+      }
+    }
+  }
   if (sgraph_exec_ && sgraph_pos_ == h_pos && sgraph_src_ == h_src) {
     ANKH_CUDA(cudaGraphLaunch(sgraph_exec_, st));
     replayed();
@@ -1294,6 +1310,7 @@ void Plan::enqueue_streamed(const double* h_pos, const double* h_src, cudaStream
     sgraph_pos_ = h_pos;
     sgraph_src_ = h_src;
     sgraph_launches_ = launches_;
+    sgraph_grid_ = last_grids_;
     ANKH_CUDA(cudaGraphLaunch(sgraph_exec_, st));
     return;
   }
@@ -1385,6 +1402,7 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
     return static_cast<int>(std::max(1ll, std::min<long long>(n_leaves, cnt + cnt / 16 + 8)));
   };
   // P2M: one warp per listed leaf, sized the same way (else 32 warps per SM striding)
+  last_grids_.assign(2 * static_cast<std::size_t>(C), 0);
   auto p2m_cap = [&](int c) {
     if (!sized) return static_cast<unsigned>(std::min<long long>(n_leaves, 32ll * sm_count_));
     const long long cnt = static_cast<long long>(h_sbounds_[c + 1]) - h_sbounds_[c];
@@ -1401,6 +1419,7 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
     ANKH_CUDA(cudaStreamWaitEvent(side_stream_, ev_s_gath_[c], 0));
     launch_p2m(d_part_, d_off_, depth, L, rb, d_hd_, d_exp_ + level_off_[depth], d_res_, d_self_leaf_, cfg.xi, 0u,
                0u, side_stream_, d_list_p2m_, d_sbounds_ + c, p2m_cap(c));
+    last_grids_[c] = p2m_cap(c);
     mark("p2m " + std::to_string(c), side_stream_);
     cudaStream_t ps = (c & 1) ? p2p_stream2_ : st;
     ANKH_CUDA(cudaStreamWaitEvent(ps, ev_s_gath_[c], 0));
@@ -1408,6 +1427,7 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
     n_near_parts = launch_p2p(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
                               p2p_cap_, leaf_begin_, leaf_end_, d_near_part_, d_pair_count_, d_res_, ps,
                               d_list_p2p_, d_sbounds_ + (C + 1) + c, p2p_grid(c));
+    last_grids_[C + c] = p2p_grid(c);
     mark("p2p " + std::to_string(c), ps);
     launches += 3;
   }

@@ -193,6 +193,7 @@ class Plan {
   const double *sgraph_warm_pos_ = nullptr, *sgraph_warm_src_ = nullptr;
   bool sgraph_warm_ = false;
   std::uint32_t sgraph_launches_ = 0;
+  std::vector<long long> sgraph_grid_, last_grids_;  // P2M / P2P chunk grids (captured, last launch)
   bool stream_bound_ = false;  // set_positions built the streamed path's lists
   static constexpr int kMaxStreamChunks = ankh_b200::kMaxStreamChunks;
   int stream_chunks_ = 16;

@@ -401,6 +401,16 @@ def test_streamed_host_path_bitwise(cuda, case, monkeypatch):
     for k in range(3):
         hs[:] = (src, src2, src)[k]
         assert key(sp.energy_sources(hs)) == key(want[k % 2]), (case, "graph, bound", k)
+    # positions changed in place (a reversed particle order: other chunk
+    # lists, so the replayed graph's grids no longer fit and it is captured
+    # again) -- still the plain path's report for that input
+    rev = np.ascontiguousarray(pos[::-1]), np.ascontiguousarray(src[::-1])
+    monkeypatch.setenv("ANKH_STREAM_INPUT", "0")
+    want_rev = plain.energy(*rev)
+    monkeypatch.setenv("ANKH_STREAM_INPUT", "1")
+    hp[:], hs[:] = rev
+    for k in range(3):
+        assert key(sp.energy(hp, hs)) == key(want_rev), (case, "graph, new positions", k)
     sp.close()
 
 
