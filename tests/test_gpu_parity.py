@@ -267,7 +267,9 @@ def test_leaf_csr_bit_exact(cuda, ref):
     # ordered input (consecutive particles share leaves: config 1's lattice)
     wpos, _, wrb, _ = inputs.make_config(1)
     for pos, rb, depth in [(inputs.random_system(200000, 5.0, seed=9)[0], 5.0, 8), (wpos, wrb, 6),
-                           (wpos, wrb, 8)]:
+                           (wpos, wrb, 8), (inputs.random_system(1, 2.0, seed=3)[0], 2.0, 8),
+                           (inputs.random_system(5, 2.0, seed=4)[0], 2.0, 7),
+                           (inputs.random_system(4095, 2.0, seed=5)[0], 2.0, 4)]:
         offs, idx = ankh.build_tree_csr(pos, rb, depth)
         o2, i2 = ref.leaf_csr(pos, rb, depth)
         assert np.array_equal(offs, o2) and np.array_equal(idx, i2)
