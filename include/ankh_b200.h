@@ -132,6 +132,15 @@ int ankh_check_call_v1(const ankh_config_v1* cfg, double box_radius, size_t n_po
 int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg,
                         ankh_plan_v1** plan, char* err, size_t errlen);
 void ankh_plan_destroy_v1(ankh_plan_v1* plan);
+/* The same plan with the ANKH-FFT far field (PAPER.md
+ * Alg. 4-5): leaf Chebyshev expansions re-interpolated onto equispaced
+ * grids of order cfg->order_equi, the far field of every non-adjacent leaf
+ * pair (images |I|_inf <= 1) as one circulant quadratic form evaluated with
+ * a 6-D DFT (e_far), the far images on the root operator as before
+ * (e_periodic_far).  Not the reference's energy: it converges to it as both
+ * orders grow (the reference has no such engine; no drop-in parity). */
+int ankh_plan_create_fft_v1(size_t n, double box_radius, const ankh_config_v1* cfg, ankh_plan_v1** plan,
+                            char* err, size_t errlen);
 
 /* Evaluate with HOST input buffers (copied in on the plan's stream). */
 int ankh_plan_energy_v1(ankh_plan_v1* plan, const double* positions, const double* sources,

@@ -21,6 +21,7 @@ from .api import (  # noqa: F401
     exchange_leaf_levels,
     fmm_energy,
     fmm_forces,
+    fft_energy,
     InducedDipoles,
     induced_dipoles,
     nccl_unique_id,

@@ -19,6 +19,7 @@ EXPORTS = [
     "ankh_fmm_forces_v1",
     "ankh_plan_forces_v1",
     "ankh_plan_derivatives_v1",
+    "ankh_plan_create_fft_v1",
     "ankh_plan_create_v1",
     "ankh_plan_destroy_v1",
     "ankh_plan_energy_v1",
@@ -87,6 +88,7 @@ def lib() -> ctypes.CDLL:
         L.ankh_plan_derivatives_v1.argtypes = [c_void_p, D, D, D, D, c_void_p, cp, c_size_t]
         L.ankh_check_call_v1.argtypes = [c_void_p, c_double, c_size_t, c_size_t, cp, c_size_t]
         L.ankh_plan_create_v1.argtypes = [c_size_t, c_double, c_void_p, c_void_p, cp, c_size_t]
+        L.ankh_plan_create_fft_v1.argtypes = [c_size_t, c_double, c_void_p, c_void_p, cp, c_size_t]
         L.ankh_plan_destroy_v1.argtypes = [c_void_p]
         L.ankh_plan_destroy_v1.restype = None
         L.ankh_plan_energy_v1.argtypes = [c_void_p, D, D, c_void_p, cp, c_size_t]

@@ -38,6 +38,7 @@ __all__ = [
     "fmm_energy",
     "fmm_forces",
     "InducedDipoles",
+    "fft_energy",
     "induced_dipoles",
     "default_depth",
     "build_tree_csr",
@@ -298,6 +299,23 @@ def induced_dipoles(plan: "Plan", positions, sources, polarizability, tol: float
     return InducedDipoles(dipoles=x, iterations=it, residual=res, field=ftot)
 
 
+def fft_energy(system: ParticleSystem, config: Optional[EwaldConfig] = None) -> EnergyReport:
+    """The ANKH-FFT engine (Alg. 4-5): the far
+    field of the leaf level as one circulant quadratic form on equispaced grids
+    of order ``config.order_equi`` (6-D DFT on the GPU, ``k_fft.cu``), near
+    field, self energy and far images as the reference computes them.  Not the
+    reference's energy (which has no such engine): it converges to it as
+    order_cheb and order_equi grow."""
+    config = config or EwaldConfig()
+    pos = _as_host(system.positions, 3)
+    src = _as_host(system.sources, 10)
+    plan = Plan(pos.shape[0], system.box_radius, config, engine="fft", phase_timing=False)
+    try:
+        return plan.energy(pos, src)
+    finally:
+        plan.close()
+
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id (rank 0 creates it; broadcast to the other shards)."""
     buf = ctypes.create_string_buffer(128)
@@ -361,7 +379,7 @@ class Plan:
 
     def __init__(self, n: int, box_radius: float, config: Optional[EwaldConfig] = None,
                  threads: int = 0, device: int = -1, rank: int = 0, world: int = 1,
-                 phase_timing: bool = True):
+                 phase_timing: bool = True, engine: str = "fmm"):
         self.config = config or EwaldConfig()
         self.n = int(n)
         self.box_radius = float(box_radius)
@@ -369,8 +387,10 @@ class Plan:
         err = ctypes.create_string_buffer(512)
         cfg = self.config._c(threads=threads, device=device, rank=rank, world=world,
                              phase_timing=phase_timing)
-        _check(lib().ankh_plan_create_v1(self.n, self.box_radius, ctypes.byref(cfg),
-                                         ctypes.byref(self._h), err, 512), err)
+        if engine not in ("fmm", "fft"):
+            raise InvalidArgument("engine must be 'fmm' (the reference's) or 'fft' (ANKH-FFT)")
+        create = lib().ankh_plan_create_fft_v1 if engine == "fft" else lib().ankh_plan_create_v1
+        _check(create(self.n, self.box_radius, ctypes.byref(cfg), ctypes.byref(self._h), err, 512), err)
 
     def close(self) -> None:
         if self._h:

@@ -213,6 +213,16 @@ int ankh_plan_create_v1(size_t n, double box_radius, const ankh_config_v1* cfg, 
   });
 }
 
+int ankh_plan_create_fft_v1(size_t n, double box_radius, const ankh_config_v1* cfg, ankh_plan_v1** plan,
+                            char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!cfg || !plan) throw AnkhError(ANKH_INVALID_ARGUMENT, "null config or plan pointer");
+    auto h = std::make_unique<ankh_plan_v1>();
+    h->plan = std::make_unique<Plan>(n, box_radius, *cfg, false, /*engine=*/1);
+    *plan = h.release();
+  });
+}
+
 void ankh_plan_destroy_v1(ankh_plan_v1* plan) { delete plan; }  // ~Plan selects its own device
 
 int ankh_check_call_v1(const ankh_config_v1* cfg, double box_radius, size_t n_positions,

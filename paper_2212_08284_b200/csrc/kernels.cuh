@@ -300,6 +300,17 @@ void launch_dsrc_out(const double* d_near, const double* d_far, const double* pa
                      std::size_t n, double xi, int include_self, double* out, cudaStream_t st);
 void launch_force_out(const double* f_near, const double* f_far, const unsigned* sorted, std::size_t n,
                       double* out, cudaStream_t st);
+// ANKH-FFT far field (k_fft.cu): the leaf-level
+// equispaced engine.  Arrays: X / tmp [cells][NF] double2, diag Pc^3 NF doubles.
+struct FftShape {
+  int n, Pc, Lu, Pn, NF;
+  long long energy_blocks;  // partials written by launch_fft_far
+};
+FftShape fft_shape(int depth, int order_equi);
+void launch_fft_precompute(const FftShape& s, int depth, double rb, double xi, int periodic, double2* tmp_a,
+                           double2* tmp_b, double* diag, cudaStream_t st);
+void launch_fft_far(const FftShape& s, const double* exp_leaf, int KS, int depth, int order_cheb, const double* E,
+                    double2* x0, double2* x1, const double* diag, double* partial, cudaStream_t st);
 void launch_dup_check(const unsigned* keys_sorted, const unsigned* idx_sorted, const double* pos,
                       std::size_t n, DevResult* res, cudaStream_t st);
 

@@ -45,14 +45,15 @@ int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b
 
 }  // namespace
 
-Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool csr_only)
-    : n(n_), rb(box_radius), cfg(cfg_), csr_only_(csr_only) {
+Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool csr_only, int engine)
+    : n(n_), rb(box_radius), cfg(cfg_), csr_only_(csr_only), fft_(engine == 1) {
   const auto t0 = std::chrono::steady_clock::now();
   validate_config(cfg);
   if (!(rb > 0.0) || !std::isfinite(rb))
     throw AnkhError(ANKH_INVALID_ARGUMENT, "fmm_energy: invalid system: box_radius must be positive and finite");
   if (n >= (1ull << 31)) throw AnkhError(ANKH_RUNTIME_ERROR, "fmm_energy: more than 2^31-1 particles");
   if (cfg.world < 1) cfg.world = 1;
+  if (fft_ && cfg.world > 1) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: sharded plans (world > 1) are not supported");
   if (cfg.rank < 0 || cfg.rank >= cfg.world) throw AnkhError(ANKH_INVALID_ARGUMENT, "rank out of range");
   if (cfg.device >= 0) {
     int count = 0;
@@ -130,7 +131,10 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
   stamp("allocate", ts);
   if (pending_code_ == 0 && n > 0 && !csr_only_) {
     build_halo();
-    build_m2l();
+    if (fft_)
+      build_fft();
+    else
+      build_m2l();
     stamp("m2l", ts);
     if (periodic) build_periodic();
     stamp("periodic", ts);
@@ -733,6 +737,36 @@ void Plan::build_m2l() {
 
 // build_periodic_operator (fmm.cpp:333-377): generator on the GPU, its r2c
 // spectrum (FFTW layout, spectral.cpp:47-62) on the host, real part uploaded.
+// ANKH-FFT engine (k_fft.cu): the equispaced transfer E (L_u x L_c), the
+// circulant spectrum of the leaf-level far-field operator (generator + 6-D
+// DFT on the device), the evaluation's work arrays, one far partial per
+// energy CTA (summed by k_finalize as the far field), no M2L classes.
+void Plan::build_fft() {
+  const int Lu = cfg.order_equi;
+  if (Lu < 2 || Lu > 16) throw AnkhError(ANKH_INVALID_ARGUMENT, "fft engine: order_equi must be in [2, 16]");
+  if (depth > 6) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: depth > 6 is not supported");
+  if (L > kMaxOrderCompiled) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: order_cheb > 10 is not supported");
+  fft_shape_ = fft_shape(depth, Lu);
+  const FftShape& s = fft_shape_;
+  const std::vector<double> E = transfer_equi(Lu, cheb_nodes(L));  // Lu x L
+  d_fft_E_ = static_cast<double*>(dalloc(E.size() * sizeof(double)));
+  ANKH_CUDA(cudaMemcpyAsync(d_fft_E_, E.data(), E.size() * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  const std::size_t cells = static_cast<std::size_t>(s.Pc) * s.Pc * s.Pc;
+  d_fft_diag_ = static_cast<double*>(dalloc(cells * s.NF * sizeof(double)));
+  d_fft_x0_ = static_cast<double2*>(dalloc(cells * s.NF * sizeof(double2)));  // precompute size (largest)
+  d_fft_x1_ = static_cast<double2*>(dalloc(cells * s.NF * sizeof(double2)));
+  launch_fft_precompute(s, depth, rb, cfg.xi, periodic ? 1 : 0, d_fft_x0_, d_fft_x1_, d_fft_diag_, stream_);
+  ANKH_CUDA(cudaGetLastError());
+  n_tiles_ = static_cast<int>(s.energy_blocks);
+  d_far_part_ = static_cast<double*>(dalloc(static_cast<std::size_t>(n_tiles_) * sizeof(double)));
+  class_range_.assign(kMaxKp8 + 1, {0, 0});
+  class_leaf_.assign(kMaxKp8 + 1, 0);
+  far_flops = 0.0;
+  m2l_instances = 0;
+  m2l_operators = 0;
+  ANKH_CUDA(cudaStreamSynchronize(stream_));
+}
+
 void Plan::build_periodic() {
   const int eb = 2 * L - 1;
   const std::size_t m = static_cast<std::size_t>(eb) * eb * eb;
@@ -854,6 +888,7 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
                  K, Kp, d_far_part_, far);
       ++launches;
     }
+    if (fft_) launches += launch_fft(far);
     if (timing) ANKH_CUDA(cudaEventRecord(ev_[3], st));
   } else {
     // M2M, M2L and the periodic far images (counted once, rank 0) in branches
@@ -906,6 +941,12 @@ void Plan::launch_all(const double* d_pos, const double* d_src, cudaStream_t st,
 // the M2M chain runs on `far`; the coarse-level tiles and the periodic term
 // follow M2M on the least-loaded branches (greedy by tiles x padded rank);
 // every branch joins back into `far`.
+std::uint32_t Plan::launch_fft(cudaStream_t s) {
+  launch_fft_far(fft_shape_, d_exp_ + level_off_[depth], Kp, depth, L, d_fft_E_, d_fft_x0_, d_fft_x1_, d_fft_diag_,
+                 d_far_part_, s);
+  return 4;
+}
+
 std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_periodic) {
   std::uint32_t launches = 0;
   std::vector<int> cls;
@@ -925,6 +966,7 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
   };
   if (!fork) {
     m2m(far);
+    if (fft_) launches += launch_fft(far);
     for (int c : cls) m2l(c, class_range_[c].first, class_range_[c].second, far);
     if (with_periodic) {
       launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, far, d_per_scratch_);
@@ -955,6 +997,11 @@ std::uint32_t Plan::launch_far_chain(cudaStream_t far, bool fork, bool with_peri
     const int k = pick(1);
     load[k] += work(c, class_leaf_[c]);
     m2l(c, class_range_[c].first, class_leaf_[c], lane[k]);
+  }
+  if (fft_) {  // the ANKH-FFT far field needs only the leaf level: beside M2M
+    const int k = pick(1);
+    load[k] += 1;
+    launches += launch_fft(lane[k]);
   }
   m2m(far);
   ANKH_CUDA(cudaEventRecord(ev_m2m_done_, far));
@@ -1448,6 +1495,7 @@ void Plan::enqueue_streamed_launch(const double* h_pos, const double* h_src, cud
                  K, Kp, d_far_part_, side_stream_);
       ++launches;
     }
+    if (fft_) launches += launch_fft(side_stream_);
     ANKH_CUDA(cudaEventRecord(ev_t_[5], side_stream_));
     if (do_periodic) {
       launch_periodic_eval(d_exp_, d_to_equi_, d_spec_re_, L, d_per_, side_stream_, d_per_scratch_);
@@ -1710,6 +1758,7 @@ void Plan::derivatives(const double* h_pos, const double* h_src, double* h_force
   if (cfg.world > 1) throw AnkhError(ANKH_RUNTIME_ERROR, "forces: sharded plans (world > 1) are not supported");
   if (L > kMaxOrderCompiled && pending_code_ == 0)
     throw AnkhError(ANKH_RUNTIME_ERROR, "forces: order_cheb > 10 is not supported (energy only)");
+  if (fft_) throw AnkhError(ANKH_RUNTIME_ERROR, "forces: not available on the fft engine (energy only)");
   if (n == 0 || pending_code_ != 0 || csr_only_) {
     enqueue_host(h_pos, h_src, nullptr);
     result(out);  // raises the deferred error, if any

@@ -89,7 +89,9 @@ struct OpInfo {
 
 class Plan {
  public:
-  Plan(std::size_t n, double box_radius, const ankh_config_v1& cfg, bool csr_only = false);
+  /// engine 0: the reference's SVD-compressed M2L (the drop-in); 1: the
+  /// ANKH-FFT leaf-level far field (k_fft.cu, L_u = cfg.order_equi).
+  Plan(std::size_t n, double box_radius, const ankh_config_v1& cfg, bool csr_only = false, int engine = 0);
   ~Plan();
   Plan(const Plan&) = delete;
   Plan& operator=(const Plan&) = delete;
@@ -160,6 +162,11 @@ class Plan {
   void build_geometry();
   void build_m2l();
   void build_periodic();
+  void build_fft();
+  bool fft_ = false;
+  FftShape fft_shape_{};
+  double *d_fft_E_ = nullptr, *d_fft_diag_ = nullptr;
+  double2 *d_fft_x0_ = nullptr, *d_fft_x1_ = nullptr;
   void allocate();
   void* dalloc(std::size_t bytes);
   // checked build (-DANKH_CHECKED): guard zones after the plan buffers
@@ -251,6 +258,7 @@ class Plan {
   cudaEvent_t ev_m2l_fork_ = nullptr, ev_m2m_done_ = nullptr, ev_m2l_join_[kM2LStreams] = {};
   std::vector<int> class_leaf_;  // leading leaf-level tiles of each class's range
   std::uint32_t launch_far_chain(cudaStream_t far, bool fork, bool with_periodic);
+  std::uint32_t launch_fft(cudaStream_t s);  // the ANKH-FFT far field (fft_ plans)
   void launch_m2m(int first, int top, cudaStream_t st, unsigned p_begin = 0, unsigned p_count = 0);
   double* d_m2m_scratch_ = nullptr;  // runtime-order M2M past the shared-memory size
   double* d_per_scratch_ = nullptr;  // periodic term past the shared-memory size

@@ -232,3 +232,22 @@ def test_golden_small_systems(golden):
         got = O.fmm_energy(pos, src, case["box_radius"], **kw)
         want = {k: float(v) for k, v in case["energies"].items()}
         assert rel(got["e_total"], want["e_total"]) < 1e-10, case["name"]
+
+
+def test_fft_engine_restatement_matches_dense_sum():
+    """oracle/fft_engine.py: the circulant/DFT evaluation of 1/2 v^T A v equals
+    the pair-by-pair dense sum on tiny trees (periodic and open), and its
+    spectrum is real (Cor. 3)."""
+    import fft_engine as F
+
+    from paper_2212_08284_b200 import inputs
+
+    for depth, Lu, xi, per in ((1, 3, 0.3, True), (2, 3, 0.1, True), (2, 2, 0.1, False)):
+        pos, src = inputs.random_system(120, 3.0, seed=depth, multipoles=True)
+        v = F.equi_leaf_values(pos, src, 3.0, depth, 4, Lu)
+        G = F.generator(3.0, depth, Lu, xi, per)
+        got = F.fft_far(v, G)
+        want = F.dense_far(v, 3.0, depth, Lu, xi, per)
+        assert abs(got - want) <= 1e-12 * abs(want)
+        d = np.fft.fftn(G)
+        assert np.abs(d.imag).max() <= 1e-10 * np.abs(d).max()
