@@ -170,7 +170,7 @@ __device__ __forceinline__ double kernel_h(double r, double xi) { return erfc_sc
 __global__ void __launch_bounds__(kNodeThreads) k_fft_gen_node(int depth, int Lu, double rb, double xi, int periodic,
                                                                double2* __restrict__ Y) {
   extern __shared__ __align__(16) double sm[];
-  const int n = 1 << depth, Pc = 2 * n - 1, Pn = 2 * Lu - 1, NF = Pn * Pn * Lu;
+  const int n = 1 << depth, Pc = 2 * n, Pn = 2 * Lu - 1, NF = Pn * Pn * Lu;
   double* g = sm;                                               // Pn^3
   double2* tw = reinterpret_cast<double2*>(g + ((Pn * Pn * Pn + 1) & ~1));  // Pn
   double2* s1 = tw + ((Pn + 1) & ~1);                           // Pn Pn Lu
@@ -179,6 +179,10 @@ __global__ void __launch_bounds__(kNodeThreads) k_fft_gen_node(int depth, int Lu
   const int tid = threadIdx.x;
   const int cell = blockIdx.x;
   const int ix = cell / (Pc * Pc), iy = (cell / Pc) % Pc, iz = cell % Pc;
+  // circulant embedding of size Pc = 2n per cell axis: offsets 0..n-1 at
+  // their index, -(n-1)..-1 at index + 2n; index n is outside the Toeplitz
+  // block (any value embeds it: zero)
+  const bool unused = ix == n || iy == n || iz == n;
   const int dcx = ix < n ? ix : ix - Pc, dcy = iy < n ? iy : iy - Pc, dcz = iz < n ? iz : iz - Pc;
   const double rad = rb / n, h = 2.0 * rad / (Lu - 1);
   for (int j = tid; j < Pn; j += kNodeThreads) {
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(kNodeThreads) k_fft_gen_node(int depth, int Lu
       for (int Iy = I0; Iy <= I1; ++Iy)
         for (int Iz = I0; Iz <= I1; ++Iz) {
           const int Dx = dcx + n * Ix, Dy = dcy + n * Iy, Dz = dcz + n * Iz;
-          if (max(abs(Dx), max(abs(Dy), abs(Dz))) < 2) continue;  // adjacent: the near field's
+          if (unused || max(abs(Dx), max(abs(Dy), abs(Dz))) < 2) continue;  // adjacent: the near field's
           const double zx = 2.0 * rad * Dx + h * dnx, zy = 2.0 * rad * Dy + h * dny, zz = 2.0 * rad * Dz + h * dnz;
           acc += kernel_h(sqrt(zx * zx + zy * zy + zz * zz), xi);
         }
@@ -212,49 +216,87 @@ constexpr int kLineLanes = 32, kLineGroups = 8, kLineThreads = kLineLanes * kLin
 
 // One cell axis of the 3-D transform over an [outer][axis][inner] complex
 // array: out[o][k][i] = sum_{j < nin} in[o][j][i] w^(j k), k < P, w = exp(-2 pi
-// i / P).  A CTA takes 32 consecutive inner elements of one outer index and all
-// P outputs (lanes = inner: coalesced); mode 0 writes complex, mode 1 writes
-// Re (the spectral diagonal), mode 2 accumulates sum_k mult(nf) D[k][i] |w|^2
-// into one partial per CTA (nf = inner index mod NF, mult = 1 on the kz = 0
-// half-plane, else 2).
+// i / P).  A CTA takes 32 R consecutive inner elements of one outer index and
+// all P outputs (lanes = inner: coalesced); a thread keeps R lines x 4 outputs
+// in registers, so each staged input and twiddle it loads feeds 4 resp. R
+// complex multiply-adds (shared-memory loads would otherwise bound it).
+// mode 0 writes complex, mode 1 writes Re (the spectral diagonal), mode 2
+// accumulates sum_k mult(nf) D[k][i] |w|^2 into one partial per CTA (nf =
+// inner index mod NF; mult = 1 on the kz = 0 half-plane, else 2).
+template <int R>
 __global__ void __launch_bounds__(kLineThreads) k_fft_line(const double2* __restrict__ in, void* __restrict__ out,
                                                             int nin, int P, long long n_inner, int mode,
                                                             const double* __restrict__ D, int NF, int Lu,
                                                             double* __restrict__ partial, double scale) {
-  extern __shared__ __align__(16) double2 sx[];  // nin x 32, then P twiddles
-  double2* tw = sx + nin * kLineLanes;
+  constexpr int W = kLineLanes * R, S = 4;
+  extern __shared__ __align__(16) double2 sx[];  // nin x W, then P twiddles
+  double2* tw = sx + nin * W;
   __shared__ double red[kLineThreads];
   const int lane = threadIdx.x & (kLineLanes - 1), grp = threadIdx.x / kLineLanes;
-  const long long tiles = (n_inner + kLineLanes - 1) / kLineLanes;
+  const long long tiles = (n_inner + W - 1) / W;
   const long long o = blockIdx.x / tiles;
-  const long long i = (blockIdx.x % tiles) * kLineLanes + lane;
-  const bool ok = i < n_inner;
+  const long long i0 = (blockIdx.x % tiles) * W + lane;
   for (int j = threadIdx.x; j < P; j += kLineThreads) {
     double s, c;
     sincospi(-2.0 * j / P, &s, &c);
     tw[j] = make_double2(c, s);
   }
   const double2* src = in + o * nin * n_inner;
-  for (int j = grp; j < nin; j += kLineGroups) sx[j * kLineLanes + lane] = ok ? src[j * n_inner + i] : make_double2(0.0, 0.0);
+  for (int j = grp; j < nin; j += kLineGroups)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long long i = i0 + kLineLanes * r;
+      sx[j * W + lane + kLineLanes * r] = i < n_inner ? src[j * n_inner + i] : make_double2(0.0, 0.0);
+    }
   __syncthreads();
   double e = 0.0;
-  const double mult = (mode == 2 && ok && (i % NF) % Lu != 0) ? 2.0 : 1.0;
-  for (int k = grp; k < P; k += kLineGroups) {
-    double2 acc = make_double2(0.0, 0.0);
-    int ph = 0;
-    for (int j = 0; j < nin; ++j) {
-      cmac(acc, sx[j * kLineLanes + lane], tw[ph]);
-      ph += k;
-      if (ph >= P) ph -= P;
+  double mult[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const long long i = i0 + kLineLanes * r;
+    mult[r] = (mode == 2 && i < n_inner && (i % NF) % Lu != 0) ? 2.0 : 1.0;
+  }
+  for (int k0 = grp; k0 < P; k0 += kLineGroups * S) {
+    double2 acc[S][R];
+    int ph[S], kk[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      kk[q] = k0 + kLineGroups * q < P ? k0 + kLineGroups * q : 0;  // past P: computed, discarded
+      ph[q] = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[q][r] = make_double2(0.0, 0.0);
     }
-    if (!ok) continue;
-    const long long dst = (o * P + k) * n_inner + i;
-    if (mode == 0)
-      static_cast<double2*>(out)[dst] = acc;
-    else if (mode == 1)
-      static_cast<double*>(out)[dst] = acc.x;
-    else
-      e = fma(D[dst] * mult, fma(acc.x, acc.x, acc.y * acc.y), e);
+    for (int j = 0; j < nin; ++j) {
+      double2 x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = sx[j * W + lane + kLineLanes * r];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const double2 t = tw[ph[q]];
+#pragma unroll
+        for (int r = 0; r < R; ++r) cmac(acc[q][r], x[r], t);
+        ph[q] += kk[q];
+        if (ph[q] >= P) ph[q] -= P;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const int k = k0 + kLineGroups * q;
+      if (k >= P) continue;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long i = i0 + kLineLanes * r;
+        if (i >= n_inner) continue;
+        const long long dst = (o * P + k) * n_inner + i;
+        const double2 a = acc[q][r];
+        if (mode == 0)
+          static_cast<double2*>(out)[dst] = a;
+        else if (mode == 1)
+          static_cast<double*>(out)[dst] = a.x;
+        else
+          e = fma(D[dst] * mult[r], fma(a.x, a.x, a.y * a.y), e);
+      }
+    }
   }
   if (mode != 2) return;
   red[threadIdx.x] = e;
@@ -266,15 +308,110 @@ __global__ void __launch_bounds__(kLineThreads) k_fft_line(const double2* __rest
   if (threadIdx.x == 0) partial[blockIdx.x] = scale * red[0];
 }
 
-std::size_t line_smem(int nin, int P) { return sizeof(double2) * (static_cast<std::size_t>(nin) * kLineLanes + P); }
+// Power-of-two line length P (the cell axes, embedding 2n): a radix-2
+// decimation-in-frequency FFT of 32 lines per CTA in shared memory
+// ([P][32] complex; inputs j >= nin are zero), outputs read back in
+// bit-reversed order -- the same three modes as k_fft_line.  HBM-bound: the
+// transform costs ~(P/2) log2 P butterflies per line instead of nin P
+// multiply-adds.
+__global__ void __launch_bounds__(kLineThreads) k_fft_line2(const double2* __restrict__ in, void* __restrict__ out,
+                                                             int nin, int P, int logP, long long n_inner, int mode,
+                                                             const double* __restrict__ D, int NF, int Lu,
+                                                             double* __restrict__ partial, double scale) {
+  extern __shared__ __align__(16) double2 sb[];  // P x 32, then P/2 twiddles
+  double2* tw = sb + P * kLineLanes;
+  __shared__ double red[kLineThreads];
+  const int lane = threadIdx.x & (kLineLanes - 1), grp = threadIdx.x / kLineLanes;
+  const long long tiles = (n_inner + kLineLanes - 1) / kLineLanes;
+  const long long o = blockIdx.x / tiles;
+  const long long i = (blockIdx.x % tiles) * kLineLanes + lane;
+  const bool ok = i < n_inner;
+  for (int j = threadIdx.x; j < P / 2; j += kLineThreads) {
+    double s, c;
+    sincospi(-2.0 * j / P, &s, &c);
+    tw[j] = make_double2(c, s);
+  }
+  const double2* src = in + o * nin * n_inner;
+  for (int j = grp; j < P; j += kLineGroups)
+    sb[j * kLineLanes + lane] = (ok && j < nin) ? src[j * n_inner + i] : make_double2(0.0, 0.0);
+  __syncthreads();
+  // DIF stages: span h = P/2 .. 1; butterfly (a, a + h), twiddle w^(r P / (2h))
+  for (int h = P >> 1, st = 1; h >= 1; h >>= 1, st <<= 1) {
+    for (int b = grp; b < P / 2; b += kLineGroups) {
+      const int r = b & (h - 1), a = ((b - r) << 1) + r;
+      const double2 u = sb[a * kLineLanes + lane], v = sb[(a + h) * kLineLanes + lane];
+      sb[a * kLineLanes + lane] = make_double2(u.x + v.x, u.y + v.y);
+      sb[(a + h) * kLineLanes + lane] = cmul(make_double2(u.x - v.x, u.y - v.y), tw[r * st]);
+    }
+    __syncthreads();
+  }
+  double e = 0.0;
+  const double mult = (mode == 2 && ok && (i % NF) % Lu != 0) ? 2.0 : 1.0;
+  for (int k = grp; k < P; k += kLineGroups) {
+    if (!ok) continue;
+    const int rk = static_cast<int>(__brev(static_cast<unsigned>(k)) >> (32 - logP));
+    const double2 a = sb[rk * kLineLanes + lane];
+    const long long dst = (o * P + k) * n_inner + i;
+    if (mode == 0)
+      static_cast<double2*>(out)[dst] = a;
+    else if (mode == 1)
+      static_cast<double*>(out)[dst] = a.x;
+    else
+      e = fma(D[dst] * mult, fma(a.x, a.x, a.y * a.y), e);
+  }
+  if (mode != 2) return;
+  red[threadIdx.x] = e;
+  __syncthreads();
+  for (int s2 = kLineThreads / 2; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2) red[threadIdx.x] += red[threadIdx.x + s2];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = scale * red[0];
+}
+
+// lines per thread: the largest R in {4, 2, 1} whose staged block stays
+// within ~100 KB (two CTAs per SM)
+int line_r(int nin) { return nin <= 48 ? 4 : (nin <= 97 ? 2 : 1); }
+
+std::size_t line_smem(int nin, int P, int R) {
+  return sizeof(double2) * (static_cast<std::size_t>(nin) * kLineLanes * R + P);
+}
+
+bool pow2(int P) { return P >= 2 && (P & (P - 1)) == 0; }
+
+long long line_blocks(long long n_outer, long long n_inner, int nin, int P) {
+  const long long W = pow2(P) ? kLineLanes : kLineLanes * line_r(nin);
+  return n_outer * ((n_inner + W - 1) / W);
+}
 
 void launch_line(const double2* in, void* out, long long n_outer, int nin, int P, long long n_inner, int mode,
                  const double* D, int NF, int Lu, double* partial, cudaStream_t st, double scale = 1.0) {
-  const long long tiles = (n_inner + kLineLanes - 1) / kLineLanes;
-  static std::atomic<unsigned long long> attr{0};
-  smem_opt_in(attr, k_fft_line, 200 * 1024);
-  k_fft_line<<<static_cast<unsigned>(n_outer * tiles), kLineThreads, line_smem(nin, P), st>>>(
-      in, out, nin, P, n_inner, mode, D, NF, Lu, partial, scale);
+  const unsigned grid = static_cast<unsigned>(line_blocks(n_outer, n_inner, nin, P));
+  if (pow2(P)) {
+    int logP = 0;
+    while ((1 << logP) < P) ++logP;
+    static std::atomic<unsigned long long> attr2{0};
+    smem_opt_in(attr2, k_fft_line2, 200 * 1024);
+    k_fft_line2<<<grid, kLineThreads, sizeof(double2) * (static_cast<std::size_t>(P) * kLineLanes + P / 2), st>>>(
+        in, out, nin, P, logP, n_inner, mode, D, NF, Lu, partial, scale);
+    return;
+  }
+  const int R = line_r(nin);
+  const std::size_t smem = line_smem(nin, P, R);
+#define ANKH_LINE(RR)                                                                                   \
+  {                                                                                                     \
+    static std::atomic<unsigned long long> attr{0};                                                     \
+    smem_opt_in(attr, k_fft_line<RR>, 200 * 1024);  /* + 3 KB static: within the 227 KB */           \
+    k_fft_line<RR><<<grid, kLineThreads, smem, st>>>(in, out, nin, P, n_inner, mode, D, NF, Lu, partial, \
+                                                     scale);                                            \
+  }
+  if (R == 4)
+    ANKH_LINE(4)
+  else if (R == 2)
+    ANKH_LINE(2)
+  else
+    ANKH_LINE(1)
+#undef ANKH_LINE
 }
 
 std::size_t node_smem_leaf(int Lc, int Lu) {
@@ -294,11 +431,11 @@ std::size_t node_smem_gen(int Lu) {
 FftShape fft_shape(int depth, int order_equi) {
   FftShape s;
   s.n = 1 << depth;
-  s.Pc = 2 * s.n - 1;
+  s.Pc = 2 * s.n;  // power-of-two circulant embedding (>= 2n - 1): radix-2 cell-axis FFTs
   s.Lu = order_equi;
   s.Pn = 2 * order_equi - 1;
   s.NF = s.Pn * s.Pn * s.Lu;
-  s.energy_blocks = (static_cast<long long>(s.Pc) * s.Pc * s.NF + kLineLanes - 1) / kLineLanes;
+  s.energy_blocks = line_blocks(1, static_cast<long long>(s.Pc) * s.Pc * s.NF, s.n, s.Pc);
   return s;
 }
 
