@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kLineThreads) k_fft_line2(const double2* __res
                                                              int nin, int P, int logP, long long n_inner, int mode,
                                                              const double* __restrict__ D, int NF, int Lu,
                                                              double* __restrict__ partial, double scale) {
-  extern __shared__ __align__(16) double2 sb[];  // P x 32, then P/2 twiddles
+  extern __shared__ __align__(16) double2 sb[];  // P x 32, then P twiddles
   double2* tw = sb + P * kLineLanes;
   __shared__ double red[kLineThreads];
   const int lane = threadIdx.x & (kLineLanes - 1), grp = threadIdx.x / kLineLanes;
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kLineThreads) k_fft_line2(const double2* __res
   const long long o = blockIdx.x / tiles;
   const long long i = (blockIdx.x % tiles) * kLineLanes + lane;
   const bool ok = i < n_inner;
-  for (int j = threadIdx.x; j < P / 2; j += kLineThreads) {
+  for (int j = threadIdx.x; j < P; j += kLineThreads) {
     double s, c;
     sincospi(-2.0 * j / P, &s, &c);
     tw[j] = make_double2(c, s);
@@ -335,13 +335,32 @@ __global__ void __launch_bounds__(kLineThreads) k_fft_line2(const double2* __res
   for (int j = grp; j < P; j += kLineGroups)
     sb[j * kLineLanes + lane] = (ok && j < nin) ? src[j * n_inner + i] : make_double2(0.0, 0.0);
   __syncthreads();
-  // DIF stages: span h = P/2 .. 1; butterfly (a, a + h), twiddle w^(r P / (2h))
-  for (int h = P >> 1, st = 1; h >= 1; h >>= 1, st <<= 1) {
+  // DIF radix-4 stages on groups of N = P, P/4, ... (span h = N/4; outputs
+  // q = 0..3 of each 4-point DFT to sub-block q, twiddled by W_N^(q r) =
+  // w^(q r P/N)), then one radix-2 stage when log2 P is odd
+  int N = P, logN = logP;
+  for (; N >= 4; N >>= 2, logN -= 2) {
+    const int h = N >> 2, st = 1 << (logP - logN);  // powers of two: no integer division
+    for (int b = grp; b < P / 4; b += kLineGroups) {
+      const int r = b & (h - 1), a = ((b - r) << 2) + r;
+      double2* x0 = sb + a * kLineLanes + lane;
+      const double2 a0 = x0[0], a1 = x0[h * kLineLanes], a2 = x0[2 * h * kLineLanes], a3 = x0[3 * h * kLineLanes];
+      const double2 b0 = make_double2(a0.x + a2.x, a0.y + a2.y), b1 = make_double2(a0.x - a2.x, a0.y - a2.y);
+      const double2 b2 = make_double2(a1.x + a3.x, a1.y + a3.y);
+      const double2 b3 = make_double2(a1.y - a3.y, a3.x - a1.x);  // -i (a1 - a3)
+      x0[0] = make_double2(b0.x + b2.x, b0.y + b2.y);
+      x0[h * kLineLanes] = cmul(make_double2(b1.x + b3.x, b1.y + b3.y), tw[r * st]);
+      x0[2 * h * kLineLanes] = cmul(make_double2(b0.x - b2.x, b0.y - b2.y), tw[2 * r * st]);
+      x0[3 * h * kLineLanes] = cmul(make_double2(b1.x - b3.x, b1.y - b3.y), tw[3 * r * st]);
+    }
+    __syncthreads();
+  }
+  if (N == 2) {
     for (int b = grp; b < P / 2; b += kLineGroups) {
-      const int r = b & (h - 1), a = ((b - r) << 1) + r;
-      const double2 u = sb[a * kLineLanes + lane], v = sb[(a + h) * kLineLanes + lane];
-      sb[a * kLineLanes + lane] = make_double2(u.x + v.x, u.y + v.y);
-      sb[(a + h) * kLineLanes + lane] = cmul(make_double2(u.x - v.x, u.y - v.y), tw[r * st]);
+      double2* x0 = sb + 2 * b * kLineLanes + lane;
+      const double2 u = x0[0], v = x0[kLineLanes];
+      x0[0] = make_double2(u.x + v.x, u.y + v.y);
+      x0[kLineLanes] = make_double2(u.x - v.x, u.y - v.y);
     }
     __syncthreads();
   }
@@ -349,7 +368,11 @@ __global__ void __launch_bounds__(kLineThreads) k_fft_line2(const double2* __res
   const double mult = (mode == 2 && ok && (i % NF) % Lu != 0) ? 2.0 : 1.0;
   for (int k = grp; k < P; k += kLineGroups) {
     if (!ok) continue;
-    const int rk = static_cast<int>(__brev(static_cast<unsigned>(k)) >> (32 - logP));
+    // storage position of output k: its mixed-radix digits (4, 4, ..., [2]),
+    // least significant first, each placing it in a sub-block of its stage
+    int rk = 0, rem = k, ls = logP;
+    for (; ls >= 2; ls -= 2, rem >>= 2) rk += (rem & 3) << (ls - 2);
+    if (ls == 1) rk += rem & 1;
     const double2 a = sb[rk * kLineLanes + lane];
     const long long dst = (o * P + k) * n_inner + i;
     if (mode == 0)
@@ -392,7 +415,7 @@ void launch_line(const double2* in, void* out, long long n_outer, int nin, int P
     while ((1 << logP) < P) ++logP;
     static std::atomic<unsigned long long> attr2{0};
     smem_opt_in(attr2, k_fft_line2, 200 * 1024);
-    k_fft_line2<<<grid, kLineThreads, sizeof(double2) * (static_cast<std::size_t>(P) * kLineLanes + P / 2), st>>>(
+    k_fft_line2<<<grid, kLineThreads, sizeof(double2) * (static_cast<std::size_t>(P) * kLineLanes + P), st>>>(
         in, out, nin, P, logP, n_inner, mode, D, NF, Lu, partial, scale);
     return;
   }
