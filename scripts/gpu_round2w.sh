@@ -1,0 +1,4 @@
+set -u
+D=gpurun_out/r02w; mkdir -p $D
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $D/smoke.log 2>&1; echo "smoke rc $?"; tail -1 $D/smoke.log
+timeout 3000 python -m pytest tests -q -m gpu --durations=12 > $D/pytest.log 2>&1; echo "pytest rc $?"; tail -18 $D/pytest.log
