@@ -27,6 +27,11 @@ roofline   : the dominant kernel (P2P), nominal 229 flop per multipole pair
              FP64 DFMA peak measured in-process (MEASURED_PEAKS.json has no
              FP64 entry); roofline_m2l against the measured DMMA peak;
              phase_rooflines: every phase against its own roofline.
+forces_e2e : energy + forces through ankh_plan_forces_v1 with host buffers.
+fft_engine : the same workload on the ANKH-FFT plan (PAPER Alg. 4-5,
+             order_equi = order_cheb), device-timed like `value`, with its
+             relative difference from the drop-in's e_total (a different
+             approximation of the same energy, not the drop-in).
 cpu_baseline / --impl reference : the reference itself (oracle/_ref, the
              unmodified reference sources built against oracle/shim), one full
              ankh::fmm_energy call per step on all host cores.
