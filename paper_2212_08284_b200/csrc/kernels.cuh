@@ -193,7 +193,7 @@ int launch_p2p(const double* part, const unsigned* leaf_off, const unsigned* lea
                double period, double xi, const P2PRadial& rad, int cap, int leaf_begin,
                int leaf_end, double* near_partial, unsigned long long* pair_count, DevResult* res,
                cudaStream_t st, const unsigned* list = nullptr, const unsigned* bounds = nullptr,
-               int list_grid = 0);
+               int list_grid = 0, int bspan = 1);
 int p2p_max_cap();
 void launch_periodic_gen(double* gen, int order, double box_radius, double xi, int p,
                          cudaStream_t st);
