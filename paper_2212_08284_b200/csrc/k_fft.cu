@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kNodeThreads) k_fft_leaf(const double* __restr
   const unsigned m = blockIdx.x;
   const int n = 1 << depth;
   const unsigned lex = (morton_compact3(m >> 2) * n + morton_compact3(m >> 1)) * n + morton_compact3(m);
+  ANKH_DASSERT(lex < static_cast<unsigned>(n * n * n) && Lu >= 2 && Lc >= 2);
   for (int e = tid; e < Kc; e += kNodeThreads) q[e] = exp_leaf[static_cast<std::size_t>(m) * KS + e];
   for (int j = tid; j < Pn; j += kNodeThreads) {
     double s, c;
@@ -326,6 +327,7 @@ __global__ void __launch_bounds__(kLineThreads) k_fft_line2(const double2* __res
   const long long o = blockIdx.x / tiles;
   const long long i = (blockIdx.x % tiles) * kLineLanes + lane;
   const bool ok = i < n_inner;
+  ANKH_DASSERT((P & (P - 1)) == 0 && (1 << logP) == P && nin <= P);
   for (int j = threadIdx.x; j < P; j += kLineThreads) {
     double s, c;
     sincospi(-2.0 * j / P, &s, &c);
