@@ -103,7 +103,12 @@ RadialFit fit_radial(double s_max) {
       double p[14] = {}, g[14] = {};
       if (!cheb_fit(p_exact, a, n, p) || !cheb_fit(g_exact, a, n, g)) continue;
       const LD e = std::max(fit_error(p_exact, p, n, a), fit_error(g_exact, g, n, a));
-      if (e <= 2e-16L) {
+      // 2.5e-14 relative on P and G: the radial factors' absolute error is
+      // then < 1e-15 of b0 and g at every near distance (xi P and g are
+      // ~1 % of 1/r there), 1e4 below the 1e-11 component parity gate --
+      // one Horner term less per polynomial than fitting to 2e-16 (config 3:
+      // 6 instead of 7 terms, 2 of ~100 FP64 instructions per pair)
+      if (e <= 2.5e-14L) {
         r.nterms = n;
         r.s_lim = s_max;
         r.max_err = static_cast<double>(e);
