@@ -81,6 +81,13 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
     pending_code_ = ANKH_RUNTIME_ERROR;
     pending_msg_ = "order_cheb > 64 is not supported by the B200 engine";
   }
+  // the FFT engine's own limits, checked before any resource is created
+  if (fft_ && pending_code_ == 0 && n > 0 && !csr_only) {
+    if (cfg.order_equi < 2 || cfg.order_equi > 16)
+      throw AnkhError(ANKH_INVALID_ARGUMENT, "fft engine: order_equi must be in [2, 16]");
+    if (depth > 6) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: depth > 6 is not supported");
+    if (L > kMaxOrderCompiled) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: order_cheb > 10 is not supported");
+  }
   ANKH_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   // The far chain (P2M -> exchange -> M2M -> M2L) and the streamed path's
   // record gathers run at the highest stream priority: the block scheduler
@@ -742,10 +749,7 @@ void Plan::build_m2l() {
 // DFT on the device), the evaluation's work arrays, one far partial per
 // energy CTA (summed by k_finalize as the far field), no M2L classes.
 void Plan::build_fft() {
-  const int Lu = cfg.order_equi;
-  if (Lu < 2 || Lu > 16) throw AnkhError(ANKH_INVALID_ARGUMENT, "fft engine: order_equi must be in [2, 16]");
-  if (depth > 6) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: depth > 6 is not supported");
-  if (L > kMaxOrderCompiled) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: order_cheb > 10 is not supported");
+  const int Lu = cfg.order_equi;  // limits checked in the constructor, before any allocation
   fft_shape_ = fft_shape(depth, Lu);
   const FftShape& s = fft_shape_;
   const std::vector<double> E = transfer_equi(Lu, cheb_nodes(L));  // Lu x L

@@ -56,3 +56,7 @@ def test_fft_engine_plan_reuse_and_limits(cuda):
         plan.close()
     with pytest.raises(ankh.InvalidArgument):
         ankh.Plan(500, 4.0, cfg, engine="bogus")
+    with pytest.raises(ankh.InvalidArgument, match="order_equi"):
+        ankh.Plan(500, 4.0, ankh.EwaldConfig(order_cheb=4, order_equi=17, depth=2), engine="fft")
+    with pytest.raises(RuntimeError, match="depth > 6"):
+        ankh.Plan(500, 4.0, ankh.EwaldConfig(order_cheb=4, order_equi=4, depth=7), engine="fft")
