@@ -88,6 +88,15 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
     if (depth > 6) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: depth > 6 is not supported");
     if (L > kMaxOrderCompiled) throw AnkhError(ANKH_RUNTIME_ERROR, "fft engine: order_cheb > 10 is not supported");
   }
+  try {
+    build_all(t0);
+  } catch (...) {
+    release();  // the destructor does not run for a constructor that throws
+    throw;
+  }
+}
+
+void Plan::build_all(std::chrono::steady_clock::time_point t0) {
   ANKH_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   // The far chain (P2M -> exchange -> M2M -> M2L) and the streamed path's
   // record gathers run at the highest stream priority: the block scheduler
@@ -151,7 +160,11 @@ Plan::Plan(std::size_t n_, double box_radius, const ankh_config_v1& cfg_, bool c
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-Plan::~Plan() {
+Plan::~Plan() { release(); }
+
+// Every resource the plan holds (also on a constructor that throws part way:
+// members not created yet are null)
+void Plan::release() noexcept {
   DeviceGuard on_device(device_, /*nothrow=*/true);
   for (cudaStream_t s : {stream_, last_stream_, side_stream_, copy_stream_, gather_stream_})
     if (s) cudaStreamSynchronize(s);
@@ -198,6 +211,7 @@ Plan::~Plan() {
     cudaStreamDestroy(side_stream_);
   }
   if (stream_) cudaStreamDestroy(stream_);
+  stream_ = nullptr;
 }
 
 // Plan buffers come from the device's stream-ordered pool, kept by the pool

