@@ -170,7 +170,7 @@ def test_radial_fit_is_roundoff_accurate(s_max, want_nt):
         for k in range(nt.value - 2, -1, -1):
             h = h * s + ld(coef[k])
         assert float(np.max(np.abs((h - ref) / ref))) < 2.6e-14
-    assert err.value < 2.5e-16
+    assert err.value < 2.6e-14
 
 
 def test_induced_dipole_solver_logic_on_a_linear_mock():
