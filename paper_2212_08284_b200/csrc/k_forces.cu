@@ -209,6 +209,197 @@ __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __rest
   }
 }
 
+// Forces only (no moment derivatives): the 13 lex-positive neighbours of the
+// energy's half shell (fmm.cpp:284-292) with Newton's third law -- the pair
+// energy depends on x_a - x_b - shift alone, so grad_b e = -grad_a e and every
+// neighbour pair is evaluated once (half k_p2p_force's pair count; own-leaf
+// pairs stay one-sided).  Deterministic, no atomics:
+//  * a tile of <= 32 targets sits on P = 2^ceil(log2 nt) adjacent lanes, the
+//    256 / P lane groups own disjoint contiguous blocks of the staged sources,
+//    and lane il walks its group's block rotated by il: at every step the
+//    lanes of a group touch distinct sources, a group never leaves its warp,
+//    and __syncwarp() orders the steps, so the source-side sums fb[] (shared)
+//    see one writer at a time in a fixed order;
+//  * the target-side sums are reduced over the groups in a fixed order (as
+//    in k_p2p_force) and belong to this CTA alone;
+//  * the source-side sums go to f_slot[direction][particle]: leaf B's slot d
+//    is written by the one CTA of leaf B - d, and k_force_out adds the 13
+//    slots in a fixed order (slots of absent or empty neighbours stay at the
+//    zero the launcher sets).
+template <int NT>
+__global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force_half(const double* __restrict__ part,
+                                                                  const unsigned* __restrict__ leaf_off,
+                                                                  const unsigned* __restrict__ leaf_mp, int depth,
+                                                                  int periodic, double period,
+                                                                  const __grid_constant__ P2PParams pp, int cap,
+                                                                  double* __restrict__ f_near,
+                                                                  double* __restrict__ f_slot,
+                                                                  std::size_t slot_stride) {
+  extern __shared__ __align__(16) double sm[];  // cap x kRec staged sources + 3 x cap source-side sums
+  __shared__ int seg_begin[14], seg_prefix[15], seg_dir[14], seg_n, any_mp;
+  __shared__ double seg_shift[14][3];
+  __shared__ double red[kForceTPB * 3];
+  double* const fb = sm + static_cast<std::size_t>(cap) * kRec;  // fb[d * cap + j]
+  const int tid = threadIdx.x;
+  const int n = 1 << depth;
+  const unsigned morton = blockIdx.x;
+  const int ax = static_cast<int>(compact3f(morton >> 2)), ay = static_cast<int>(compact3f(morton >> 1)),
+            az = static_cast<int>(compact3f(morton));
+  const unsigned leaf = static_cast<unsigned>((ax * n + ay) * n + az);
+  const int a_begin = static_cast<int>(leaf_off[leaf]);
+  const int na = static_cast<int>(leaf_off[leaf + 1]) - a_begin;
+  if (na == 0) return;
+  // segment table: lane 0 = own leaf, lanes 1..13 = the lex-positive
+  // directions (0,0,1), (0,1,-1..1), (1,-1..1,-1..1), as k_p2p orders them
+  if (tid < 32) {
+    const int lane = tid;
+    int bb = 0, nb = 0;
+    bool lmp = false;
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    if (lane == 0) {
+      bb = a_begin;
+      nb = na;
+      lmp = leaf_mp[leaf] != 0u;
+    } else if (lane <= 13) {
+      const int d = lane - 1;
+      const int ox = d < 4 ? 0 : 1;
+      const int oy = d == 0 ? 0 : (d < 4 ? 1 : (d - 4) / 3 - 1);
+      const int oz = d == 0 ? 1 : (d < 4 ? d - 2 : (d - 4) % 3 - 1);
+      const int ext[3] = {ax + ox, ay + oy, az + oz};
+      int in[3], img[3];
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (!periodic && (ext[k] < 0 || ext[k] >= n)) ok = false;
+        split_extf(ext[k], n, in[k], img[k]);
+      }
+      if (ok) {
+        const unsigned b = static_cast<unsigned>((in[0] * n + in[1]) * n + in[2]);
+        bb = static_cast<int>(leaf_off[b]);
+        nb = static_cast<int>(leaf_off[b + 1]) - bb;
+        lmp = nb > 0 && leaf_mp[b] != 0u;
+        sx = period * img[0];
+        sy = period * img[1];
+        sz = period * img[2];
+      }
+    }
+    const unsigned keep = __ballot_sync(0xffffffffu, lane == 0 || nb > 0);
+    const unsigned mps = __ballot_sync(0xffffffffu, lmp);
+    int incl = nb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if ((keep >> lane) & 1u) {
+      const int slot = __popc(keep & ((1u << lane) - 1u));
+      seg_begin[slot] = bb;
+      seg_dir[slot] = lane;
+      seg_shift[slot][0] = sx;
+      seg_shift[slot][1] = sy;
+      seg_shift[slot][2] = sz;
+      seg_prefix[slot + 1] = incl;
+    }
+    if (lane == 0) {
+      seg_prefix[0] = 0;
+      seg_n = __popc(keep);
+      any_mp = mps != 0u;
+    }
+  }
+  __syncthreads();
+  const int total = seg_prefix[seg_n];
+  const bool mp = any_mp != 0;
+  for (int c0 = 0; c0 < total; c0 += cap) {
+    const int cn = min(cap, total - c0);
+    ANKH_DASSERT(cn > 0 && cn <= cap);
+    __syncthreads();  // the previous chunk's sums are flushed
+    for (int q = tid; q < cn; q += kForceTPB) {
+      const int g = c0 + q;
+      int sgi = 0;
+      while (g >= seg_prefix[sgi + 1]) ++sgi;
+      const double2* r = reinterpret_cast<const double2*>(
+          part + static_cast<std::size_t>(seg_begin[sgi] + (g - seg_prefix[sgi])) * kRec);
+      double2* d = reinterpret_cast<double2*>(sm + static_cast<std::size_t>(q) * kRec);
+      double2 v0 = __ldg(r), v1 = __ldg(r + 1);
+      v0.x = v0.x + seg_shift[sgi][0];  // positions[iy] + shift (fmm.cpp:319)
+      v0.y = v0.y + seg_shift[sgi][1];
+      v1.x = v1.x + seg_shift[sgi][2];
+      d[0] = v0;
+      d[1] = v1;
+#pragma unroll
+      for (int k = 2; k < 7; ++k) d[k] = __ldg(r + k);
+      fb[q] = 0.0;
+      fb[cap + q] = 0.0;
+      fb[2 * cap + q] = 0.0;
+    }
+    __syncthreads();
+    const int own_end = na - c0;  // chunk entries below it are the own leaf's
+    for (int t0 = 0; t0 < na; t0 += 32) {
+      const int nt = min(32, na - t0);
+      int P = 1;
+      while (P < nt) P <<= 1;
+      const int S = kForceTPB / P;  // lane groups = source blocks
+      const int il = tid & (P - 1), grp = tid / P;
+      const bool active = il < nt;
+      const int m = (cn + S - 1) / S;  // sources per block
+      const int R = max(m, P);         // rotation length: distinct lanes, distinct sources
+      const int jb = grp * m;
+      const int jn = min(m, cn - jb);  // <= 0: an empty block
+      const Target tg = load_target(part + static_cast<std::size_t>(a_begin + t0 + (active ? il : 0)) * kRec);
+      const int self = t0 + il - c0;  // the target itself (own leaf = entries [0, na) of the list)
+      double grad[3] = {0.0, 0.0, 0.0};
+      int p = il;
+      for (int i = 0; i < R; ++i) {
+        const int j = jb + p;
+        if (active && p < jn && j != self) {
+          double gp[3] = {0.0, 0.0, 0.0};
+          const double* sb = sm + static_cast<std::size_t>(j) * kRec;
+          if (mp)
+            pair_grad_mp<NT>(tg, sb, pp, gp);
+          else
+            pair_grad_q<NT>(tg, sb, pp, gp);
+          grad[0] += gp[0];
+          grad[1] += gp[1];
+          grad[2] += gp[2];
+          if (j >= own_end) {  // F_b = -grad_b e = +grad_a e
+            fb[j] += gp[0];
+            fb[cap + j] += gp[1];
+            fb[2 * cap + j] += gp[2];
+          }
+        }
+        __syncwarp();
+        if (++p == R) p = 0;
+      }
+      // fixed-order sum over the target's groups; F = -grad
+#pragma unroll
+      for (int d = 0; d < 3; ++d) red[3 * tid + d] = grad[d];
+      __syncthreads();
+      if (tid < nt) {
+        double f[3] = {0.0, 0.0, 0.0};
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) f[d] += red[3 * (s * P + tid) + d];
+        double* out = f_near + 3 * static_cast<std::size_t>(a_begin + t0 + tid);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) out[d] = c0 == 0 ? -f[d] : out[d] - f[d];
+      }
+      __syncthreads();
+    }
+    // the neighbours' sums of this chunk, each (direction, particle) slot once
+    for (int q = tid; q < cn; q += kForceTPB) {
+      const int g = c0 + q;
+      if (g < na) continue;
+      int sgi = 0;
+      while (g >= seg_prefix[sgi + 1]) ++sgi;
+      const std::size_t b = static_cast<std::size_t>(seg_begin[sgi] + (g - seg_prefix[sgi]));
+      double* out = f_slot + static_cast<std::size_t>(seg_dir[sgi] - 1) * slot_stride + 3 * b;
+      out[0] = fb[q];
+      out[1] = fb[cap + q];
+      out[2] = fb[2 * cap + q];
+    }
+  }
+}
+
 // ------------------------------------------------- far field: dE/dM per cell
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -620,13 +811,24 @@ __global__ void k_dsrc_out(const double* __restrict__ d_near, const double* __re
 }
 
 // forces[idx[j]] = near[j] + far[j]: back to the caller's particle order
+// (+ the 13 source-side slots of k_p2p_force_half, added in direction order)
 __global__ void k_force_out(const double* __restrict__ f_near, const double* __restrict__ f_far,
+                            const double* __restrict__ f_slot, std::size_t slot_stride,
                             const unsigned* __restrict__ sorted, std::size_t n, double* __restrict__ out) {
   const std::size_t j = static_cast<std::size_t>(blockIdx.x) * 256 + threadIdx.x;
   if (j >= n) return;
   const std::size_t i = sorted[j];
+  double f[3] = {f_near[3 * j], f_near[3 * j + 1], f_near[3 * j + 2]};
+  if (f_slot) {
 #pragma unroll
-  for (int d = 0; d < 3; ++d) out[3 * i + d] = f_near[3 * j + d] + f_far[3 * j + d];
+    for (int k = 0; k < 13; ++k) {
+      const double* s = f_slot + k * slot_stride + 3 * j;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) f[d] += s[d];
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) out[3 * i + d] = f[d] + f_far[3 * j + d];
 }
 
 P2PParams make_force_params(double xi, const P2PRadial& rad) {
@@ -647,13 +849,19 @@ P2PParams make_force_params(double xi, const P2PRadial& rad) {
 template <int NT>
 void launch_force_near_t(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth,
                          int periodic, double period, const P2PParams& pp, int cap, double* f_near,
-                         double* d_near, cudaStream_t st) {
+                         double* d_near, double* f_slot, std::size_t slot_stride, cudaStream_t st) {
   const std::size_t smem = sizeof(double) * static_cast<std::size_t>(cap) * kRec;
   if (d_near) {
     static std::atomic<unsigned long long> attr{0};
     smem_opt_in(attr, k_p2p_force<NT, true>, sizeof(double) * force_max_cap() * kRec);
     k_p2p_force<NT, true><<<1u << (3 * depth), kForceTPB, smem, st>>>(part, leaf_off, leaf_mp, depth, periodic,
                                                                       period, pp, cap, f_near, d_near);
+  } else if (f_slot) {
+    static std::atomic<unsigned long long> attr{0};
+    smem_opt_in(attr, k_p2p_force_half<NT>, sizeof(double) * force_half_max_cap() * (kRec + 3));
+    k_p2p_force_half<NT><<<1u << (3 * depth), kForceTPB, sizeof(double) * static_cast<std::size_t>(cap) * (kRec + 3),
+                           st>>>(part, leaf_off, leaf_mp, depth, periodic, period, pp, cap, f_near, f_slot,
+                                 slot_stride);
   } else {
     static std::atomic<unsigned long long> attr{0};
     smem_opt_in(attr, k_p2p_force<NT, false>, sizeof(double) * force_max_cap() * kRec);
@@ -664,16 +872,19 @@ void launch_force_near_t(const double* part, const unsigned* leaf_off, const uns
 
 }  // namespace
 
-int force_max_cap() { return 960; }  // 960 x 112 B = 105 KB: two CTAs per SM
+int force_max_cap() { return 960; }       // 960 x 112 B = 105 KB: two CTAs per SM
+int force_half_max_cap() { return 768; }  // 768 x 136 B = 102 KB (+ 7 KB static): two CTAs per SM
 
 void launch_force_near(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth,
                        int periodic, double period, double xi, const P2PRadial& rad, int cap, double* f_near,
-                       cudaStream_t st, double* d_near) {
-  cap = cap < 64 ? 64 : (cap > force_max_cap() ? force_max_cap() : cap);
+                       cudaStream_t st, double* d_near, double* f_slot, std::size_t slot_stride) {
+  const int cap_max = (f_slot && !d_near) ? force_half_max_cap() : force_max_cap();
+  cap = cap < 64 ? 64 : (cap > cap_max ? cap_max : cap);
   if (d_near && cap < kForceTPB) cap = kForceTPB;  // the moment sums are staged in the source buffer
   const P2PParams pp = make_force_params(xi, rad);
-#define ANKH_F_NT(N) \
-  launch_force_near_t<N>(part, leaf_off, leaf_mp, depth, periodic, period, pp, cap, f_near, d_near, st)
+#define ANKH_F_NT(N)                                                                                         \
+  launch_force_near_t<N>(part, leaf_off, leaf_mp, depth, periodic, period, pp, cap, f_near, d_near, f_slot, \
+                         slot_stride, st)
   switch (rad.nterms) {
     case 6: ANKH_F_NT(6); break;
     case 7: ANKH_F_NT(7); break;
@@ -745,9 +956,10 @@ void launch_l2p(const double* part, const unsigned* leaf_off, int depth, int ord
 }
 
 void launch_force_out(const double* f_near, const double* f_far, const unsigned* sorted, std::size_t n,
-                      double* out, cudaStream_t st) {
+                      double* out, cudaStream_t st, const double* f_slot, std::size_t slot_stride) {
   if (n == 0) return;
-  k_force_out<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(f_near, f_far, sorted, n, out);
+  k_force_out<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(f_near, f_far, f_slot, slot_stride, sorted,
+                                                                      n, out);
 }
 
 void launch_dsrc_out(const double* d_near, const double* d_far, const double* part, const unsigned* sorted,

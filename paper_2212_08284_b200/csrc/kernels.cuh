@@ -280,10 +280,15 @@ void launch_halo_rows(double* exp, const long long* row_off, long long n_rows, i
 // class, first class index, count <= 32), op_of[level * 343 + offset slot] =
 // (first operator block, blocks) -- the periodic root term, L2L, L2P (f_far);
 // then forces[sorted[j]] = f_near[j] + f_far[j].
+// With f_slot (13 x slot_stride doubles, zeroed by the caller; forces only):
+// the half shell with Newton's third law, the neighbours' sums per direction
+// slot, added by launch_force_out.
 int force_max_cap();
+int force_half_max_cap();
 void launch_force_near(const double* part, const unsigned* leaf_off, const unsigned* leaf_mp, int depth,
                        int periodic, double period, double xi, const P2PRadial& rad, int cap, double* f_near,
-                       cudaStream_t st, double* d_near = nullptr);
+                       cudaStream_t st, double* d_near = nullptr, double* f_slot = nullptr,
+                       std::size_t slot_stride = 0);
 std::size_t m2l_local_smem(int Kp);
 void launch_m2l_local(const double* exp, double* loc, const long long* level_off, const double* factors,
                       const M2LOp* ops, const int2* op_of, const int4* tiles, int n_tiles, int Kp, int periodic,
@@ -299,7 +304,7 @@ void launch_l2p(const double* part, const unsigned* leaf_off, int depth, int ord
 void launch_dsrc_out(const double* d_near, const double* d_far, const double* part, const unsigned* sorted,
                      std::size_t n, double xi, int include_self, double* out, cudaStream_t st);
 void launch_force_out(const double* f_near, const double* f_far, const unsigned* sorted, std::size_t n,
-                      double* out, cudaStream_t st);
+                      double* out, cudaStream_t st, const double* f_slot = nullptr, std::size_t slot_stride = 0);
 // ANKH-FFT far field (k_fft.cu): the leaf-level
 // equispaced engine.  Arrays: X / tmp [cells][NF] double2, diag Pc^3 NF doubles.
 struct FftShape {

@@ -1777,6 +1777,10 @@ void Plan::force_setup() {
   const double per_leaf = static_cast<double>(n) / n_leaves;
   force_cap_ = static_cast<int>(std::ceil(27.0 * per_leaf * 1.3 / 32.0)) * 32;
   force_cap_ = std::max(256, std::min(force_cap_, force_max_cap()));
+  // forces without moment derivatives: the half shell (own leaf + 13 neighbours)
+  force_half_cap_ = static_cast<int>(std::ceil(14.0 * per_leaf * 1.25 / 32.0)) * 32;
+  force_half_cap_ = std::max(128, std::min(force_half_cap_, force_half_max_cap()));
+  force_half_ = std::getenv("ANKH_FORCE_FULL_STENCIL") == nullptr;
   ANKH_CUDA(cudaStreamSynchronize(stream_));
   force_init_ = true;
 }
@@ -1809,8 +1813,17 @@ void Plan::derivatives(const double* h_pos, const double* h_src, double* h_force
     d_dfar_ = static_cast<double*>(dalloc(nn * 10 * sizeof(double)));
     d_dout_ = static_cast<double*>(dalloc(nn * 10 * sizeof(double)));
   }
-  launch_force_near(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_, force_cap_,
-                    d_fnear_, st, dsrc ? d_dnear_ : nullptr);
+  // forces alone: every neighbour pair once (Newton's third law), the
+  // neighbours' sums in 13 direction slots that launch_force_out adds
+  const bool half = force_half_ && !dsrc;
+  const std::size_t slot_stride = std::max<std::size_t>(n, 1) * 3;
+  if (half) {
+    if (!d_fslot_) d_fslot_ = static_cast<double*>(dalloc(13 * slot_stride * sizeof(double)));
+    ANKH_CUDA(cudaMemsetAsync(d_fslot_, 0, 13 * slot_stride * sizeof(double), st));
+  }
+  launch_force_near(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
+                    half ? force_half_cap_ : force_cap_, d_fnear_, st, dsrc ? d_dnear_ : nullptr,
+                    half ? d_fslot_ : nullptr, slot_stride);
   launch_m2l_local(d_exp_, d_loc_, d_level_off_, d_factors_, d_ops_, d_op_of_, d_loc_tiles_, n_loc_tiles_, Kp,
                    periodic ? 1 : 0, st);
   if (periodic) launch_periodic_local(d_exp_, d_to_equi_, d_gen_, L, d_loc_, st);
@@ -1818,7 +1831,7 @@ void Plan::derivatives(const double* h_pos, const double* h_src, double* h_force
   launch_l2p(d_part_, d_off_, depth, L, rb, d_hd4_, d_loc_ + level_off_[depth], d_ffar_, st,
              dsrc ? d_dfar_ : nullptr);
   if (h_forces) {
-    launch_force_out(d_fnear_, d_ffar_, d_idx2_, n, d_fout_, st);
+    launch_force_out(d_fnear_, d_ffar_, d_idx2_, n, d_fout_, st, half ? d_fslot_ : nullptr, slot_stride);
     ANKH_CUDA(cudaMemcpyAsync(h_forces, d_fout_, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   }
   if (dsrc) {

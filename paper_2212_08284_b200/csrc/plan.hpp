@@ -339,7 +339,9 @@ class Plan {
   double* d_gen_ = nullptr;  // periodic generator (build_periodic)
   int2* d_op_of_ = nullptr;
   int4* d_loc_tiles_ = nullptr;
-  int n_loc_tiles_ = 0, force_cap_ = 960;
+  int n_loc_tiles_ = 0, force_cap_ = 960, force_half_cap_ = 576;
+  bool force_half_ = true;      // forces alone: half shell + direction slots (ANKH_FORCE_FULL_STENCIL unsets)
+  double* d_fslot_ = nullptr;   // 13 x n x 3 source-side sums of k_p2p_force_half
   // timing
   cudaEvent_t ev_[8] = {};
   bool evaluated_ = false;

@@ -117,6 +117,46 @@ def test_forces_at_scale_match_own_energy_differences(cuda, config):
     plan.close()
 
 
+HALF_CASES = {
+    # n, rb, seed, multipoles, config: sparse and dense leaves (several source
+    # chunks and target tiles per leaf), image shifts at depth 1, open boundary
+    "mp_E2_periodic": (400, 5.0, 21, True, dict(order_cheb=4, order_equi=4, depth=2, p=15)),
+    "mp_E1_periodic_dense": (3000, 4.0, 22, True, dict(order_cheb=3, order_equi=3, depth=1, p=15)),
+    "q_E1_open_dense": (2500, 4.0, 23, False, dict(order_cheb=3, order_equi=3, depth=1, p=0)),
+    "mp_E3_open": (2500, 8.0, 24, True, dict(order_cheb=3, order_equi=3, depth=3, p=0)),
+    "mp_E2_p2_uneven": (900, 6.0, 25, True, dict(order_cheb=3, order_equi=3, depth=2, p=2)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(HALF_CASES))
+def test_half_shell_forces_equal_full_stencil(cuda, name, monkeypatch):
+    """The forces-only near field (half shell + Newton's third law, direction
+    slots; k_p2p_force_half) against the full 27-leaf stencil kernel that the
+    derivative pass keeps: the same pair gradients, summed in another order."""
+    n, rb, seed, mp, kw = HALF_CASES[name]
+    pos, src = inputs.random_system(n, rb, seed=seed, multipoles=mp)
+    if "uneven" in name:  # most particles in one octant: leaf sizes from 0 to hundreds
+        pos[: n // 2] = pos[: n // 2] * 0.24 + 0.7 * rb
+    ec = ankh.EwaldConfig(**kw)
+    plan = ankh.Plan(n, rb, ec)
+    rep, f = plan.forces(pos, src)
+    rep_b, f_b = plan.forces(pos, src)
+    assert np.array_equal(f, f_b)
+    plan.close()
+    monkeypatch.setenv("ANKH_FORCE_FULL_STENCIL", "1")
+    plan2 = ankh.Plan(n, rb, ec)
+    rep2, f2 = plan2.forces(pos, src)
+    plan2.close()
+    assert rep.e_total == rep2.e_total
+    assert np.abs(f - f2).max() <= 2e-12 * np.abs(f2).max(), np.abs(f - f2).max() / np.abs(f2).max()
+    # and through the derivative pass (always the full stencil)
+    monkeypatch.delenv("ANKH_FORCE_FULL_STENCIL")
+    plan3 = ankh.Plan(n, rb, ec)
+    _, f3, _ = plan3.derivatives(pos, src)
+    plan3.close()
+    assert np.abs(f - f3).max() <= 2e-12 * np.abs(f3).max()
+
+
 # ---------------------------------------------------------------- moment gradient
 def _fd_moments(ref, pos, src, rb, kw, pairs, h):
     """Central differences of the reference energy in single stored moments:
