@@ -412,7 +412,23 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
 }
 
 constexpr int kLocWarps = 4;              // 8 targets per warp, 32 per CTA
-constexpr int kLocRows = 32;              // factor rows staged per pass
+// A/B knobs (make variants VAR_SRC=k_forces), k_m2l_local at config 3: rows 32
+// with 3 CTAs per SM asked for (160 registers) 7.32 ms; no minimum (162
+// registers) 7.65; rows 16 / 4 CTAs 7.44; rows 24 / 4 CTAs 11.0 (ranks of 32
+// take two passes); rows 16 / 5 CTAs (96 registers, spills) 13.8; two or four
+// GEMM 1 accumulator sets 9.0 / 10.7; 48 rows (2 CTAs) 16.1.  Tiles of one
+// boundary signature (one factor pass per offset instead of 1.12 on average)
+// add 14 % more tiles and gain nothing: the kernel is bound by the per-pass
+// latency chain (stage -> barrier -> GEMM 1 -> GEMM 2) at three CTAs per SM,
+// the DMMA pipe ~60 % active.
+#ifndef ANKH_LOC_ROWS
+#define ANKH_LOC_ROWS 32
+#endif
+#ifndef ANKH_LOC_MINB
+#define ANKH_LOC_MINB 3
+#endif
+#define ANKH_LOC_BOUNDS __launch_bounds__(kLocWarps * 32, ANKH_LOC_MINB)
+constexpr int kLocRows = ANKH_LOC_ROWS;   // factor rows staged per pass (multiple of 8)
 constexpr int kLocRowTiles = 16;          // Lambda rows per row group: 128
 
 // One CTA = up to 32 target cells of one parity class at one level (Morton
@@ -424,7 +440,7 @@ constexpr int kLocRowTiles = 16;          // Lambda rows per row group: 128
 // GEMM 1 takes the partners' expansion rows straight from global (L2) as B
 // fragments; V moves from the accumulator layout to GEMM 2's B layout by warp
 // shuffles; Lambda stays in registers for all offsets (no atomics).
-__global__ void __launch_bounds__(kLocWarps * 32) k_m2l_local(
+__global__ void ANKH_LOC_BOUNDS k_m2l_local(
     const double* __restrict__ exp, double* __restrict__ loc, const long long* __restrict__ level_off,
     const double* __restrict__ factors, const M2LOp* __restrict__ ops, const int2* __restrict__ op_of,
     const int4* __restrict__ tiles, int Kp, int periodic) {
