@@ -411,6 +411,38 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 
+// bulk (TMA 1-D) row copies completing on an mbarrier (ANKH_LOC_BULK variant)
+__device__ __forceinline__ unsigned loc_saddr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void loc_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(loc_saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void loc_mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(loc_saddr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void loc_mbar_wait(unsigned long long* b, unsigned parity) {
+  const unsigned a = loc_saddr(b);
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void loc_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          loc_saddr(dst)),
+      "l"(src), "r"(bytes), "r"(loc_saddr(bar))
+      : "memory");
+}
+
 constexpr int kLocWarps = 4;              // 8 targets per warp, 32 per CTA
 // A/B knobs (make variants VAR_SRC=k_forces), k_m2l_local at config 3: rows 32
 // with 3 CTAs per SM asked for (160 registers) 7.32 ms; no minimum (162
@@ -448,6 +480,16 @@ __global__ void ANKH_LOC_BOUNDS k_m2l_local(
   const int KS = Kp + 4;
   double* sX = sm;                   // kLocRows x KS
   double* sY = sX + kLocRows * KS;   // kLocRows x KS
+#ifdef ANKH_LOC_BULK
+  __shared__ unsigned long long bar_x, bar_y;
+  if (threadIdx.x == 0) {
+    loc_mbar_init(&bar_x, 1);
+    loc_mbar_init(&bar_y, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned bar_phase = 0;
+#endif
   const int4 tile = tiles[blockIdx.x];  // (level, cls, j0, count)
   const int level = tile.x, cls = tile.y, count = tile.w;
   const int n = 1 << level;
@@ -509,6 +551,25 @@ __global__ void ANKH_LOC_BOUNDS k_m2l_local(
               for (int r0 = 0; r0 < op.kp; r0 += kLocRows) {
                 const int rb = min(kLocRows, op.kp - r0);  // multiple of 8
                 __syncthreads();  // previous readers of sX / sY are done
+#ifdef ANKH_LOC_BULK
+                // one bulk copy per factor row (warp 0), X and Y on their own
+                // barriers: GEMM 1 starts when X is in, Y lands meanwhile
+                if (warp == 0) {
+                  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                  if (lane == 0) {
+                    loc_mbar_expect(&bar_x, static_cast<unsigned>(rb * Kp) * 8u);
+                    loc_mbar_expect(&bar_y, static_cast<unsigned>(rb * Kp) * 8u);
+                  }
+                  __syncwarp();
+                  for (int r = lane; r < rb; r += 32) {
+                    loc_bulk_g2s(sX + r * KS, Xg + static_cast<std::size_t>(r0 + r) * Kp,
+                                 static_cast<unsigned>(Kp) * 8u, &bar_x);
+                    loc_bulk_g2s(sY + r * KS, Yg + static_cast<std::size_t>(r0 + r) * Kp,
+                                 static_cast<unsigned>(Kp) * 8u, &bar_y);
+                  }
+                }
+                loc_mbar_wait(&bar_x, bar_phase);
+#else
                 for (int w = threadIdx.x; w < rb * (Kp / 2); w += kLocWarps * 32) {
                   const int r = w / (Kp / 2), c2 = 2 * (w - (Kp / 2) * (w / (Kp / 2)));
                   cp_async16(sX + r * KS + c2, Xg + static_cast<std::size_t>(r0 + r) * Kp + c2);
@@ -516,6 +577,7 @@ __global__ void ANKH_LOC_BOUNDS k_m2l_local(
                 }
                 asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
                 __syncthreads();
+#endif
                 // GEMM 1: V (rb x 8) = X (rb x Kp) . [M_p] (Kp x 8)
                 double v[kLocRows / 8][2];
 #pragma unroll
@@ -527,6 +589,10 @@ __global__ void ANKH_LOC_BOUNDS k_m2l_local(
                   for (int m = 0; m < kLocRows / 8; ++m)
                     if (m < rb8) dmma(v[m], sX[(8 * m + (lane >> 2)) * KS + 4 * ks + (lane & 3)], b);
                 }
+#ifdef ANKH_LOC_BULK
+                loc_mbar_wait(&bar_y, bar_phase);
+                bar_phase ^= 1u;
+#endif
                 // GEMM 2: Lambda (rows x 8) += Y^T (rows x rb) . V (rb x 8)
 #pragma unroll
                 for (int s = 0; s < kLocRows / 4; ++s) {

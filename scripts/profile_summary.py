@@ -123,7 +123,7 @@ def main():
     summary["kernels"] = kernels
     with open(os.path.join(dst, "summary.json"), "w") as f:
         json.dump(summary, f, indent=1)
-    p2p = [k for k in kernels if k["kernel"].startswith("k_p2p")]
+    p2p = [k for k in kernels if k["kernel"].startswith("k_p2p") and not k["kernel"].startswith("k_p2p_force")]
     if p2p:
         k = p2p[0]
         traffic = {"p2p": {"kernel": k["kernel"], "dram_bytes_per_launch":
