@@ -21,6 +21,8 @@
 //        138-203): dM_leaf/dx_a uses S^(n+1) = rad^-(n+1) H D^(n+1) T(local)
 //        for every term S^(n) of modified_charges (k_l2p).
 // The self energy does not depend on positions.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "pair.cuh"
 
@@ -448,7 +450,8 @@ constexpr int kLocWarps = 4;              // 8 targets per warp, 32 per CTA
 // with 3 CTAs per SM asked for (160 registers) 7.32 ms; no minimum (162
 // registers) 7.65; rows 16 / 4 CTAs 7.44; rows 24 / 4 CTAs 11.0 (ranks of 32
 // take two passes); rows 16 / 5 CTAs (96 registers, spills) 13.8; two or four
-// GEMM 1 accumulator sets 9.0 / 10.7; 48 rows (2 CTAs) 16.1.  Tiles of one
+// GEMM 1 accumulator sets 9.0 / 10.7; 48 rows (2 CTAs) 16.1; bulk row copies
+// on mbarriers (ANKH_LOC_BULK) 7.30 against 7.40 in the same run.  Tiles of one
 // boundary signature (one factor pass per offset instead of 1.12 on average)
 // add 14 % more tiles and gain nothing: the kernel is bound by the per-pass
 // latency chain (stage -> barrier -> GEMM 1 -> GEMM 2) at three CTAs per SM,
@@ -475,11 +478,13 @@ constexpr int kLocRowTiles = 16;          // Lambda rows per row group: 128
 __global__ void ANKH_LOC_BOUNDS k_m2l_local(
     const double* __restrict__ exp, double* __restrict__ loc, const long long* __restrict__ level_off,
     const double* __restrict__ factors, const M2LOp* __restrict__ ops, const int2* __restrict__ op_of,
-    const int4* __restrict__ tiles, int Kp, int periodic) {
+    const int4* __restrict__ tiles, int Kp, int periodic, int rows) {
   extern __shared__ __align__(16) double sm[];
   const int KS = Kp + 4;
-  double* sX = sm;                   // kLocRows x KS
-  double* sY = sX + kLocRows * KS;   // kLocRows x KS
+  // rows (<= kLocRows, a multiple of 8): factor rows staged per pass, fewer
+  // than kLocRows when the order's row length would not fit shared memory
+  double* sX = sm;               // rows x KS
+  double* sY = sX + rows * KS;   // rows x KS
 #ifdef ANKH_LOC_BULK
   __shared__ unsigned long long bar_x, bar_y;
   if (threadIdx.x == 0) {
@@ -548,8 +553,8 @@ __global__ void ANKH_LOC_BOUNDS k_m2l_local(
               const double* Rg = Lg + static_cast<std::size_t>(op.kp) * Kp;
               const double* Xg = pass == 0 ? Rg : Lg;
               const double* Yg = pass == 0 ? Lg : Rg;
-              for (int r0 = 0; r0 < op.kp; r0 += kLocRows) {
-                const int rb = min(kLocRows, op.kp - r0);  // multiple of 8
+              for (int r0 = 0; r0 < op.kp; r0 += rows) {
+                const int rb = min(rows, op.kp - r0);  // multiple of 8
                 __syncthreads();  // previous readers of sX / sY are done
 #ifdef ANKH_LOC_BULK
                 // one bulk copy per factor row (warp 0), X and Y on their own
@@ -979,7 +984,16 @@ void launch_force_near(const double* part, const unsigned* leaf_off, const unsig
 #undef ANKH_F_NT
 }
 
-std::size_t m2l_local_smem(int Kp) { return sizeof(double) * 2 * kLocRows * static_cast<std::size_t>(Kp + 4); }
+// factor rows staged per pass: kLocRows, or what the order's row length
+// leaves room for (orders 8..10: 24, 16, 8 rows)
+int m2l_local_rows(int Kp) {
+  const std::size_t row = sizeof(double) * 2 * static_cast<std::size_t>(Kp + 4);
+  const int fit = static_cast<int>((224 * 1024) / row) / 8 * 8;
+  return std::max(8, std::min(kLocRows, fit));
+}
+std::size_t m2l_local_smem(int Kp) {
+  return sizeof(double) * 2 * m2l_local_rows(Kp) * static_cast<std::size_t>(Kp + 4);
+}
 
 void launch_m2l_local(const double* exp, double* loc, const long long* level_off, const double* factors,
                       const M2LOp* ops, const int2* op_of, const int4* tiles, int n_tiles, int Kp, int periodic,
@@ -987,9 +1001,9 @@ void launch_m2l_local(const double* exp, double* loc, const long long* level_off
   if (n_tiles <= 0) return;
   const std::size_t smem = m2l_local_smem(Kp);
   static std::atomic<unsigned long long> attr{0};
-  smem_opt_in(attr, k_m2l_local, 227 * 1024);  // the device maximum: plans of any order
+  smem_opt_in(attr, k_m2l_local, 225 * 1024);  // the device maximum less the static part: plans of any order
   k_m2l_local<<<n_tiles, kLocWarps * 32, smem, st>>>(exp, loc, level_off, factors, ops, op_of, tiles, Kp,
-                                                     periodic);
+                                                     periodic, m2l_local_rows(Kp));
 }
 
 void launch_periodic_local(const double* root, const double* to_equi, const double* gen, int order,

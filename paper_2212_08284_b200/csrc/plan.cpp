@@ -1800,9 +1800,10 @@ void Plan::derivatives(const double* h_pos, const double* h_src, double* h_force
     result(out);  // raises the deferred error, if any
     return;
   }
-  ANKH_CUDA(cudaMemcpyAsync(d_pos_, h_pos, n * 3 * sizeof(double), cudaMemcpyHostToDevice, stream_));
-  ANKH_CUDA(cudaMemcpyAsync(d_src_, h_src, n * 10 * sizeof(double), cudaMemcpyHostToDevice, stream_));
-  enqueue(d_pos_, d_src_, stream_);  // energies, records, leaf CSR, expansions of every level
+  // energies, records, leaf CSR, expansions of every level: the energy call's
+  // own host path (large systems stream the inputs in chunks under the
+  // kernels; its side streams are joined on stream_ before the final sums)
+  enqueue_host(h_pos, h_src, stream_);
   force_setup();
   cudaStream_t st = stream_;
   ANKH_CUDA(cudaMemsetAsync(d_loc_, 0, level_off_[depth + 1] * sizeof(double), st));

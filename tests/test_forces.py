@@ -117,6 +117,29 @@ def test_forces_at_scale_match_own_energy_differences(cuda, config):
     plan.close()
 
 
+def test_forces_high_order_match_own_energy_differences(cuda):
+    """Order 8 (K = 512: the dE/dM kernel stages fewer factor rows per pass so
+    a pass fits shared memory; the factors come from the randomized
+    compression): forces against central differences of the engine's own
+    energy."""
+    n, rb = 300, 5.0
+    pos, src = inputs.random_system(n, rb, seed=31, multipoles=True)
+    ec = ankh.EwaldConfig(order_cheb=8, order_equi=8, depth=2, p=15)
+    plan = ankh.Plan(n, rb, ec)
+    rep, f = plan.forces(pos, src)
+    h = 1e-5
+    cand = _inside_leaf(pos, rb, 2, 50 * h)
+    idx = cand[np.linspace(0, len(cand) - 1, 2).astype(int)]
+    for i in idx:
+        for d in range(3):
+            p1, p2 = pos.copy(), pos.copy()
+            p1[i, d] += h
+            p2[i, d] -= h
+            fd = -(plan.energy(p1, src).e_total - plan.energy(p2, src).e_total) / (2 * h)
+            assert abs(f[i, d] - fd) <= 1e-7 * np.abs(f).max() + 2e-14 * abs(rep.e_total) / h, (i, d, f[i, d], fd)
+    plan.close()
+
+
 HALF_CASES = {
     # n, rb, seed, multipoles, config: sparse and dense leaves (several source
     # chunks and target tiles per leaf), image shifts at depth 1, open boundary
