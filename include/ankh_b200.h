@@ -100,7 +100,8 @@ int ankh_fmm_energy_v1(size_t n, const double* positions, const double* sources,
 /* Forces (the reference computes energies only):
  * forces[3 i + d] = -dE/dx_{i,d} of the same energy ankh_fmm_energy_v1
  * returns (moments held fixed in the lab frame) -- near field by the
- * gradient of pair_interaction over every leaf's 27-leaf stencil, far field
+ * gradient of pair_interaction (every neighbour pair of the energy's half
+ * shell once, Newton's third law; deterministic, no atomics), far field
  * by the adjoint (dE/dM per cell from the M2L factors, the periodic root
  * operator, L2L = M2M^T, L2P = differentiated P2M).  The report holds the
  * energies.  One GPU (a sharded plan raises ANKH_RUNTIME_ERROR). */

@@ -4,9 +4,12 @@
 // differentiate exactly the energy the reference defines (fmm.cpp:383-436):
 //
 //   near field  E_near = sum_pairs e(x_a - x_b - shift)   (fmm.cpp:278-327)
-//     -> k_p2p_force: per target particle, the gradient of pair_interaction
-//        (pair.cuh pair_grad_mp) over its own leaf and all 26 neighbours
-//        (full stencil: every thread owns its target's sum, deterministic).
+//     -> k_p2p_force_half (forces alone): the gradient of pair_interaction
+//        (pair.cuh pair_grad_mp) over the energy's half shell, every
+//        neighbour pair once (Newton's third law; source-side sums in 13
+//        direction slots, deterministic, no atomics);
+//     -> k_p2p_force (with the moment derivatives): per target particle over
+//        its own leaf and all 26 neighbours (every thread owns its target's sum).
 //   far field   E_far = sum_canonical (L_o M_t).(R_o M_s)  (fmm.cpp:238-276)
 //     -> Lambda_c = dE/dM_c for every cell (k_m2l_local, DMMA): for every
 //        partner p of c, L_o^T R_o M_p when (c, p) is the canonical instance,
@@ -56,8 +59,10 @@ __device__ __forceinline__ void split_extf(int ext, int n, int& in_box, int& ima
 constexpr int kForceTPB = 256;
 
 // kDsrc: also the derivative of the pair energies with respect to the
-// target's 10 moments (pair_dsrc) into d_near[10 j] (sorted order)
-template <int NT, bool kDsrc>
+// target's 10 moments (pair_dsrc) into d_near[10 j] (sorted order);
+// kGrad = false: the moment derivatives alone (a field evaluation of the
+// induced-dipole solve: no pair gradient, f_near untouched)
+template <int NT, bool kDsrc, bool kGrad = true>
 __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __restrict__ part,
                                                              const unsigned* __restrict__ leaf_off,
                                                              const unsigned* __restrict__ leaf_mp, int depth,
@@ -167,30 +172,32 @@ __global__ void __launch_bounds__(kForceTPB, 2) k_p2p_force(const double* __rest
       if (mp) {
         for (int j = sl; j < cn; j += S)
           if (j != skip) {
-            pair_grad_mp<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
+            if (kGrad) pair_grad_mp<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
             if (kDsrc) pair_dsrc<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, ds);
           }
       } else {
         for (int j = sl; j < cn; j += S)
           if (j != skip) {
-            pair_grad_q<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
+            if (kGrad) pair_grad_q<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, grad);
             if (kDsrc) pair_dsrc<NT>(tg, sm + static_cast<std::size_t>(j) * kRec, pp, ds);
           }
       }
     }
     // fixed-order sum over the target's slices; F = -grad
     __syncthreads();
+    if (kGrad) {
 #pragma unroll
-    for (int d = 0; d < 3; ++d) red[3 * tid + d] = grad[d];
-    __syncthreads();
-    if (tid < nt) {
-      double f[3] = {0.0, 0.0, 0.0};
-      for (int s = 0; s < S; ++s)
+      for (int d = 0; d < 3; ++d) red[3 * tid + d] = grad[d];
+      __syncthreads();
+      if (tid < nt) {
+        double f[3] = {0.0, 0.0, 0.0};
+        for (int s = 0; s < S; ++s)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) f[d] += red[3 * (s * nt + tid) + d];
-      double* out = f_near + 3 * static_cast<std::size_t>(a_begin + t0 + tid);
+          for (int d = 0; d < 3; ++d) f[d] += red[3 * (s * nt + tid) + d];
+        double* out = f_near + 3 * static_cast<std::size_t>(a_begin + t0 + tid);
 #pragma unroll
-      for (int d = 0; d < 3; ++d) out[d] = -f[d];
+        for (int d = 0; d < 3; ++d) out[d] = -f[d];
+      }
     }
     if (kDsrc) {  // the same fixed-order slice sum, staged in the (finished) source buffer
       ANKH_DASSERT(cap * kRec >= 10 * kForceTPB);
@@ -938,7 +945,12 @@ void launch_force_near_t(const double* part, const unsigned* leaf_off, const uns
                          int periodic, double period, const P2PParams& pp, int cap, double* f_near,
                          double* d_near, double* f_slot, std::size_t slot_stride, cudaStream_t st) {
   const std::size_t smem = sizeof(double) * static_cast<std::size_t>(cap) * kRec;
-  if (d_near) {
+  if (d_near && !f_near) {
+    static std::atomic<unsigned long long> attr{0};
+    smem_opt_in(attr, k_p2p_force<NT, true, false>, sizeof(double) * force_max_cap() * kRec);
+    k_p2p_force<NT, true, false><<<1u << (3 * depth), kForceTPB, smem, st>>>(
+        part, leaf_off, leaf_mp, depth, periodic, period, pp, cap, nullptr, d_near);
+  } else if (d_near) {
     static std::atomic<unsigned long long> attr{0};
     smem_opt_in(attr, k_p2p_force<NT, true>, sizeof(double) * force_max_cap() * kRec);
     k_p2p_force<NT, true><<<1u << (3 * depth), kForceTPB, smem, st>>>(part, leaf_off, leaf_mp, depth, periodic,

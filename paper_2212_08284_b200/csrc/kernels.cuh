@@ -280,7 +280,8 @@ void launch_halo_rows(double* exp, const long long* row_off, long long n_rows, i
 // class, first class index, count <= 32), op_of[level * 343 + offset slot] =
 // (first operator block, blocks) -- the periodic root term, L2L, L2P (f_far);
 // then forces[sorted[j]] = f_near[j] + f_far[j].
-// With f_slot (13 x slot_stride doubles, zeroed by the caller; forces only):
+// With d_near and f_near == nullptr: the moment derivatives alone (no pair
+// gradient).  With f_slot (13 x slot_stride doubles, zeroed by the caller; forces only):
 // the half shell with Newton's third law, the neighbours' sums per direction
 // slot, added by launch_force_out.
 int force_max_cap();

@@ -1823,7 +1823,8 @@ void Plan::derivatives(const double* h_pos, const double* h_src, double* h_force
     ANKH_CUDA(cudaMemsetAsync(d_fslot_, 0, 13 * slot_stride * sizeof(double), st));
   }
   launch_force_near(d_part_, d_off_, d_leaf_mp_, depth, periodic ? 1 : 0, 2.0 * rb, cfg.xi, radial_,
-                    half ? force_half_cap_ : force_cap_, d_fnear_, st, dsrc ? d_dnear_ : nullptr,
+                    half ? force_half_cap_ : force_cap_, (dsrc && !h_forces) ? nullptr : d_fnear_, st,
+                    dsrc ? d_dnear_ : nullptr,
                     half ? d_fslot_ : nullptr, slot_stride);
   launch_m2l_local(d_exp_, d_loc_, d_level_off_, d_factors_, d_ops_, d_op_of_, d_loc_tiles_, n_loc_tiles_, Kp,
                    periodic ? 1 : 0, st);

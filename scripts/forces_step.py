@@ -15,6 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--field", action="store_true", help="also time Plan.field (moment derivatives alone)")
     a = ap.parse_args()
     import numpy as np
 
@@ -31,6 +32,14 @@ def main():
     dt = (time.perf_counter() - t0) / max(1, a.reps)
     print(f"config {a.config}: energy + forces {dt * 1e3:.2f} ms per call (host buffers), e_total {rep.e_total:.17g}, "
           f"|F| max {np.abs(f).max():.6g}, sum F {f.sum(axis=0)}", flush=True)
+    if a.field:
+        plan.field(pos, src)
+        t0 = time.perf_counter()
+        for _ in range(max(1, a.reps)):
+            e = plan.field(pos, src)
+        dt = (time.perf_counter() - t0) / max(1, a.reps)
+        print(f"config {a.config}: field evaluation {dt * 1e3:.2f} ms per call (host buffers), |E| max {np.abs(e).max():.6g}",
+              flush=True)
     plan.close()
 
 

@@ -175,9 +175,12 @@ def test_half_shell_forces_equal_full_stencil(cuda, name, monkeypatch):
     # and through the derivative pass (always the full stencil)
     monkeypatch.delenv("ANKH_FORCE_FULL_STENCIL")
     plan3 = ankh.Plan(n, rb, ec)
-    _, f3, _ = plan3.derivatives(pos, src)
+    _, f3, ds3 = plan3.derivatives(pos, src)
+    # the moment derivatives alone (a field evaluation: no pair gradient in the near pass)
+    _, f4, ds4 = plan3.derivatives(pos, src, forces=False)
     plan3.close()
     assert np.abs(f - f3).max() <= 2e-12 * np.abs(f3).max()
+    assert f4 is None and np.abs(ds4 - ds3).max() <= 1e-13 * np.abs(ds3).max()
 
 
 # ---------------------------------------------------------------- moment gradient
