@@ -431,7 +431,7 @@ class Plan:
                                          512), err)
         return EnergyReport._from_c(rep), forces
 
-    def derivatives(self, positions, sources, forces: bool = True):
+    def derivatives(self, positions, sources, forces: bool = True, _dsrc_out=None):
         """Energy, forces F = -dE/dx (n x 3, or None with ``forces=False``) and
         the moment gradient dE/ds (n x 10, the stored moment layout: dE/dq is
         the potential, dE/dmu minus the field, dE/dTheta per stored component)
@@ -442,7 +442,7 @@ class Plan:
         rep = _Report()
         err = ctypes.create_string_buffer(512)
         f = np.zeros((pos.shape[0], 3), dtype=np.float64) if forces else None
-        dsrc = np.zeros((pos.shape[0], 10), dtype=np.float64)
+        dsrc = _dsrc_out if _dsrc_out is not None else np.zeros((pos.shape[0], 10), dtype=np.float64)
         _check(lib().ankh_plan_derivatives_v1(self._h, _ptr(pos), _ptr(src), _ptr(f) if f is not None else None,
                                               _ptr(dsrc), ctypes.byref(rep), err, 512), err)
         return EnergyReport._from_c(rep), f, dsrc
@@ -450,7 +450,13 @@ class Plan:
     def field(self, positions, sources) -> np.ndarray:
         """The electric field at every particle, -dE/dmu (n x 3): the quantity
         an induced-dipole solve iterates on (``induced_dipoles``)."""
-        return -self.derivatives(positions, sources, forces=False)[2][:, 1:4]
+        # the n x 10 result buffer is kept between calls (the induced-dipole
+        # solve evaluates a field per iteration; a fresh 80 B / particle array
+        # would be page-faulted in every time); the caller gets a copy
+        buf = getattr(self, "_field_buf", None)
+        if buf is None or buf.shape[0] != np.shape(positions)[0]:
+            buf = self._field_buf = np.empty((np.shape(positions)[0], 10), dtype=np.float64)
+        return -self.derivatives(positions, sources, forces=False, _dsrc_out=buf)[2][:, 1:4]
 
     def set_positions(self, positions) -> None:
         """Bind host positions (copied, validated, binned and sorted once) for
