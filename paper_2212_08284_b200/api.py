@@ -419,14 +419,24 @@ class Plan:
         _check(lib().ankh_plan_energy_v1(self._h, _ptr(pos), _ptr(src), ctypes.byref(rep), err, 512), err)
         return EnergyReport._from_c(rep)
 
-    def forces(self, positions, sources):
-        """Energy and forces F = -dE/dx (n x 3) of host arrays: (EnergyReport, forces)."""
+    def forces(self, positions, sources, out=None):
+        """Energy and forces F = -dE/dx (n x 3) of host arrays: (EnergyReport, forces).
+        ``out``: a C-contiguous float64 (n, 3) array to receive the forces (a
+        page-locked one is filled at the full copy rate; a fresh pageable
+        array per call costs its page faults)."""
         pos = _as_host(positions, 3)
         src = _as_host(sources, 10)
         self._check_n(pos, src)
         rep = _Report()
         err = ctypes.create_string_buffer(512)
-        forces = np.zeros((pos.shape[0], 3), dtype=np.float64)
+        if out is None:
+            forces = np.zeros((pos.shape[0], 3), dtype=np.float64)
+        else:
+            forces = out
+            if (not isinstance(forces, np.ndarray) or forces.dtype != np.float64 or
+                    forces.shape != (pos.shape[0], 3) or not forces.flags.c_contiguous or
+                    not forces.flags.writeable):
+                raise ValueError("forces: out must be a writable C-contiguous float64 array of shape (n, 3)")
         _check(lib().ankh_plan_forces_v1(self._h, _ptr(pos), _ptr(src), _ptr(forces), ctypes.byref(rep), err,
                                          512), err)
         return EnergyReport._from_c(rep), forces

@@ -204,3 +204,25 @@ def test_induced_dipole_solver_logic_on_a_linear_mock():
     assert Mock.calls == sol.iterations + 3  # F0, the first product, one per iteration, the check
     with pytest.raises(ankh.InvalidArgument):
         ankh.induced_dipoles(Mock(), pos, src, 0.0)
+
+
+def test_forces_out_buffer_is_validated():
+    """Plan.forces(out=...) rejects a buffer of the wrong shape, dtype or
+    layout before any library call (host logic; no GPU needed)."""
+    import numpy as np
+
+    from paper_2212_08284_b200 import api
+
+    class P(api.Plan):
+        def __init__(self):  # no library handle: the checks come first
+            self.n = 4
+            self._h = None
+
+        def close(self):
+            pass
+
+    p = P()
+    pos, src = np.zeros((4, 3)), np.zeros((4, 10))
+    for bad in (np.zeros((3, 3)), np.zeros((4, 3), dtype=np.float32), np.zeros((3, 4)).T, [[0.0] * 3] * 4):
+        with pytest.raises(ValueError):
+            p.forces(pos, src, out=bad)
