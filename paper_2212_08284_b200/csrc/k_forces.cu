@@ -458,7 +458,9 @@ constexpr int kLocWarps = 4;              // 8 targets per warp, 32 per CTA
 // registers) 7.65; rows 16 / 4 CTAs 7.44; rows 24 / 4 CTAs 11.0 (ranks of 32
 // take two passes); rows 16 / 5 CTAs (96 registers, spills) 13.8; two or four
 // GEMM 1 accumulator sets 9.0 / 10.7; 48 rows (2 CTAs) 16.1; bulk row copies
-// on mbarriers (ANKH_LOC_BULK) 7.30 against 7.40 in the same run.  Tiles of one
+// on mbarriers (ANKH_LOC_BULK) 7.30 against 7.40 in the same run; GEMM 1's
+// partner rows as batches of eight 16-B loads per lane (with 16-B A fragments)
+// 7.59 against 7.41.  Tiles of one
 // boundary signature (one factor pass per offset instead of 1.12 on average)
 // add 14 % more tiles and gain nothing: the kernel is bound by the per-pass
 // latency chain (stage -> barrier -> GEMM 1 -> GEMM 2) at three CTAs per SM,
