@@ -1,6 +1,6 @@
 # closing check of the final tree: full GPU suite, smoke, the bench lines
 set -u
-O=gpurun_out/r02am; mkdir -p $O
+O=gpurun_out/r02aq; mkdir -p $O
 timeout 1800 python -m pytest tests -q -m gpu 2>&1 | tail -6 > $O/pytest_gpu.txt; tail -3 $O/pytest_gpu.txt
 python -c "import __graft_entry__ as g; g.smoke()" >> $O/pytest_gpu.txt 2>&1; tail -1 $O/pytest_gpu.txt
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; tail -c 400 $O/bench.json
